@@ -1,0 +1,449 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 MSV/SSV filter scan (BASELINE.json metric: MSV/SSV
+GCUPS, device-timed, vs model length).
+
+Default workload = BASELINE.json configs[1]: SSV with synthetic models
+M = 48 / 400 / 1000 over 1M Swiss-Prot-like synthetic sequences per GPU
+(synth::lognormal_records(1e6, 290, 0.65, 2), seed 0x5EED; models
+synth::random_profile(seed 7000+M)), weak scaling: N GPUs scan N x 1M
+sequences, sharded by residue count, raw/pass gathered to rank 0 over NCCL.
+One step = the three SSV scans over the resident database (every cell
+computed; no early exit).  GCUPS = real residues x M / device seconds.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--workload c2|c1|c3|c4|sweep] [--variant auto|dpx16|fp16|swar8]
+
+N>1: launched by torch.distributed.run, one rank per GPU (nccl).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+CELLS_PER_CLK_PER_SM = 64  # packed-integer-SIMD roofline
+
+WORKLOADS = {
+    # name: (description, alg, models, nseq per GPU, generator)
+    "c2": ("SSV, synthetic models M=48/400/1000 vs 1M Swiss-Prot-like synthetic sequences per GPU",
+           "ssv", (48, 400, 1000), 1_000_000, ("lognormal", 290.0, 0.65, 2)),
+    "c1": ("MSV, M=200 vs 10k random sequences (mean ~350 aa)",
+           "msv", (200,), 10_000, ("uniform", 50, 650)),
+    "c3": ("MSV, M=2405 vs 1M Swiss-Prot-like synthetic sequences per GPU",
+           "msv", (2405,), 1_000_000, ("lognormal", 290.0, 0.65, 2)),
+    "c4": ("MSV+SSV, M=200 vs env_nr-like synthetic sequences (lognormal median 170, sigma 0.55)",
+           "both", (200,), 6_250_000, ("lognormal", 170.0, 0.55, 2)),
+    "sweep": ("MSV+SSV, M=48..2405 sweep vs 1M Swiss-Prot-like synthetic sequences per GPU",
+              "both", (48, 100, 200, 400, 800, 1000, 1500, 2000, 2405), 1_000_000,
+              ("lognormal", 290.0, 0.65, 2)),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def make_db(P, gen, nseq, seed=0x5EED):
+    rng = P.Rng(seed)
+    if gen[0] == "lognormal":
+        return rng.lognormal_records(nseq, gen[1], gen[2], gen[3])
+    return rng.random_records(nseq, gen[1], gen[2])
+
+
+def make_models(P, models, q):
+    out = []
+    for m in models:
+        hmm = P.Rng(7000 + m).random_profile(m)
+        out.append((hmm, P.quantize_emissions(hmm, q)))
+    return out
+
+
+def algs_of(wl_alg):
+    return {"ssv": ["ssv"], "msv": ["msv"], "both": ["msv", "ssv"]}[wl_alg]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.rows, self.proc, self.gpu = [], None, gpu_index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for i, n in enumerate(names):
+                    if r[5 + i].lower().startswith("active"):
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                pass
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_reference_gcups(P, db, models, algs, q, sample_n, reps=1):
+    """The reference CPU filter (oracle/_ref: lanehmm::scan_database with the
+    reference geometry policy, all host threads), or the oracle port when the
+    reference library is absent, on a fixed-stride sample of the workload."""
+    import oracle
+    stride = max(1, db.count // sample_n)
+    idx = np.arange(0, db.count, stride)[:sample_n]
+    sample = db.subset(idx)
+    cores = os.cpu_count() or 1
+    oq = oracle.QuantParams(q.scale, q.base, q.dbias, q.tec, q.tjb)
+    try:
+        ref = oracle.Reference()
+        kind = "reference"
+    except FileNotFoundError:
+        ref, kind = None, "port"
+        ora = oracle.Oracle()
+    best = None
+    for _ in range(reps):
+        cells, secs = 0, 0.0
+        for hmm, costs in models:
+            for a in algs:
+                alg = 0 if a == "msv" else 1
+                if ref is not None:
+                    _, s, _ = ref.scan_database(alg, hmm.match_scores.reshape(-1), hmm.lambda_,
+                                                hmm.tau, costs.bytes, oq, sample.residues,
+                                                sample.offsets, cores)
+                else:
+                    t0 = time.perf_counter()
+                    ora.scan_flat(alg, costs.bytes, sample.residues, sample.offsets, oq, cores)
+                    s = time.perf_counter() - t0
+                secs += s
+                cells += sample.total_residues() * hmm.length
+        g = cells / secs / 1e9
+        best = g if best is None else max(best, g)
+    desc = (f"fixed-stride sample of {sample.count} of {db.count} sequences "
+            f"({sample.total_residues()} residues), models M={[h.length for h, _ in models]}, "
+            f"{'+'.join(algs)}; lanehmm::scan_database with reference geometry, "
+            f"{cores} threads, host CPU '{cpu_model()}'" if kind == "reference" else
+            f"fixed-stride sample of {sample.count} sequences, C oracle port on {cores} threads")
+    return {"value": round(best, 3), "unit": "GCUPS", "cores": cores, "kind": kind,
+            "sample": desc}
+
+
+def run_reference(args, wl):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import paper_1707_09683_b200 as P  # generators only (same streams as synth::*)
+    desc, wl_alg, models_m, nseq, gen = WORKLOADS[args.workload]
+    q = P.QuantParams()
+    db = make_db(P, gen, nseq * world)
+    models = make_models(P, models_m, q)
+    algs = algs_of(wl_alg)
+    sample_n = args.ref_sample
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_gcups(P, db, models, algs, q, sample_n)
+        if i >= args.warmup:
+            vals.append(r["value"])
+    v = statistics.median(vals) if vals else r["value"]
+    cfg = {"workload": desc, "models": list(models_m), "algorithms": algs,
+           "sequences": int(db.count), "residues": int(db.total_residues()),
+           "data": "synthetic (lanehmm synth:: streams)"}
+    line = {"metric": "MSV/SSV GCUPS (device-timed) vs model length", "value": v, "unit": "GCUPS",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "impl": "reference",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic", "config": cfg,
+            "cpu_baseline": {**r, "value": v},
+            "e2e": {"value": v, "unit": "GCUPS", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--variant", default="auto", choices=["auto", "dpx16", "fp16", "swar8"])
+    ap.add_argument("--nseq", type=int, default=0, help="override sequences per GPU")
+    ap.add_argument("--ref-sample", type=int, default=20000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--lanes", type=int, default=0)
+    ap.add_argument("--rows", type=int, default=0)
+    args = ap.parse_args()
+    if args.nseq:
+        w = list(WORKLOADS[args.workload])
+        w[3] = args.nseq
+        WORKLOADS[args.workload] = tuple(w)
+    if args.impl == "reference":
+        return run_reference(args, None)
+
+    import torch
+    import paper_1707_09683_b200 as P
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        log(f"note: WORLD_SIZE={world} but --gpus={args.gpus}; using WORLD_SIZE")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    desc, wl_alg, models_m, nseq, gen = WORKLOADS[args.workload]
+    variant = {"auto": P.Variant.Auto, "dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16,
+               "swar8": P.Variant.Swar8}[args.variant]
+    q = P.QuantParams()
+    algs = algs_of(wl_alg)
+    threshold = 0.022
+
+    t0 = time.perf_counter()
+    db = make_db(P, gen, nseq * world)
+    models = make_models(P, models_m, q)
+    t_gen = time.perf_counter() - t0
+
+    stream = torch.cuda.current_stream()
+    s = P.Scanner(local)
+    s.set_stream(stream.cuda_stream)
+    t0 = time.perf_counter()
+    n_local = s.set_database(db, rank, world)
+    t_pack = time.perf_counter() - t0
+    gidx = torch.from_numpy(s.shard_indices().astype(np.int64)).cuda()
+    dbstats = s.database_stats()
+    pids = [s.add_profile(c, q, h.lambda_, h.tau) for h, c in models]
+    info = s.device_info()
+    scans = [(pid, hmm.length, a) for pid, (hmm, _) in zip(pids, models) for a in algs]
+    outs = {k: (torch.empty(max(n_local, 1), dtype=torch.uint8, device="cuda"),
+                torch.empty(max(n_local, 1), dtype=torch.uint8, device="cuda"))
+            for k in range(len(scans))}
+
+    def opt_for(a):
+        return P.ScanOptions(alg=P.Algorithm.Msv if a == "msv" else P.Algorithm.Ssv,
+                             variant=variant, lanes=args.lanes, rows=args.rows,
+                             threshold=threshold)
+
+    per_launch = {k: [] for k in range(len(scans))}
+    geo = {}
+
+    def step(record):
+        launches = 0
+        for k, (pid, m, a) in enumerate(scans):
+            s.select_profile(pid)
+            st = s.scan_device(opt_for(a), outs[k][0].data_ptr(), outs[k][1].data_ptr())
+            launches += st["launches"]
+            geo[k] = (st["lanes"], st["rows"], st["variant"], st["grid"], st["smem_bytes"])
+            if record:
+                per_launch[k].append(st["device_ms"])
+        return launches
+
+    def gather_results():
+        """Per-sequence raw + pass bytes of every scan to rank 0 (NCCL gather)."""
+        if world == 1:
+            return
+        counts = torch.tensor([n_local], device="cuda")
+        allc = [torch.zeros_like(counts) for _ in range(world)]
+        dist.all_gather(allc, counts)
+        mx = int(max(int(c) for c in allc))
+        for k in range(len(scans)):
+            buf = torch.zeros(2, mx, dtype=torch.uint8, device="cuda")
+            buf[0, :n_local] = outs[k][0][:n_local]
+            buf[1, :n_local] = outs[k][1][:n_local]
+            glist = [torch.zeros_like(buf) for _ in range(world)] if rank == 0 else None
+            dist.gather(buf, glist, dst=0)
+
+    for _ in range(args.warmup):
+        step(False)
+        gather_results()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            launches += step(True)
+            gather_results()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    cells_local = sum(dbstats["residues"] * m for _, m, _ in scans) * args.steps
+    cells_t = torch.tensor([float(cells_local)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(cells_t, op=dist.ReduceOp.SUM)
+    ms_max = float(ms_t.item())
+    total_cells = float(cells_t.item())
+    gcups = total_cells / (ms_max * 1e-3) / 1e9
+
+    # ---- end to end through the C ABI with host buffers --------------------
+    e2e = None
+    if not args.no_e2e:
+        def e2e_step():
+            s.upload_database()  # H2D of the packed (pinned) database
+            d2h = 0
+            for k, (pid, m, a) in enumerate(scans):
+                s.select_profile(pid)
+                rep = s.scan(opt_for(a))  # kernel + D2H of raw and pass bytes
+                d2h += 2 * int(rep.raw.size)
+            return d2h
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        d2h = 0
+        for _ in range(args.steps):
+            d2h = e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        h2d = dbstats["packed_bytes"] + 16 * dbstats["tiles"] * 32
+        e2e = {"value": round(total_cells / (float(ems.item()) * 1e-3) / 1e9, 3), "unit": "GCUPS",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "path": "C ABI lhmm_upload_database + lhmm_scan (host outputs) per model"}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+
+    peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = info["sm_count"]
+    peak_gcups = n_sm * sm_max * 1e6 * CELLS_PER_CLK_PER_SM / 1e9
+    # dominant kernel: the scan with the largest share of the step
+    dom = max(per_launch, key=lambda k: sum(per_launch[k]))
+    dom_ms = statistics.mean(per_launch[dom])
+    _, dom_m, dom_a = scans[dom]
+    dom_cells = dbstats["residues"] * dom_m
+    achieved = dom_cells / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    if os.path.exists(TRAFFIC_PATH):
+        tr = json.load(open(TRAFFIC_PATH))
+        traffic = tr.get(f"{args.workload}:{dom_a}:M{dom_m}")
+    hbm_gbs = float(peaks.get("hbm_gbs", 6545.9))
+    hbm_achieved = (dbstats["packed_bytes"] + 9 * n_local) / (dom_ms * 1e-3) / 1e9
+    share = sum(per_launch[dom]) / ms_max if ms_max else None
+    clocks = clk.summary()
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_gcups(P, db, models, algs, q, args.ref_sample)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "error": str(e)}
+    per_scan = []
+    for k, (pid, m, a) in enumerate(scans):
+        t = statistics.mean(per_launch[k])
+        L, H, v, grid, smem = geo[k]
+        per_scan.append({"alg": a, "M": m, "ms": round(t, 4),
+                         "gcups": round(dbstats["residues"] * m / (t * 1e-3) / 1e9, 1),
+                         "lanes": L, "rows": H, "variant": ["auto", "dpx16", "fp16", "swar8"][v],
+                         "grid": grid, "smem_bytes": smem})
+    line = {
+        "metric": "MSV/SSV GCUPS (device-timed) vs model length",
+        "value": round(gcups, 2), "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": desc, "models": list(models_m), "algorithms": algs,
+                   "sequences": int(db.count), "residues": int(db.total_residues()),
+                   "threshold": threshold, "quant": "QuantParams{3.0,195,3,3,3}",
+                   "parallelism": f"shard{world} by residue count, raw+pass gathered to rank 0",
+                   "l2": "inputs larger than L2 (packed database "
+                         f"{dbstats['packed_bytes'] / 1e6:.0f} MB per GPU > 126 MB)",
+                   "early_exit": False},
+        "e2e": e2e,
+        "gpu_launches": launches * world,
+        "roofline": {"bound": "int-simd", "achieved": round(achieved, 1),
+                     "peak": round(peak_gcups, 1), "unit": "GCUPS",
+                     "frac": round(achieved / peak_gcups, 4), "traffic": traffic,
+                     "kernel": f"{dom_a} M={dom_m}", "kernel_share_of_step": share,
+                     "peak_basis": f"{n_sm} SMs x {sm_max:.0f} MHz x 64 cells/clk/SM "
+                                   "(64 INT32 lane-ops/clk/SM x 4 packed u8 cells / 4 ops per cell)",
+                     "hbm": {"bound": "hbm", "achieved": round(hbm_achieved, 1),
+                             "peak": hbm_gbs, "unit": "GB/s",
+                             "frac": round(hbm_achieved / hbm_gbs, 4)}},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "scans": per_scan,
+        "setup": {"generate_s": round(t_gen, 2), "pack_upload_s": round(t_pack, 2),
+                  "packed_bytes": dbstats["packed_bytes"], "padded_cells": dbstats["padded_cells"],
+                  "tiles": dbstats["tiles"]},
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,202 @@
+/*
+ * lhmm_b200.h -- C ABI of the B200-native MSV/SSV filter scan.
+ *
+ * This is the drop-in boundary for the reference's hot path (lanehmm, the
+ * CPU implementation of arxiv 1707.09683 CUDAMPF++).  Every entry point is
+ * plain C: pointers, sizes and PODs, int status codes, no exceptions and no
+ * torch / STL types.  Host code (the C++ engine.hpp shim, the Python mirror
+ * in paper_1707_09683_b200/lanehmm.py, or a ctypes/cffi binding) calls it;
+ * behind it sit hand-written sm_100a kernels.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   lhmm_quantize_emissions  <- quantize_emissions      src/profile.cpp:144-165, include/lanehmm/profile.hpp:71
+ *   lhmm_move_cost           <- oracle::move_cost / engine_move_cost  src/oracle.cpp:28-35, src/engine.cpp:28-35
+ *   lhmm_sequence_base       <- engine_sequence_base    src/engine.cpp:38-41, include/lanehmm/engine.hpp:85
+ *   lhmm_finalize_hit        <- finalize_hit            src/engine.cpp:59-81, include/lanehmm/engine.hpp:79-80
+ *   lhmm_select_geometry     <- lane_count + select_geometry  src/select.cpp:16-48 (retuned for B200)
+ *   lhmm_set_profile         <- build_striped (device tables)   src/profile.cpp:167-208
+ *   lhmm_set_database        <- pack_blocks (length-binned tiles) src/seqdb.cpp:109-188
+ *   lhmm_scan / lhmm_scan_device
+ *                            <- scan_database / scan_block / scan_sequences_s1
+ *                               src/engine.cpp:488-594, include/lanehmm/engine.hpp:90-101
+ *   lhmm_filter_pipeline     <- filter_pipeline         src/engine.cpp:596-657, include/lanehmm/engine.hpp:130-132
+ *   lhmm_rng_* / lhmm_synth_* <- synth::*               src/synth.cpp:8-81, include/lanehmm/synth.hpp
+ *
+ * Error convention: every function returns LHMM_OK (0) or a status; the
+ * message of the last failure on the calling thread is lhmm_last_error().
+ * LHMM_ERR_CONTRACT corresponds to the reference's ContractError and
+ * LHMM_ERR_DATA to DataError (include/lanehmm/errors.hpp:10-32).
+ *
+ * Threading: a context is bound to one device and one stream and is not
+ * thread-safe; separate contexts are independent.
+ */
+#ifndef LHMM_B200_H
+#define LHMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LHMM_ABI_VERSION 1
+
+enum lhmm_status {
+    LHMM_OK = 0,
+    LHMM_ERR_CONTRACT = 1, /* caller broke a precondition (ContractError) */
+    LHMM_ERR_DATA = 2,     /* malformed data (DataError) */
+    LHMM_ERR_CUDA = 3,     /* CUDA runtime / launch failure */
+    LHMM_ERR_NOMEM = 4     /* host or device allocation failed */
+};
+
+enum lhmm_alg { LHMM_MSV = 0, LHMM_SSV = 1 };
+
+/* Arithmetic variant of the DP kernel.  All are bit-exact. */
+enum lhmm_variant {
+    LHMM_VARIANT_AUTO = 0,  /* per (alg, M) choice from measurement */
+    LHMM_VARIANT_DPX16 = 1, /* u16x2 lanes, native VIADDMNMX/VIMNMX (ALU pipe) */
+    LHMM_VARIANT_FP16 = 2,  /* f16x2 saturating adds on the FMA pipe */
+    LHMM_VARIANT_SWAR8 = 3  /* u8x4 __vaddus4/__vsubus4/__vmaxu4 (paper tier 5) */
+};
+
+/* Byte-space constants; mirror of lanehmm::QuantParams
+ * (include/lanehmm/profile.hpp:27-38).  Defaults {3.0, 195, 3, 3, 3}. */
+typedef struct lhmm_quant {
+    double scale;
+    uint8_t base;
+    uint8_t dbias;
+    uint8_t tec;
+    uint8_t tjb;
+} lhmm_quant;
+
+typedef struct lhmm_scan_options {
+    int alg;            /* lhmm_alg */
+    int variant;        /* lhmm_variant */
+    uint32_t lanes;     /* lanes cooperating on one sequence (1..32, pow2); 0 = auto */
+    uint32_t rows;      /* striped rows H per lane; 0 = auto */
+    double threshold;   /* pass iff pValue <= threshold || overflow; in [0,1] */
+    int fault_injection;/* verification aid: corrupts one lane's E (ScanOptions.faultInjection) */
+} lhmm_scan_options;
+
+typedef struct lhmm_scan_stats {
+    double device_ms;       /* CUDA-event time of the scan kernel(s) */
+    double gcups;           /* residues * M / device seconds / 1e9 */
+    uint64_t sequences;     /* sequences scanned by this context */
+    uint64_t residues;      /* real residues (excludes padding) */
+    uint64_t cells;         /* residues * M */
+    uint32_t lanes;         /* geometry used */
+    uint32_t rows;
+    uint32_t variant;
+    uint32_t launches;      /* kernels launched for this scan */
+    uint32_t grid;          /* CTAs of the persistent grid */
+    uint32_t threads;       /* threads per CTA */
+    uint32_t smem_bytes;    /* dynamic shared memory per CTA */
+    uint32_t reserved;
+} lhmm_scan_stats;
+
+typedef struct lhmm_context lhmm_context;
+typedef struct lhmm_rng lhmm_rng;
+
+int lhmm_abi_version(void);
+const char* lhmm_last_error(void);
+
+/* ---- host-side byte-space helpers (bit-identical to the reference) ---- */
+int lhmm_quantize_emissions(const double* match_scores /* m x 20 */, uint32_t m,
+                            const lhmm_quant* q, uint8_t* costs_out /* m x 21 */);
+uint8_t lhmm_move_cost(uint64_t seq_len, const lhmm_quant* q);
+uint8_t lhmm_sequence_base(uint64_t seq_len, const lhmm_quant* q);
+int lhmm_finalize_hit(uint8_t raw, uint64_t seq_len, double lambda, double tau,
+                      const lhmm_quant* q, int alg, double* bits, double* p_value,
+                      int* overflow);
+/* Geometry the auto policy picks for a model of m nodes. */
+int lhmm_select_geometry(uint32_t m, int alg, int variant, uint32_t* lanes, uint32_t* rows);
+
+/* The per-length device lookup tables a scan uses (host-only, for checks):
+ * base_out[len] = engine_sequence_base(len); rawmin_out[len] = least raw byte
+ * that passes (pValue <= threshold || overflow), so that the device pass bit
+ * is raw == 255 || raw >= rawmin[len].  Arrays hold max_len+1 bytes. */
+int lhmm_length_tables(const lhmm_quant* q, double lambda, double tau, int alg, double threshold,
+                       uint32_t max_len, uint8_t* base_out, uint8_t* rawmin_out);
+/* The shard plan lhmm_set_database applies (host-only): global indices of
+ * shard `rank` of `world` in ascending order; *count gets their number
+ * (call with out == NULL to size). */
+int lhmm_shard_plan(const uint64_t* offsets, uint64_t nseq, uint32_t rank, uint32_t world,
+                    uint64_t* out, uint64_t* count);
+
+/* ---- device context ---------------------------------------------------- */
+int lhmm_context_create(int device, lhmm_context** out);
+int lhmm_context_destroy(lhmm_context* ctx);
+/* Run subsequent work on an existing cudaStream_t (e.g. torch's current
+ * stream); NULL restores the context's own stream. */
+int lhmm_context_set_stream(lhmm_context* ctx, void* cuda_stream);
+int lhmm_context_device_info(lhmm_context* ctx, int* sm_count, int* sm_clock_khz,
+                             int* cc_major, int* cc_minor);
+
+/* Profile: quantized cost matrix m x 21 (CostMatrix bytes, profile.hpp:43-52)
+ * plus the Gumbel parameters used for pass decisions. */
+int lhmm_set_profile(lhmm_context* ctx, const uint8_t* costs, uint32_t m, const lhmm_quant* q,
+                     double lambda, double tau);
+
+/* Additional resident profiles: scan several models over one resident
+ * database without re-staging.  lhmm_add_profile makes the new profile
+ * current and returns its id; lhmm_set_profile always replaces id 0. */
+int lhmm_add_profile(lhmm_context* ctx, const uint8_t* costs, uint32_t m, const lhmm_quant* q,
+                     double lambda, double tau, uint32_t* profile_id);
+int lhmm_select_profile(lhmm_context* ctx, uint32_t profile_id);
+
+/* Database: flat residue codes (0..20) with nseq+1 offsets.  Packs the
+ * shard (shard_rank of shard_count, balanced by residue count) into
+ * length-binned 32-sequence tiles and uploads it.  shard_count = 1 keeps
+ * everything.  Returns the number of sequences this shard owns. */
+int lhmm_set_database(lhmm_context* ctx, const uint8_t* residues, const uint64_t* offsets,
+                      uint64_t nseq, uint32_t shard_rank, uint32_t shard_count,
+                      uint64_t* local_sequences);
+/* Global indices of the shard's sequences, ascending; local index i of the
+ * scan outputs is global index out[i]. */
+int lhmm_shard_indices(lhmm_context* ctx, uint64_t* out);
+/* Packed-database statistics (the B200 analogue of balance_stats,
+ * seqdb.cpp:190-227): residues, padded rows*slots, tiles. */
+int lhmm_database_stats(lhmm_context* ctx, uint64_t* residues, uint64_t* padded_cells,
+                        uint64_t* tiles, uint64_t* packed_bytes);
+
+/* Re-copy the packed host image (pinned) to the device: the host->device
+ * leg of an end-to-end scan whose packing was done once. */
+int lhmm_upload_database(lhmm_context* ctx);
+
+/* Scan the resident database; raw/pass are host arrays of local_sequences
+ * bytes in local index order (copied back after the kernel). */
+int lhmm_scan(lhmm_context* ctx, const lhmm_scan_options* opt, uint8_t* raw_out,
+              uint8_t* pass_out, lhmm_scan_stats* stats);
+/* Same, but raw/pass are DEVICE pointers on ctx's device (no D2H, no sync
+ * beyond the event timing). */
+int lhmm_scan_device(lhmm_context* ctx, const lhmm_scan_options* opt, uint8_t* d_raw,
+                     uint8_t* d_pass, lhmm_scan_stats* stats);
+
+/* SSV over all sequences, then MSV over the survivors (pass bit set),
+ * compacted on the device.  ssv_raw/pass for all; msv_raw valid where
+ * pass_out != 0, else 0.  Returns survivors via *rescored. */
+int lhmm_filter_pipeline(lhmm_context* ctx, double threshold, int variant, uint8_t* ssv_raw,
+                         uint8_t* pass_out, uint8_t* msv_raw, uint64_t* rescored,
+                         lhmm_scan_stats* ssv_stats, lhmm_scan_stats* msv_stats);
+
+/* ---- seeded synthetic inputs (same streams as synth::*) ------------------ */
+int lhmm_rng_create(uint64_t seed, lhmm_rng** out);
+int lhmm_rng_destroy(lhmm_rng* rng);
+uint64_t lhmm_rng_next(lhmm_rng* rng);
+int lhmm_synth_random_profile(lhmm_rng* rng, uint32_t m, double* scores /* m x 20 */,
+                              double* lambda, double* tau);
+/* Generates a record set into the rng's pending buffer; *total gets the
+ * residue count so the caller can size lhmm_synth_take's buffers. */
+int lhmm_synth_random_records(lhmm_rng* rng, uint64_t count, uint64_t len_lo, uint64_t len_hi,
+                              uint64_t* total);
+int lhmm_synth_lognormal_records(lhmm_rng* rng, uint64_t count, double median, double sigma,
+                                 uint64_t min_len, uint64_t* total);
+int lhmm_synth_plant_motifs(lhmm_rng* rng, const double* scores, uint32_t m, double fraction);
+int lhmm_synth_take(lhmm_rng* rng, uint8_t* residues, uint64_t* offsets /* count+1 */);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LHMM_B200_H */

@@ -1,0 +1,401 @@
+// lhmm_kernel.cuh -- sm_100a MSV/SSV filter scan kernels.
+//
+// One warp runs G = 32/L sequences side by side ("multi-sequence-per-warp"
+// tiering); the L lanes of a group share one sequence and
+// hold its model striped across registers: lane oig, word h, sub-word k holds
+// model node  j = (CPW*oig + k)*H + h + 1  -- the reference's striping
+// node = stripe*H + h + 1 (src/profile.cpp:176-181).  Every residue row:
+//
+//   1. the stripe shift (vwarp::reorder, src/vwarp.cpp:27-64): word H-1 moves
+//      one stripe up -- a __byte_perm inside the lane plus one __shfl_up_sync
+//      inside the group, with -inf injected at stripe 0;
+//   2. H cell updates in registers, in place from h = H-1 down to 0, with the
+//      emission costs for (residue, h) read from the shared-memory profile
+//      (one LDS per word, immediate offsets);
+//   3. the running E max; for MSV the group max is reduced every row with
+//      xor shuffles (vwarp::max_reduce, src/vwarp.cpp:66-89) and B updated
+//      with the exact J-free form  B = max(base, subs(E, tec+tjb))
+//      (special_state_update, src/engine.cpp:53-57).
+//
+// Scores are saturated bytes (the device-side bit-exact contract of
+// SURVEY.md §8(a)); the arithmetic "variant" policy decides how the bytes
+// are packed in a 32-bit register:
+//   Dpx16  : two u16 cells, native DPX VIADDMNMX / VIMNMX / VIMNMX3 (ALU pipe)
+//   Fp16   : two f16 cells in a fixed-point byte domain, saturating HADD2 on
+//            the FMA pipe (exact: every value is a multiple of 2^-8 or 2^-7)
+//   Swar8  : four u8 cells, __vaddus4 / __vsubus4 / __vmaxu4 (paper tier 5)
+//
+// Sequences are length-binned into 32-sequence tiles (host packer); a
+// persistent grid of warps pulls (tile, sub-batch) work items from a global
+// counter, longest tiles first.  Residues stream from HBM as 16-byte chunks
+// (one 128-bit load per lane per 16 rows, coalesced per warp).  The profile
+// table is staged once per CTA with one cp.async.bulk (TMA engine) copy.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace lhmm {
+
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kResidueRows = 23;  // codes 0..20, 21 '@', 22 '#'
+constexpr int kPadCode = 22;
+constexpr int kMaxThreads = 512;
+
+struct KParams {
+    const uint8_t* db;          // packed tiles
+    const uint64_t* tile_off;   // byte offset of each tile
+    const uint32_t* lens;       // per sorted slot (tiles*32); 0 for empty slots
+    const uint32_t* out_idx;    // per sorted slot -> output index (0xffffffff: none)
+    const uint8_t* base_tab;    // MSV B base per length  [max_len+1]
+    const uint8_t* rawmin_tab;  // pass threshold per length [max_len+1]
+    const uint32_t* table;      // profile table, smem image
+    uint8_t* raw_out;
+    uint8_t* pass_out;
+    uint32_t* counter;          // work-item counter (zeroed per launch)
+    uint32_t n_items;           // tiles * L
+    uint32_t table_bytes;       // multiple of 16
+    uint32_t res_stride;        // words per residue row (P)
+    uint32_t copy_stride;       // words between per-group replicas (0: shared)
+    uint32_t dbias;             // per-step bias
+    uint32_t tecjb;             // tec + tjb (may exceed 255)
+    uint32_t fault;             // fault injection (verification only)
+};
+
+// ---------------------------------------------------------------------------
+// small PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Stage `bytes` (multiple of 16) from global into shared memory with the
+// bulk-copy (TMA) engine, completing on an mbarrier.
+__device__ __forceinline__ void stage_table(uint32_t* smem, const uint32_t* gsrc, uint32_t bytes,
+                                            uint64_t* bar) {
+    const uint32_t b = smem_u32(bar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                     : "memory");
+        const uint32_t chunk = 65536u;
+        for (uint32_t off = 0; off < bytes; off += chunk) {
+            const uint32_t n = bytes - off < chunk ? bytes - off : chunk;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+                "[%3];" ::"r"(smem_u32(smem) + off),
+                "l"(reinterpret_cast<const char*>(gsrc) + off), "r"(n), "r"(b)
+                : "memory");
+        }
+    }
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(b)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint8_t* p) {
+    return __ldcs(reinterpret_cast<const uint4*>(p));
+}
+
+__device__ __forceinline__ __half2 as_h2(uint32_t u) {
+    return *reinterpret_cast<__half2*>(&u);
+}
+__device__ __forceinline__ uint32_t as_u32(__half2 h) {
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// ---------------------------------------------------------------------------
+// arithmetic variants.  Each provides:
+//   CPW                 cells per 32-bit word
+//   NEG                 -inf (floor) word
+//   St                  per-sequence constants + B
+//   init(st, base, p)   per-sequence setup
+//   cell(x, c, st)      one word update from the diagonal predecessor x
+//   acc2(E, a, b)       E = max(E, a, b)
+//   shift(top, up)      stripe shift of the last row word
+//   group_reduce<L>(E)  max over the whole sequence share (all sub-words, lanes)
+//   update_B(st, E)     MSV B update from reduced E
+//   raw(E)              byte score from reduced E
+
+template <int ALG>
+struct Dpx16 {
+    static constexpr int CPW = 2;
+    static constexpr bool kMsv = ALG == 0;
+    static constexpr uint32_t NEG = kMsv ? 0u : 0x00800080u;
+    struct St {
+        uint32_t B, base2, d2, ntj2;
+    };
+    __device__ static __forceinline__ void init(St& s, uint32_t base, const KParams& p) {
+        s.base2 = base * 0x00010001u;
+        s.B = s.base2;
+        s.d2 = p.dbias * 0x00010001u;
+        s.ntj2 = (0u - p.tecjb) & 0xffffu;
+        s.ntj2 |= s.ntj2 << 16;
+    }
+    __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
+        if constexpr (kMsv) {
+            uint32_t y = __viaddmin_u16x2(__vmaxu2(x, s.B), s.d2, 0x00ff00ffu);
+            return __viaddmax_s16x2(y, c, 0u);
+        } else {
+            uint32_t y = __viaddmin_u16x2(x, s.d2, 0x00ff00ffu);
+            return __viaddmax_s16x2(y, c, 0x00800080u);
+        }
+    }
+    __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
+        return __vimax3_u16x2(E, a, b);
+    }
+    __device__ static __forceinline__ uint32_t acc1(uint32_t E, uint32_t a) {
+        return __vmaxu2(E, a);
+    }
+    __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
+        return __byte_perm(top, up, 0x1076);
+    }
+    template <int L>
+    __device__ static __forceinline__ uint32_t group_reduce(uint32_t E) {
+        uint32_t e = __vmaxu2(E, __byte_perm(E, E, 0x1032));
+#pragma unroll
+        for (int off = 1; off < L; off <<= 1) e = __vmaxu2(e, __shfl_xor_sync(kFull, e, off));
+        return e;
+    }
+    __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
+        s.B = __viaddmax_s16x2(e, s.ntj2, s.base2);
+    }
+    __device__ static __forceinline__ uint32_t raw(uint32_t e) { return e & 0xffu; }
+};
+
+// f16 fixed-point byte domain.  MSV: stored q = v/256; the top clamp
+// (adds dbias, cap 255) runs in p = (v+1)/256 so that HADD2.SAT's 1.0 cap is
+// byte 255; the bottom clamp (subs cost, floor 0) lands back in q with
+// HADD2.SAT's 0.0 floor.  Table entries are -(cost+1)/256.  SSV: the same
+// with q = (v-128)/128, p = (v-127)/128 and table entries -(cost+1)/128.
+// All intermediate values are multiples of 2^-8 in [-2, 2]: exact in f16.
+// Non-negative f16 bit patterns order like u16, so E/B maxima use DPX ops.
+template <int ALG>
+struct Fp16 {
+    static constexpr int CPW = 2;
+    static constexpr bool kMsv = ALG == 0;
+    static constexpr uint32_t NEG = 0u;  // +0.0 in both halves
+    struct St {
+        uint32_t B, base2, d1, tj2;
+    };
+    __device__ static __forceinline__ uint32_t splat(float f) {
+        return as_u32(__float2half2_rn(f));
+    }
+    __device__ static __forceinline__ void init(St& s, uint32_t base, const KParams& p) {
+        if constexpr (kMsv) {
+            s.base2 = splat(float(base) / 256.f);
+            s.d1 = splat(float(p.dbias + 1) / 256.f);
+            s.tj2 = splat(float(p.tecjb) / 256.f);
+        } else {
+            s.base2 = 0;
+            s.d1 = splat(float(p.dbias + 1) / 128.f);
+            s.tj2 = 0;
+        }
+        s.B = s.base2;
+    }
+    __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
+        if constexpr (kMsv) {
+            const uint32_t m = __vmaxu2(x, s.B);
+            const __half2 pp = __hadd2_sat(as_h2(m), as_h2(s.d1));
+            return as_u32(__hadd2_sat(pp, as_h2(c)));
+        } else {
+            const __half2 pp = __hadd2_sat(as_h2(x), as_h2(s.d1));
+            return as_u32(__hadd2_sat(pp, as_h2(c)));
+        }
+    }
+    __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
+        return __vimax3_u16x2(E, a, b);
+    }
+    __device__ static __forceinline__ uint32_t acc1(uint32_t E, uint32_t a) {
+        return __vmaxu2(E, a);
+    }
+    __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
+        return __byte_perm(top, up, 0x1076);
+    }
+    template <int L>
+    __device__ static __forceinline__ uint32_t group_reduce(uint32_t E) {
+        uint32_t e = __vmaxu2(E, __byte_perm(E, E, 0x1032));
+#pragma unroll
+        for (int off = 1; off < L; off <<= 1) e = __vmaxu2(e, __shfl_xor_sync(kFull, e, off));
+        return e;
+    }
+    __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
+        // max(base, E - (tec+tjb)); the difference may be negative -> f16 max
+        s.B = as_u32(__hmax2(__hsub2(as_h2(e), as_h2(s.tj2)), as_h2(s.base2)));
+    }
+    __device__ static __forceinline__ uint32_t raw(uint32_t e) {
+        const float f = __low2float(as_h2(e));
+        return kMsv ? uint32_t(f * 256.f + 0.5f) : 128u + uint32_t(f * 128.f + 0.5f);
+    }
+};
+
+template <int ALG>
+struct Swar8 {
+    static constexpr int CPW = 4;
+    static constexpr bool kMsv = ALG == 0;
+    static constexpr uint32_t NEG = kMsv ? 0u : 0x80808080u;
+    struct St {
+        uint32_t B, base4, d4, tj4;
+    };
+    __device__ static __forceinline__ void init(St& s, uint32_t base, const KParams& p) {
+        s.base4 = base * 0x01010101u;
+        s.B = s.base4;
+        s.d4 = p.dbias * 0x01010101u;
+        s.tj4 = (p.tecjb > 255u ? 255u : p.tecjb) * 0x01010101u;
+    }
+    __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
+        if constexpr (kMsv) {
+            return __vsubus4(__vaddus4(__vmaxu4(x, s.B), s.d4), c);
+        } else {
+            return __vmaxu4(__vsubus4(__vaddus4(x, s.d4), c), 0x80808080u);
+        }
+    }
+    __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
+        return __vmaxu4(__vmaxu4(E, a), b);
+    }
+    __device__ static __forceinline__ uint32_t acc1(uint32_t E, uint32_t a) {
+        return __vmaxu4(E, a);
+    }
+    __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
+        return __byte_perm(top, up, 0x2107);
+    }
+    template <int L>
+    __device__ static __forceinline__ uint32_t group_reduce(uint32_t E) {
+        uint32_t e = __vmaxu4(E, __byte_perm(E, E, 0x1032));
+        e = __vmaxu4(e, __byte_perm(e, e, 0x2301));
+#pragma unroll
+        for (int off = 1; off < L; off <<= 1) e = __vmaxu4(e, __shfl_xor_sync(kFull, e, off));
+        return e;
+    }
+    __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
+        s.B = __vmaxu4(s.base4, __vsubus4(e, s.tj4));
+    }
+    __device__ static __forceinline__ uint32_t raw(uint32_t e) { return e & 0xffu; }
+};
+
+// ---------------------------------------------------------------------------
+// the scan kernel
+
+template <class V, int L, int H>
+__global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
+    extern __shared__ __align__(128) uint32_t smem[];
+    __shared__ __align__(8) uint64_t bar;
+    stage_table(smem, p.table, p.table_bytes, &bar);
+
+    constexpr int G = 32 / L;  // sequences per warp
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t oig = lane & (L - 1);
+    const uint32_t grp = lane / L;
+    const uint32_t P = p.res_stride;
+    const uint32_t* tab_lane = smem + grp * p.copy_stride + oig;
+
+    for (;;) {
+        uint32_t item = 0;
+        if (lane == 0) item = atomicAdd(p.counter, 1u);
+        item = __shfl_sync(kFull, item, 0);
+        if (item >= p.n_items) break;
+        const uint32_t tile = item / L;
+        const uint32_t sub = item % L;
+        const uint32_t slot = sub * G + grp;
+        const uint32_t sidx = tile * 32u + slot;
+        const uint32_t len = p.lens[sidx];
+        const uint32_t rows = p.lens[tile * 32u + sub * G];  // longest of the sub-batch
+        const uint8_t* src = p.db + p.tile_off[tile] + slot * 16u;
+
+        typename V::St st;
+        V::init(st, p.base_tab[len], p);
+        uint32_t g[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) g[h] = V::NEG;
+        uint32_t E = V::NEG;
+
+        for (uint32_t r0 = 0; r0 < rows; r0 += 16) {
+            const uint4 v = ld_stream(src + (r0 >> 4) * 512u);
+            uint32_t w0 = v.x, w1 = v.y, w2 = v.z, w3 = v.w;
+#pragma unroll 1
+            for (uint32_t q = 0; q < 4; ++q) {
+                const uint32_t cur = w0;
+                w0 = w1;
+                w1 = w2;
+                w2 = w3;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    if (r0 + q * 4 + b < rows) {
+                        const uint32_t x = (cur >> (8 * b)) & 0xffu;
+                        const uint32_t* tp = tab_lane + x * P;
+                        const uint32_t top = g[H - 1];
+                        uint32_t up = V::NEG;
+                        if constexpr (L > 1) {
+                            up = __shfl_up_sync(kFull, top, 1, L);
+                            if (oig == 0) up = V::NEG;
+                        }
+                        const uint32_t sh = V::shift(top, up);
+#pragma unroll
+                        for (int h = H - 1; h >= 1; --h) g[h] = V::cell(g[h - 1], tp[h * L], st);
+                        g[0] = V::cell(sh, tp[0], st);
+#pragma unroll
+                        for (int h = 0; h + 1 < H; h += 2) E = V::acc2(E, g[h], g[h + 1]);
+                        if constexpr (H % 2) E = V::acc1(E, g[H - 1]);
+                        if constexpr (V::kMsv) {
+                            E = V::template group_reduce<L>(E);
+                            V::update_B(st, E);
+                        }
+                    }
+                }
+            }
+        }
+        if constexpr (!V::kMsv) E = V::template group_reduce<L>(E);
+        uint32_t raw = V::raw(E);
+        if (p.fault && grp == 0 && raw < 255u) raw += 1u;  // verification aid
+        const uint32_t oi = p.out_idx[sidx];
+        if (oig == 0 && oi != 0xffffffffu) {
+            p.raw_out[oi] = uint8_t(raw);
+            p.pass_out[oi] = uint8_t(raw == 255u || raw >= p.rawmin_tab[len]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host-side launch plumbing, instantiated per (variant, alg, L) translation
+// unit by gen_instances.py
+
+struct LaunchCfg {
+    int threads;
+    size_t smem;
+    int blocks_per_sm;  // out (query)
+    int grid;           // in (launch)
+    cudaStream_t stream;
+};
+
+enum { kOpQuery = 0, kOpLaunch = 1 };
+
+template <class V, int L, int H>
+int launch_one(int op, LaunchCfg* c, const KParams* p) {
+    auto* k = &scan_kernel<V, L, H>;
+    if (op == kOpQuery) {
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(c->smem)) !=
+            cudaSuccess)
+            return -2;
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, c->threads, c->smem) !=
+            cudaSuccess)
+            return -2;
+        c->blocks_per_sm = n;
+        return 0;
+    }
+    k<<<c->grid, c->threads, c->smem, c->stream>>>(*p);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -2;
+}
+
+}  // namespace lhmm

@@ -1,0 +1,70 @@
+"""Multi-GPU driver: one process per GPU, the database sharded by residue
+count (lhmm_set_database's LPT tile plan), per-sequence raw scores and pass
+bits gathered to rank 0.  The path has no reduction -- only this gather
+(BASELINE.json north_star).
+
+Works with any torch.distributed backend: NCCL over NVLink/NVSwitch on the
+GPU box, gloo on CPU for the tests.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def gather_to_rank0(dist, raw, passed, gidx, n_total, device=None):
+    """Gather each rank's (raw, pass) bytes for its global indices `gidx`
+    into full-length arrays on rank 0 (None elsewhere).
+
+    raw / passed: uint8 tensors of the shard's local outputs (local order);
+    gidx: int64 tensor of the matching global indices.  Shards are padded to
+    the largest count so a single gather carries them.
+    """
+    import torch
+
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    dev = raw.device if device is None else device
+    n = torch.tensor([raw.numel()], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(counts, n)
+    mx = int(max(int(c) for c in counts))
+    # one int64 row of indices + one row of packed (raw | pass << 8) int64
+    buf = torch.full((2, max(mx, 1)), -1, dtype=torch.int64, device=dev)
+    k = raw.numel()
+    buf[0, :k] = gidx.to(dev, torch.int64)
+    buf[1, :k] = raw.to(dev, torch.int64) | (passed.to(dev, torch.int64) << 8)
+    glist = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
+    dist.gather(buf, glist, dst=0)
+    if rank != 0:
+        return None, None
+    out_raw = np.zeros(n_total, dtype=np.uint8)
+    out_pass = np.zeros(n_total, dtype=bool)
+    seen = np.zeros(n_total, dtype=np.int32)
+    for r, g in enumerate(glist):
+        c = int(counts[r])
+        idx = g[0, :c].cpu().numpy()
+        val = g[1, :c].cpu().numpy()
+        out_raw[idx] = (val & 0xFF).astype(np.uint8)
+        out_pass[idx] = ((val >> 8) & 1).astype(bool)
+        seen[idx] += 1
+    if not (seen == 1).all():
+        raise RuntimeError("shards do not partition the database")
+    return out_raw, out_pass
+
+
+def shard_plan(offsets, rank, world):
+    """Global indices shard `rank` of `world` owns (host-only; the same plan
+    lhmm_set_database applies)."""
+    import ctypes as C
+
+    from . import _native
+    from .lanehmm import _check
+    off = np.ascontiguousarray(offsets, dtype=np.uint64)
+    n = off.size - 1
+    cnt = C.c_uint64()
+    _check(_native.lib().lhmm_shard_plan(off.ctypes.data_as(_native.u64p), n, rank, world, None,
+                                         C.byref(cnt)))
+    out = np.zeros(max(cnt.value, 1), dtype=np.uint64)
+    _check(_native.lib().lhmm_shard_plan(off.ctypes.data_as(_native.u64p), n, rank, world,
+                                         out.ctypes.data_as(_native.u64p), C.byref(cnt)))
+    return out[:cnt.value]

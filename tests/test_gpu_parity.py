@@ -1,0 +1,191 @@
+"""GPU parity: every kernel variant / lane count / algorithm against the CPU
+oracle, bit-exact (integer byte scores and pass bits), through the C ABI.
+
+Mirrors the reference's engine tests (proj/tests/test_engine.cpp) and the
+acceptance criteria 1, 5 and 6 (proj/tests/acceptance_main.cpp)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1707_09683_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = [P.Variant.Dpx16, P.Variant.Fp16, P.Variant.Swar8]
+QUANTS = [P.QuantParams(), P.QuantParams(3.0, 120, 3, 20, 20), P.QuantParams(2.0, 240, 10, 1, 5),
+          P.QuantParams(3.0, 0, 0, 0, 0)]
+
+
+def oq(q):
+    return oracle.QuantParams(q.scale, q.base, q.dbias, q.tec, q.tjb)
+
+
+def rows_for(variant, L, m):
+    cpw = 4 if variant == P.Variant.Swar8 else 2
+    rows = {P.Variant.Swar8: [2, 4, 8, 12, 16, 24, 32, 40, 48]}.get(
+        variant, [2, 4, 6, 8, 10, 12, 14, 16, 20, 24, 28, 32, 36, 40, 44, 48, 52, 56, 60, 64, 72])
+    for h in rows:
+        if cpw * L * h >= m:
+            return h
+    return None
+
+
+def scan(costs, q, db, hmm, **kw):
+    with P.Scanner(0) as s:
+        s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        s.set_database(db)
+        return s.scan(P.ScanOptions(**kw))
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=lambda v: v.name)
+@pytest.mark.parametrize("alg", [P.Algorithm.Msv, P.Algorithm.Ssv], ids=lambda a: a.name)
+@pytest.mark.parametrize("L", [1, 2, 4, 8, 16, 32])
+def test_every_lane_count_matches_oracle(ora, variant, alg, L):
+    rng = P.Rng(1000 + 97 * L + int(alg) + 7 * int(variant))
+    cpw = 4 if variant == P.Variant.Swar8 else 2
+    maxcap = cpw * L * (48 if variant == P.Variant.Swar8 else 72)
+    for t, q in enumerate(QUANTS):
+        m = int(7 + rng.next() % max(1, min(maxcap, 2405) - 6))
+        hmm = rng.random_profile(m)
+        db = rng.random_records(64, 1, max(8, min(400, 3_000_000 // (64 * m))),
+                                plant=(hmm, 0.2))
+        costs = P.quantize_emissions(hmm, q)
+        H = rows_for(variant, L, m)
+        rep = scan(costs, q, db, hmm, alg=alg, variant=variant, lanes=L, rows=H, threshold=0.3)
+        want = ora.scan_flat(int(alg), costs.bytes, db.residues, db.offsets, oq(q))
+        assert rep.lanes == L and rep.rows == H
+        np.testing.assert_array_equal(rep.raw, want, err_msg=f"m={m} q={q} L={L} H={H}")
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=lambda v: v.name)
+def test_pass_bits_match_finalize_hit(ora, variant):
+    rng = P.Rng(0xC1)
+    hmm = rng.random_profile(200)
+    db = rng.random_records(500, 50, 650, plant=(hmm, 0.05))
+    for q in QUANTS[:2]:
+        costs = P.quantize_emissions(hmm, q)
+        lens = np.diff(db.offsets)
+        for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
+            for t in (0.0, 0.022, 0.103, 0.307, 0.458, 1.0):
+                rep = scan(costs, q, db, hmm, alg=alg, variant=variant, threshold=t)
+                want = np.array([ora.passes(int(r), int(n), hmm.lambda_, hmm.tau, oq(q), int(alg), t)
+                                 for r, n in zip(rep.raw, lens)])
+                np.testing.assert_array_equal(rep.passed, want, err_msg=f"{alg} t={t}")
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=lambda v: v.name)
+def test_edge_lengths_and_empty_sequences(ora, variant):
+    """Empty sequences score the floor (test_oracle.cpp:22-28); lengths around
+    the 16-row chunk boundary; a single residue; long sequences."""
+    rng = P.Rng(5)
+    hmm = rng.random_profile(61)
+    q = P.QuantParams(3.0, 120, 3, 20, 20)
+    costs = P.quantize_emissions(hmm, q)
+    lens = [0, 1, 2, 15, 16, 17, 31, 32, 33, 0, 47, 48, 49, 255, 256, 257, 1000, 3001, 0, 5]
+    seqs = [np.frombuffer(np.random.default_rng(n + 1).integers(0, 21, n).astype(np.uint8).tobytes(),
+                          np.uint8) for n in lens]
+    db = P.SequenceDB.from_sequences(seqs)
+    for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
+        for L in (1, 4, 32):
+            rep = scan(costs, q, db, hmm, alg=alg, variant=variant, lanes=L)
+            want = ora.scan_flat(int(alg), costs.bytes, db.residues, db.offsets, oq(q))
+            np.testing.assert_array_equal(rep.raw, want)
+            assert rep.raw[0] == (0 if alg == P.Algorithm.Msv else 0x80)
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=lambda v: v.name)
+def test_floor_profiles(variant):
+    """Flat profile with zero base pins MSV at 0 (test_engine.cpp:112-134);
+    all-invalid emissions keep SSV at 0x80 (test_engine.cpp:386-404)."""
+    rng = P.Rng(3)
+    db = rng.random_records(40, 1, 50)
+    flat = P.ProfileHMM("flat", 1, np.zeros((1, 20)), 0.7, 2.0)
+    q0 = P.QuantParams(base=0)
+    rep = scan(P.quantize_emissions(flat, q0), q0, db, flat, alg=P.Algorithm.Msv, variant=variant)
+    assert (rep.raw == 0).all()
+    inv = P.ProfileHMM("inv", 5, np.full((5, 20), -100.0), 0.7, 2.0)
+    q = P.QuantParams()
+    rep = scan(P.quantize_emissions(inv, q), q, db, inv, alg=P.Algorithm.Ssv, variant=variant)
+    assert (rep.raw == 0x80).all()
+
+
+def test_largest_pfam_model_2405(ora):
+    rng = P.Rng(2405)
+    hmm = rng.random_profile(2405)
+    db = rng.random_records(96, 1, 300)
+    for q in QUANTS[:2]:
+        costs = P.quantize_emissions(hmm, q)
+        for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
+            for variant in (P.Variant.Dpx16, P.Variant.Fp16):
+                rep = scan(costs, q, db, hmm, alg=alg, variant=variant)
+                want = ora.scan_flat(int(alg), costs.bytes, db.residues, db.offsets, oq(q))
+                np.testing.assert_array_equal(rep.raw, want)
+
+
+def test_fault_injection_is_detected(ora):
+    rng = P.Rng(37)
+    hmm = rng.random_profile(64)
+    db = rng.random_records(16, 40, 80)
+    q = P.QuantParams(3.0, 120, 3, 20, 20)
+    costs = P.quantize_emissions(hmm, q)
+    rep = scan(costs, q, db, hmm, alg=P.Algorithm.Msv, lanes=32, fault_injection=True)
+    want = ora.scan_flat(0, costs.bytes, db.residues, db.offsets, oq(q))
+    assert (rep.raw != want).any()
+
+
+def test_shards_cover_the_database(ora):
+    rng = P.Rng(77)
+    hmm = rng.random_profile(150)
+    db = rng.lognormal_records(3000, 290, 0.65, 2)
+    q = P.QuantParams(3.0, 120, 3, 20, 20)
+    costs = P.quantize_emissions(hmm, q)
+    want = ora.scan_flat(0, costs.bytes, db.residues, db.offsets, oq(q))
+    got = np.full(db.count, -1, dtype=np.int32)
+    with P.Scanner(0) as s:
+        s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        for r in range(3):
+            s.set_database(db, r, 3)
+            idx = s.shard_indices()
+            rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv))
+            assert (got[idx] == -1).all()
+            got[idx] = rep.raw
+    np.testing.assert_array_equal(got, want)
+
+
+def test_device_outputs_via_torch(ora):
+    import torch
+    rng = P.Rng(11)
+    hmm = rng.random_profile(300)
+    db = rng.random_records(1000, 10, 500)
+    q = P.QuantParams()
+    costs = P.quantize_emissions(hmm, q)
+    raw = torch.zeros(db.count, dtype=torch.uint8, device="cuda:0")
+    ps = torch.zeros(db.count, dtype=torch.uint8, device="cuda:0")
+    with P.Scanner(0) as s:
+        s.set_stream(torch.cuda.current_stream().cuda_stream)
+        s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        s.set_database(db)
+        st = s.scan_device(P.ScanOptions(alg=P.Algorithm.Ssv), raw.data_ptr(), ps.data_ptr())
+    torch.cuda.synchronize()
+    want = ora.scan_flat(1, costs.bytes, db.residues, db.offsets, oq(q))
+    np.testing.assert_array_equal(raw.cpu().numpy(), want)
+    assert st["launches"] == 1
+
+
+def test_multiple_resident_profiles(ora):
+    rng = P.Rng(12)
+    db = rng.random_records(300, 10, 400)
+    q = P.QuantParams(3.0, 120, 3, 20, 20)
+    with P.Scanner(0) as s:
+        s.set_database(db)
+        ids, models = [], []
+        for m in (48, 400, 1000):
+            hmm = rng.random_profile(m)
+            c = P.quantize_emissions(hmm, q)
+            ids.append(s.add_profile(c, q, hmm.lambda_, hmm.tau))
+            models.append(c)
+        for pid, c in reversed(list(zip(ids, models))):
+            s.select_profile(pid)
+            rep = s.scan(P.ScanOptions(alg=P.Algorithm.Ssv))
+            want = ora.scan_flat(1, c.bytes, db.residues, db.offsets, oq(q))
+            np.testing.assert_array_equal(rep.raw, want)
