@@ -227,12 +227,19 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--models", default="", help="override model lengths, e.g. 1000,2405")
+    ap.add_argument("--algs", default="", help="override algorithms: msv, ssv or both")
     ap.add_argument("--lanes", type=int, default=0)
     ap.add_argument("--rows", type=int, default=0)
     args = ap.parse_args()
-    if args.nseq:
+    if args.nseq or args.models or args.algs:
         w = list(WORKLOADS[args.workload])
-        w[3] = args.nseq
+        if args.nseq:
+            w[3] = args.nseq
+        if args.models:
+            w[2] = tuple(int(x) for x in args.models.split(","))
+        if args.algs:
+            w[1] = args.algs
         WORKLOADS[args.workload] = tuple(w)
     if args.impl == "reference":
         return run_reference(args, None)

@@ -102,7 +102,9 @@ bool use_replica(int variant, uint32_t L, uint32_t H) {
 int resolve_variant(int variant, int alg, uint32_t m) {
     (void)alg;
     (void)m;
-    if (variant == LHMM_VARIANT_AUTO) return LHMM_VARIANT_DPX16;
+    // measured on B200 (profiles/round1_sweep.md): the f16 FMA-pipe variant
+    // is fastest for both algorithms at every model length 48..2405
+    if (variant == LHMM_VARIANT_AUTO) return LHMM_VARIANT_FP16;
     return variant;
 }
 

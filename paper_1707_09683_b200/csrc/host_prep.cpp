@@ -259,36 +259,32 @@ void free_packed(PackedDb& db, void (*host_free)(void*)) {
 // 0xff.  Residue rows 21 ('@') and 22 ('#') are all 0xff, which makes padding
 // rows inert (test_engine.cpp:172-195).
 //
-// Bank layout: with L == 1 the residue stride is odd, so the 32 lanes'
-// residues hit distinct banks (equal residues broadcast).  With 1 < L < 32
-// every group of L lanes reads its own replica whose bank window is
-// [g*L, g*L+L): copy_stride = 23*P + L with P a multiple of 32.  With
-// L == 32 the whole warp shares one residue.
+// Bank layout: every lane reads its words four rows at a time with one
+// 128-bit LDS (word (h/4)*4L + 4*oig + h%4 of its residue row), so a
+// quarter-warp (8 lanes x 16 B) is one shared-memory wavefront.  The 8/L lane
+// groups of a quarter-warp (L < 8) read distinct replicas whose bank windows
+// [4L*c, 4L*c + 4L) tile the 32 banks -- conflict-free for any residue mix.
+// With L >= 8 a quarter-warp lies inside one group and one copy suffices.
 
 uint32_t cells_per_word(int variant) { return variant == LHMM_VARIANT_SWAR8 ? 4u : 2u; }
 
-static void strides_for(uint32_t L, uint32_t H, bool replicate, uint32_t& P, uint32_t& copies,
+static void strides_for(uint32_t L, uint32_t H, uint32_t& P, uint32_t& copies,
                         uint32_t& copy_stride) {
-    if (L == 1) {
-        P = H | 1u;
-        copies = 1;
-        copy_stride = 0;
-    } else if (L == 32 || !replicate) {
-        P = H * L;
-        if (L < 32) P += L;  // unreplicated fallback: shift residue windows
-        copies = 1;
-        copy_stride = 0;
-    } else {
+    copies = L < 8 ? 8u / L : 1u;
+    if (copies > 1) {
         P = (H * L + 31u) / 32u * 32u;
-        copies = 32u / L;
-        copy_stride = 23u * P + L;
+        copy_stride = 23u * P + 4u * L;  // == 4L (mod 32)
+    } else {
+        P = H * L;
+        copy_stride = 0;
     }
 }
 
 uint64_t table_bytes_for(int variant, uint32_t L, uint32_t H, bool replicate) {
     (void)variant;
+    (void)replicate;
     uint32_t P, copies, cs;
-    strides_for(L, H, replicate, P, copies, cs);
+    strides_for(L, H, P, copies, cs);
     uint64_t words = copies > 1 ? uint64_t(copies - 1) * cs + 23ull * P : 23ull * P;
     return (words * 4 + 15) / 16 * 16;
 }
@@ -321,7 +317,7 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
                  bool replicate, TableImage& out) {
     const uint32_t cpw = cells_per_word(variant);
     uint32_t P, copies, cs;
-    strides_for(L, H, replicate, P, copies, cs);
+    strides_for(L, H, P, copies, cs);
     out.res_stride = P;
     out.copy_stride = copies > 1 ? cs : 0;
     out.words.assign(table_bytes_for(variant, L, H, replicate) / 4, 0);
@@ -334,8 +330,8 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
                     c[k] = (node > m || x > kUnknown) ? 0xff : costs[(node - 1) * 21 + x];
                 }
                 const uint32_t w = encode_word(variant, alg, c, cpw);
-                for (uint32_t g = 0; g < copies; ++g)
-                    out.words[size_t(g) * cs + size_t(x) * P + size_t(h) * L + oig] = w;
+                const size_t at = size_t(x) * P + size_t(h / 4) * 4 * L + 4 * oig + (h % 4);
+                for (uint32_t g = 0; g < copies; ++g) out.words[size_t(g) * cs + at] = w;
             }
 }
 

@@ -293,12 +293,14 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
     __shared__ __align__(8) uint64_t bar;
     stage_table(smem, p.table, p.table_bytes, &bar);
 
-    constexpr int G = 32 / L;  // sequences per warp
+    static_assert(H % 4 == 0, "rows are read four at a time");
+    constexpr int G = 32 / L;                    // sequences per warp
+    constexpr int COPIES = L < 8 ? 8 / L : 1;    // table replicas (one per quarter-warp group)
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t oig = lane & (L - 1);
     const uint32_t grp = lane / L;
     const uint32_t P = p.res_stride;
-    const uint32_t* tab_lane = smem + grp * p.copy_stride + oig;
+    const uint32_t* tab_lane = smem + (grp % COPIES) * p.copy_stride + 4u * oig;
 
     for (;;) {
         uint32_t item = 0;
@@ -318,7 +320,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
         uint32_t g[H];
 #pragma unroll
         for (int h = 0; h < H; ++h) g[h] = V::NEG;
-        uint32_t E = V::NEG;
+        // four independent running maxima keep the E chain short
+        uint32_t e0 = V::NEG, e1 = V::NEG, e2 = V::NEG, e3 = V::NEG;
 
         for (uint32_t r0 = 0; r0 < rows; r0 += 16) {
             const uint4 v = ld_stream(src + (r0 >> 4) * 512u);
@@ -342,19 +345,34 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
                         }
                         const uint32_t sh = V::shift(top, up);
 #pragma unroll
-                        for (int h = H - 1; h >= 1; --h) g[h] = V::cell(g[h - 1], tp[h * L], st);
-                        g[0] = V::cell(sh, tp[0], st);
+                        for (int h4 = H / 4 - 1; h4 >= 0; --h4) {
+                            const uint4 c = *reinterpret_cast<const uint4*>(tp + h4 * 4 * L);
+                            const int h = 4 * h4;
+                            g[h + 3] = V::cell(g[h + 2], c.w, st);
+                            g[h + 2] = V::cell(g[h + 1], c.z, st);
+                            g[h + 1] = V::cell(g[h], c.y, st);
+                            g[h] = V::cell(h ? g[h - 1] : sh, c.x, st);
+                        }
 #pragma unroll
-                        for (int h = 0; h + 1 < H; h += 2) E = V::acc2(E, g[h], g[h + 1]);
-                        if constexpr (H % 2) E = V::acc1(E, g[H - 1]);
+                        for (int h = 0; h < H; h += 8) {
+                            e0 = V::acc2(e0, g[h], g[h + 1]);
+                            e1 = V::acc2(e1, g[h + 2], g[h + 3]);
+                            if (h + 4 < H) {
+                                e2 = V::acc2(e2, g[h + 4], g[h + 5]);
+                                e3 = V::acc2(e3, g[h + 6], g[h + 7]);
+                            }
+                        }
                         if constexpr (V::kMsv) {
-                            E = V::template group_reduce<L>(E);
+                            const uint32_t E =
+                                V::template group_reduce<L>(V::acc2(V::acc2(e0, e1, e2), e3, e3));
+                            e0 = E;
                             V::update_B(st, E);
                         }
                     }
                 }
             }
         }
+        uint32_t E = V::acc2(V::acc2(e0, e1, e2), e3, e3);
         if constexpr (!V::kMsv) E = V::template group_reduce<L>(E);
         uint32_t raw = V::raw(E);
         if (p.fault && grp == 0 && raw < 255u) raw += 1u;  // verification aid

@@ -22,8 +22,8 @@ def oq(q):
 
 def rows_for(variant, L, m):
     cpw = 4 if variant == P.Variant.Swar8 else 2
-    rows = {P.Variant.Swar8: [2, 4, 8, 12, 16, 24, 32, 40, 48]}.get(
-        variant, [2, 4, 6, 8, 10, 12, 14, 16, 20, 24, 28, 32, 36, 40, 44, 48, 52, 56, 60, 64, 72])
+    rows = {P.Variant.Swar8: [4, 8, 12, 16, 24, 32, 40, 48]}.get(
+        variant, [4, 8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 52, 56, 60, 64, 68, 72])
     for h in rows:
         if cpw * L * h >= m:
             return h
