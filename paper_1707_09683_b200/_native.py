@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "_lib", "liblhmm_b200.so")
+# LHMM_LIB selects an experimental side build (tuning sweeps only)
+LIB_PATH = os.environ.get("LHMM_LIB") or os.path.join(PKG, "_lib", "liblhmm_b200.so")
 
 
 class NativeLibraryError(RuntimeError):

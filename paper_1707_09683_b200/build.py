@@ -51,7 +51,15 @@ def _compile(src, obj, verbose):
     return obj
 
 
-def build(verbose=False, jobs=None):
+def build(verbose=False, jobs=None, defines=(), tag=""):
+    """Build the library; `defines`/`tag` produce experimental side builds
+    (_build<tag>/, _lib<tag>/) used only by tuning sweeps."""
+    global BUILD, LIBDIR, LIB, COMMON
+    if tag:
+        BUILD = os.path.join(PKG, "_build" + tag)
+        LIBDIR = os.path.join(PKG, "_lib" + tag)
+        LIB = os.path.join(LIBDIR, "liblhmm_b200.so")
+    COMMON = COMMON + [f"-D{d}" for d in defines]
     sys.path.insert(0, CSRC)
     try:
         import gen_instances
@@ -82,4 +90,10 @@ def build(verbose=False, jobs=None):
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("-D", action="append", default=[])
+    ap.add_argument("--tag", default="")
+    a = ap.parse_args()
+    print(build(verbose=a.v, defines=a.D, tag=a.tag))

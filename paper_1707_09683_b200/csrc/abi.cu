@@ -15,6 +15,11 @@
 #include "lhmm_kernel.cuh"
 #include "gen/registry.inc"
 
+namespace lhmm {
+#include "calib_b200.inc"
+}  // namespace lhmm
+using lhmm::kCalib;
+
 using lhmm::set_error;
 
 namespace {
@@ -99,58 +104,88 @@ bool use_replica(int variant, uint32_t L, uint32_t H) {
     return L > 1 && L < 32 && lhmm::table_bytes_for(variant, L, H, true) <= kMaxTableBytes;
 }
 
-int resolve_variant(int variant, int alg, uint32_t m) {
-    (void)alg;
-    (void)m;
-    // measured on B200 (profiles/round1_sweep.md): the f16 FMA-pipe variant
-    // is fastest for both algorithms at every model length 48..2405
-    if (variant == LHMM_VARIANT_AUTO) return LHMM_VARIANT_FP16;
-    return variant;
+double calib_rate(int variant, int alg, uint32_t L, uint32_t H) {
+    for (const auto& c : kCalib)
+        if (c.variant == variant && c.alg == alg && uint32_t(c.lanes) == L && uint32_t(c.rows) == H)
+            return c.cell_gcups;
+    return -1.0;
 }
 
-// B200 geometry policy (the analogue of lane_count/select_geometry,
-// src/select.cpp:16-48): among instantiated (L, H) whose capacity CPW*L*H
-// covers the model, minimise the estimated lane-instructions per residue
-// row, L*(H*w + overhead(L)).
-int select_geometry_impl(uint32_t m, int alg, int variant, uint32_t* Lout, uint32_t* Hout) {
-    if (m < 1) return set_error(LHMM_ERR_CONTRACT, "model length must be positive");
-    variant = resolve_variant(variant, alg, m);
-    const uint32_t cpw = lhmm::cells_per_word(variant);
-    int n;
-    const int* rows = rows_list(variant, &n);
-    double wcell;
+// Fallback cost model for points without a measurement: estimated
+// lane-instructions per residue row, L*(H*w + overhead(L)), as a rate.
+double model_rate(int variant, int alg, uint32_t L, uint32_t H) {
+    double w;
     if (variant == LHMM_VARIANT_SWAR8)
-        wcell = alg == LHMM_MSV ? 30.0 : 26.0;
+        w = alg == LHMM_MSV ? 30.0 : 26.0;
     else if (variant == LHMM_VARIANT_FP16)
-        wcell = alg == LHMM_MSV ? 4.5 : 3.0;
+        w = alg == LHMM_MSV ? 4.5 : 3.0;
     else
-        wcell = alg == LHMM_MSV ? 4.5 : 3.5;
-    double best = 1e300;
-    uint32_t bL = 0, bH = 0;
-    for (uint32_t L = 1; L <= 32; L *= 2) {
-        uint32_t H = 0;
-        for (int i = 0; i < n; ++i)
-            if (uint64_t(cpw) * L * uint32_t(rows[i]) >= m) {
-                H = uint32_t(rows[i]);
-                break;
+        w = alg == LHMM_MSV ? 4.5 : 3.5;
+    const double lg = std::log2(double(L));
+    const double ovh = 14.0 + (L > 1 ? 3.0 : 0.0) + (alg == LHMM_MSV ? 4.0 + 3.0 * lg : 0.0);
+    const double cpw = double(lhmm::cells_per_word(variant));
+    return 2.0e4 * cpw * double(H) / (double(H) * w + ovh);
+}
+
+struct Choice {
+    int variant = 0;
+    uint32_t L = 0, H = 0;
+    double predicted = -1.0;
+};
+
+// B200 geometry policy (the analogue of lane_count/select_geometry,
+// src/select.cpp:16-48): among the compiled (variant, L, H) whose capacity
+// CPW*L*H covers the model, maximise predicted throughput
+//     rate(L, H) * M / capacity * fill
+// where rate is the computed-cell throughput measured on B200 by the
+// calibration sweep (calib_b200.inc from scripts/calibrate.py) and fill the
+// fraction of the persistent grid's warps the database's work items
+// (tiles * L) can occupy.  `want_L` pins the lane count when non-zero.
+Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64_t n_tiles,
+                       int sm_count) {
+    Choice best;
+    const int vs[2] = {LHMM_VARIANT_FP16, LHMM_VARIANT_DPX16};
+    const int nv = variant == LHMM_VARIANT_AUTO ? 2 : 1;
+    for (int vi = 0; vi < nv; ++vi) {
+        const int v = variant == LHMM_VARIANT_AUTO ? vs[vi] : variant;
+        const uint32_t cpw = lhmm::cells_per_word(v);
+        int n;
+        const int* rows = rows_list(v, &n);
+        for (uint32_t L = 1; L <= 32; L *= 2) {
+            if (want_L && L != want_L) continue;
+            for (int i = 0; i < n; ++i) {
+                const uint32_t H = uint32_t(rows[i]);
+                const uint64_t cap = uint64_t(cpw) * L * H;
+                if (cap < m) continue;
+                if (lhmm::table_bytes_for(v, L, H, true) > kMaxTableBytes) continue;
+                double rate = calib_rate(v, alg, L, H);
+                if (rate < 0) rate = model_rate(v, alg, L, H);
+                double fill = 1.0;
+                if (n_tiles > 0 && sm_count > 0) {
+                    const double slots = double(sm_count) * (lhmm::kMaxThreads / 32);
+                    fill = std::min(1.0, double(n_tiles) * double(L) / slots);
+                }
+                const double pred = rate * double(m) / double(cap) * fill;
+                if (pred > best.predicted * 1.0001) {
+                    best.variant = v;
+                    best.L = L;
+                    best.H = H;
+                    best.predicted = pred;
+                }
             }
-        if (!H) continue;
-        if (lhmm::table_bytes_for(variant, L, H, use_replica(variant, L, H)) > kMaxTableBytes)
-            continue;
-        double lg = std::log2(double(L));
-        double ovh = 14.0 + (L > 1 ? 3.0 : 0.0) + (alg == LHMM_MSV ? 4.0 + 3.0 * lg : 0.0);
-        double cost = double(L) * (double(H) * wcell + ovh);
-        if (cost < best) {
-            best = cost;
-            bL = L;
-            bH = H;
         }
     }
-    if (!bL)
+    return best;
+}
+
+int select_geometry_impl(uint32_t m, int alg, int variant, uint32_t* Lout, uint32_t* Hout) {
+    if (m < 1) return set_error(LHMM_ERR_CONTRACT, "model length must be positive");
+    Choice c = choose_geometry(m, alg, variant, 0, 0, 0);
+    if (!c.L)
         return set_error(LHMM_ERR_DATA,
                          "no instantiated geometry covers model length " + std::to_string(m));
-    *Lout = bL;
-    *Hout = bH;
+    *Lout = c.L;
+    *Hout = c.H;
     return LHMM_OK;
 }
 
@@ -257,21 +292,23 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_SWAR8)
         return set_error(LHMM_ERR_CONTRACT, "unknown kernel variant");
     ProfileSlot& pf = c->profiles[c->current];
-    const int variant = resolve_variant(opt->variant, opt->alg, pf.m);
+    int variant = opt->variant;
     uint32_t L = opt->lanes, H = opt->rows;
-    if (L == 0 || H == 0) {
-        uint32_t aL, aH;
-        if (int rc = select_geometry_impl(pf.m, opt->alg, variant, &aL, &aH)) return rc;
-        if (L == 0) L = aL;
-        if (H == 0) {
-            // smallest instantiated H covering the model at lane count L
-            int n;
-            const int* rows = rows_list(variant, &n);
-            H = 0;
-            for (int i = 0; i < n && !H; ++i)
-                if (uint64_t(lhmm::cells_per_word(variant)) * L * uint32_t(rows[i]) >= pf.m)
-                    H = uint32_t(rows[i]);
-            if (!H) H = aH;
+    if (L != 0 && (L > 32 || (L & (L - 1))))
+        return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,32]");
+    if (H == 0) {
+        Choice ch = choose_geometry(pf.m, opt->alg, variant, L, c->db.n_tiles, c->sm_count);
+        if (!ch.L)
+            return set_error(LHMM_ERR_DATA,
+                             "no instantiated geometry covers model length " + std::to_string(pf.m));
+        variant = ch.variant;
+        L = ch.L;
+        H = ch.H;
+    } else {
+        if (variant == LHMM_VARIANT_AUTO) variant = LHMM_VARIANT_FP16;
+        if (L == 0) {
+            Choice ch = choose_geometry(pf.m, opt->alg, variant, 0, c->db.n_tiles, c->sm_count);
+            L = ch.L ? ch.L : 1;
         }
     }
     if (L < 1 || L > 32 || (L & (L - 1)))

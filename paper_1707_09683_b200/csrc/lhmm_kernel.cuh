@@ -40,7 +40,10 @@ namespace lhmm {
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kResidueRows = 23;  // codes 0..20, 21 '@', 22 '#'
 constexpr int kPadCode = 22;
-constexpr int kMaxThreads = 512;
+#ifndef LHMM_MAX_THREADS
+#define LHMM_MAX_THREADS 512
+#endif
+constexpr int kMaxThreads = LHMM_MAX_THREADS;
 
 struct KParams {
     const uint8_t* db;          // packed tiles
@@ -108,6 +111,21 @@ __device__ __forceinline__ uint4 ld_stream(const uint8_t* p) {
     return __ldcs(reinterpret_cast<const uint4*>(p));
 }
 
+// Max of a u32 over the L lanes of this lane's group (vwarp::max_reduce,
+// src/vwarp.cpp:66-89).  A whole warp uses one REDUX.MAX; smaller aligned
+// groups use log2(L) xor shuffles (a REDUX with per-group masks serialises
+// over the distinct masks -- measured 40% slower on B200).
+template <int L>
+__device__ __forceinline__ uint32_t group_max(uint32_t v) {
+    if constexpr (L == 32) {
+        return __reduce_max_sync(kFull, v);
+    } else {
+#pragma unroll
+        for (int off = 1; off < L; off <<= 1) v = max(v, __shfl_xor_sync(kFull, v, off));
+        return v;
+    }
+}
+
 __device__ __forceinline__ __half2 as_h2(uint32_t u) {
     return *reinterpret_cast<__half2*>(&u);
 }
@@ -163,10 +181,10 @@ struct Dpx16 {
     }
     template <int L>
     __device__ static __forceinline__ uint32_t group_reduce(uint32_t E) {
-        uint32_t e = __vmaxu2(E, __byte_perm(E, E, 0x1032));
-#pragma unroll
-        for (int off = 1; off < L; off <<= 1) e = __vmaxu2(e, __shfl_xor_sync(kFull, e, off));
-        return e;
+        // both halves -> their max; then one REDUX across the lane group
+        // (equal halves make the u32 order the u16 order)
+        const uint32_t e = __vmaxu2(E, __byte_perm(E, E, 0x1032));
+        return group_max<L>(e);
     }
     __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
         s.B = __viaddmax_s16x2(e, s.ntj2, s.base2);
@@ -225,10 +243,10 @@ struct Fp16 {
     }
     template <int L>
     __device__ static __forceinline__ uint32_t group_reduce(uint32_t E) {
-        uint32_t e = __vmaxu2(E, __byte_perm(E, E, 0x1032));
-#pragma unroll
-        for (int off = 1; off < L; off <<= 1) e = __vmaxu2(e, __shfl_xor_sync(kFull, e, off));
-        return e;
+        // both halves -> their max; then one REDUX across the lane group
+        // (equal halves make the u32 order the u16 order)
+        const uint32_t e = __vmaxu2(E, __byte_perm(E, E, 0x1032));
+        return group_max<L>(e);
     }
     __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
         // max(base, E - (tec+tjb)); the difference may be negative -> f16 max
@@ -274,9 +292,7 @@ struct Swar8 {
     __device__ static __forceinline__ uint32_t group_reduce(uint32_t E) {
         uint32_t e = __vmaxu4(E, __byte_perm(E, E, 0x1032));
         e = __vmaxu4(e, __byte_perm(e, e, 0x2301));
-#pragma unroll
-        for (int off = 1; off < L; off <<= 1) e = __vmaxu4(e, __shfl_xor_sync(kFull, e, off));
-        return e;
+        return group_max<L>(e);
     }
     __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
         s.B = __vmaxu4(s.base4, __vsubus4(e, s.tj4));
@@ -323,55 +339,71 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
         // four independent running maxima keep the E chain short
         uint32_t e0 = V::NEG, e1 = V::NEG, e2 = V::NEG, e3 = V::NEG;
 
+        // Rows run in 16-row chunks (one 128-bit residue load per lane), fully
+        // unrolled.  Slot naming rotates with the row: at chunk row r, model
+        // cell h sits in register g[(h - r) mod H].  The diagonal dependency
+        // (cell h <- cell h-1 of the previous row) then becomes an in-place
+        // update g[s] = f(g[s]) with compile-time s, so no register moves are
+        // needed inside the chunk; one slot permutation restores the naming
+        // after 16 rows (free when H divides 16).
         for (uint32_t r0 = 0; r0 < rows; r0 += 16) {
             const uint4 v = ld_stream(src + (r0 >> 4) * 512u);
-            uint32_t w0 = v.x, w1 = v.y, w2 = v.z, w3 = v.w;
-#pragma unroll 1
-            for (uint32_t q = 0; q < 4; ++q) {
-                const uint32_t cur = w0;
-                w0 = w1;
-                w1 = w2;
-                w2 = w3;
+            const uint32_t wds[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (r0 + 4u * q >= rows) goto finished;  // warp-uniform
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                    if (r0 + q * 4 + b < rows) {
-                        const uint32_t x = (cur >> (8 * b)) & 0xffu;
-                        const uint32_t* tp = tab_lane + x * P;
-                        const uint32_t top = g[H - 1];
-                        uint32_t up = V::NEG;
-                        if constexpr (L > 1) {
-                            up = __shfl_up_sync(kFull, top, 1, L);
-                            if (oig == 0) up = V::NEG;
-                        }
-                        const uint32_t sh = V::shift(top, up);
+                    const int r = 4 * q + b;
+                    const uint32_t x = (wds[q] >> (8 * b)) & 0xffu;
+                    const uint32_t* tp = tab_lane + x * P;
+                    // the register holding cell H-1 becomes cell 0 (stripe shift)
+                    constexpr int kTopBase = H - 1;
+                    const int stop = ((kTopBase - r) % H + H) % H;
+                    uint32_t up = V::NEG;
+                    if constexpr (L > 1) {
+                        up = __shfl_up_sync(kFull, g[stop], 1, L);
+                        if (oig == 0) up = V::NEG;
+                    }
 #pragma unroll
-                        for (int h4 = H / 4 - 1; h4 >= 0; --h4) {
-                            const uint4 c = *reinterpret_cast<const uint4*>(tp + h4 * 4 * L);
-                            const int h = 4 * h4;
-                            g[h + 3] = V::cell(g[h + 2], c.w, st);
-                            g[h + 2] = V::cell(g[h + 1], c.z, st);
-                            g[h + 1] = V::cell(g[h], c.y, st);
-                            g[h] = V::cell(h ? g[h - 1] : sh, c.x, st);
-                        }
+                    for (int h4 = H / 4 - 1; h4 >= 0; --h4) {
+                        const uint4 c = *reinterpret_cast<const uint4*>(tp + h4 * 4 * L);
+                        const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-                        for (int h = 0; h < H; h += 8) {
-                            e0 = V::acc2(e0, g[h], g[h + 1]);
-                            e1 = V::acc2(e1, g[h + 2], g[h + 3]);
-                            if (h + 4 < H) {
-                                e2 = V::acc2(e2, g[h + 4], g[h + 5]);
-                                e3 = V::acc2(e3, g[h + 6], g[h + 7]);
-                            }
+                        for (int k = 3; k >= 0; --k) {
+                            const int h = 4 * h4 + k;
+                            const int sl = ((h - 1 - r) % H + H) % H;
+                            const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
+                            g[sl] = V::cell(in, cw[k], st);
                         }
-                        if constexpr (V::kMsv) {
-                            const uint32_t E =
-                                V::template group_reduce<L>(V::acc2(V::acc2(e0, e1, e2), e3, e3));
-                            e0 = E;
-                            V::update_B(st, E);
+                    }
+#pragma unroll
+                    for (int h = 0; h < H; h += 8) {
+                        e0 = V::acc2(e0, g[h], g[h + 1]);
+                        e1 = V::acc2(e1, g[h + 2], g[h + 3]);
+                        if (h + 4 < H) {
+                            e2 = V::acc2(e2, g[h + 4], g[h + 5]);
+                            e3 = V::acc2(e3, g[h + 6], g[h + 7]);
                         }
+                    }
+                    if constexpr (V::kMsv) {
+                        const uint32_t E =
+                            V::template group_reduce<L>(V::acc2(V::acc2(e0, e1, e2), e3, e3));
+                        e0 = E;
+                        V::update_B(st, E);
                     }
                 }
             }
+            if constexpr (16 % H != 0) {
+                // after 16 rows cell h sits in g[(h - 16) mod H]: rename back
+                uint32_t t[H];
+#pragma unroll
+                for (int h = 0; h < H; ++h) t[h] = g[((h - 16) % H + H) % H];
+#pragma unroll
+                for (int h = 0; h < H; ++h) g[h] = t[h];
+            }
         }
+    finished:
         uint32_t E = V::acc2(V::acc2(e0, e1, e2), e3, e3);
         if constexpr (!V::kMsv) E = V::template group_reduce<L>(E);
         uint32_t raw = V::raw(E);

@@ -1,0 +1,58 @@
+#!/usr/bin/env python
+"""Calibration sweep for the B200 geometry policy (the analogue of the
+reference's calibrate_hmax, src/select.cpp:80-105): for every instantiated
+(variant, alg, L, H) measure device GCUPS on the 1M Swiss-Prot-like set with
+a model that exactly fills the geometry (M = CPW*L*H, capped at 2405), and
+report computed-cell efficiency = GCUPS * capacity / M.  Output: JSON lines."""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "paper_1707_09683_b200", "csrc"))
+
+import gen_instances  # noqa: E402
+import paper_1707_09683_b200 as P  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--nseq", type=int, default=1_000_000)
+    ap.add_argument("--variants", default="fp16")
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    db = P.Rng(0x5EED).lognormal_records(args.nseq, 290, 0.65, 2)
+    q = P.QuantParams()
+    s = P.Scanner(0)
+    s.set_database(db)
+    res = db.total_residues()
+    vmap = {"dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16, "swar8": P.Variant.Swar8}
+    for vn in args.variants.split(","):
+        cpw = 4 if vn == "swar8" else 2
+        for L in gen_instances.LANES:
+            for H in gen_instances.ROWS[vn]:
+                cap = cpw * L * H
+                m = min(cap, 4096)
+                hmm = P.Rng(9000 + m).random_profile(m)
+                s.set_profile(P.quantize_emissions(hmm, q), q, hmm.lambda_, hmm.tau)
+                for a in ("msv", "ssv"):
+                    alg = P.Algorithm.Msv if a == "msv" else P.Algorithm.Ssv
+                    opt = P.ScanOptions(alg=alg, variant=vmap[vn], lanes=L, rows=H)
+                    try:
+                        s.scan(opt)
+                        t = min(s.scan(opt).stats["device_ms"] for _ in range(args.reps))
+                    except Exception as e:  # noqa: BLE001  (e.g. table too large)
+                        print(json.dumps({"variant": vn, "alg": a, "lanes": L, "rows": H,
+                                          "error": str(e)}), flush=True)
+                        continue
+                    g = res * m / (t * 1e-3) / 1e9
+                    print(json.dumps({"variant": vn, "alg": a, "lanes": L, "rows": H, "M": m,
+                                      "gcups": round(g, 1),
+                                      "cell_gcups": round(g * cap / m, 1)}), flush=True)
+    s.close()
+
+
+if __name__ == "__main__":
+    main()

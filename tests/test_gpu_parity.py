@@ -22,7 +22,8 @@ def oq(q):
 
 def rows_for(variant, L, m):
     cpw = 4 if variant == P.Variant.Swar8 else 2
-    rows = {P.Variant.Swar8: [4, 8, 12, 16, 24, 32, 40, 48]}.get(
+    rows = {P.Variant.Swar8: [4, 8, 16, 24, 32],
+            P.Variant.Dpx16: [4, 8, 12, 16, 24, 32, 40, 48, 56, 64]}.get(
         variant, [4, 8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 52, 56, 60, 64, 68, 72])
     for h in rows:
         if cpw * L * h >= m:
@@ -43,7 +44,7 @@ def scan(costs, q, db, hmm, **kw):
 def test_every_lane_count_matches_oracle(ora, variant, alg, L):
     rng = P.Rng(1000 + 97 * L + int(alg) + 7 * int(variant))
     cpw = 4 if variant == P.Variant.Swar8 else 2
-    maxcap = cpw * L * (48 if variant == P.Variant.Swar8 else 72)
+    maxcap = cpw * L * {P.Variant.Swar8: 32, P.Variant.Dpx16: 64}.get(variant, 72)
     for t, q in enumerate(QUANTS):
         m = int(7 + rng.next() % max(1, min(maxcap, 2405) - 6))
         hmm = rng.random_profile(m)
