@@ -230,9 +230,11 @@ struct lhmm_context {
     std::vector<ProfileSlot> profiles;
     int current = -1;
 
-    // database
+    // database (packed host image in a reused pinned buffer)
     lhmm::PackedDb db;
     bool have_db = false;
+    uint8_t* pinned = nullptr;
+    size_t pinned_cap = 0;
     uint64_t db_gen = 0;
     DevBuf<uint8_t> d_db;
     DevBuf<uint64_t> d_tile_off;
@@ -489,7 +491,9 @@ int lhmm_context_destroy(lhmm_context* c) {
     if (!c) return LHMM_OK;
     DeviceGuard g(c->device);
     cudaStreamSynchronize(c->stream);
+    c->db.data = nullptr;  // owned by the pinned cache
     lhmm::free_packed(c->db, pinned_free);
+    if (c->pinned) pinned_free(c->pinned);
     c->d_db.release();
     c->d_tile_off.release();
     c->d_lens.release();
@@ -570,11 +574,20 @@ int lhmm_set_database(lhmm_context* c, const uint8_t* residues, const uint64_t* 
     if (!c || !offsets || (!residues && nseq && offsets[nseq] > 0))
         return set_error(LHMM_ERR_CONTRACT, "null argument");
     DeviceGuard g(c->device);
+    c->db.data = nullptr;  // the pinned cache keeps the buffer
     lhmm::free_packed(c->db, pinned_free);
     c->have_db = false;
     static const uint8_t empty = 0;
+    auto alloc = [c](size_t n) -> void* {
+        if (n > c->pinned_cap) {
+            if (c->pinned) pinned_free(c->pinned);
+            c->pinned = static_cast<uint8_t*>(pinned_alloc(n));
+            c->pinned_cap = c->pinned ? n : 0;
+        }
+        return c->pinned;
+    };
     if (int rc = lhmm::pack_database(residues ? residues : &empty, offsets, nseq, rank, world,
-                                     c->db, pinned_alloc, pinned_free))
+                                     c->db, alloc))
         return rc;
     if (int rc = upload_db(c)) return rc;
     c->have_db = true;

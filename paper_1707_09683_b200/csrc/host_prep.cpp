@@ -115,8 +115,7 @@ int build_length_tables(const lhmm_quant& q, double lambda, double tau, int alg,
 // packer
 
 int pack_database(const uint8_t* residues, const uint64_t* offsets, uint64_t nseq, uint32_t rank,
-                  uint32_t world, PackedDb& out, void* (*host_alloc)(size_t),
-                  void (*host_free)(void*)) {
+                  uint32_t world, PackedDb& out, const HostAlloc& host_alloc) {
     if (world < 1 || rank >= world) return set_error(LHMM_ERR_CONTRACT, "bad shard rank/count");
     if (nseq >= 0xffffffffull)
         return set_error(LHMM_ERR_CONTRACT, "at most 2^32-2 sequences per database");
@@ -242,11 +241,10 @@ int pack_database(const uint8_t* residues, const uint64_t* offsets, uint64_t nse
                     src[r];
         }
     }
-    (void)host_free;
     return LHMM_OK;
 }
 
-void free_packed(PackedDb& db, void (*host_free)(void*)) {
+void free_packed(PackedDb& db, const HostFree& host_free) {
     if (db.data) host_free(db.data);
     db = PackedDb{};
 }
@@ -413,8 +411,7 @@ int lhmm_shard_plan(const uint64_t* offsets, uint64_t nseq, uint32_t rank, uint3
     std::vector<uint64_t> off(offsets, offsets + nseq + 1);
     for (auto& o : off) o -= offsets[0];
     if (int rc = lhmm::pack_database(zeros.data(), off.data(), nseq, rank, world, db,
-                                     [](size_t n) -> void* { return std::malloc(n); },
-                                     [](void* p) { std::free(p); }))
+                                     [](size_t n) -> void* { return std::malloc(n); }))
         return rc;
     *count = db.n_local;
     if (out) std::memcpy(out, db.global_idx.data(), db.global_idx.size() * sizeof(uint64_t));

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -45,10 +46,11 @@ struct PackedDb {
     uint64_t n_local = 0;
     uint64_t n_tiles = 0;
 };
+using HostAlloc = std::function<void*(size_t)>;
+using HostFree = std::function<void(void*)>;
 int pack_database(const uint8_t* residues, const uint64_t* offsets, uint64_t nseq, uint32_t rank,
-                  uint32_t world, PackedDb& out, void* (*host_alloc)(size_t),
-                  void (*host_free)(void*));
-void free_packed(PackedDb& db, void (*host_free)(void*));
+                  uint32_t world, PackedDb& out, const HostAlloc& host_alloc);
+void free_packed(PackedDb& db, const HostFree& host_free);
 
 // profile table image in the kernel's shared-memory layout
 struct TableImage {

@@ -303,6 +303,16 @@ struct Swar8 {
 // ---------------------------------------------------------------------------
 // the scan kernel
 
+// Rows per unrolled iteration: the largest of 16/8/4 whose unrolled body
+// (~H*(3.75|2.75)+20 instructions per row for MSV|SSV, 16 B each) stays
+// within ~32 KB of SASS -- ncu showed no_instruction stalls beyond that.
+template <class V, int H>
+__host__ __device__ constexpr int rows_per_iter() {
+    constexpr int per_row = H * (V::kMsv ? 15 : 11) / 4 + 20;
+    constexpr int words = V::CPW == 4 ? per_row * 3 : per_row;  // SWAR8 ops are emulated
+    return 16 * words * 16 <= 32768 ? 16 : (8 * words * 16 <= 32768 ? 8 : 4);
+}
+
 template <class V, int L, int H>
 __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
     extern __shared__ __align__(128) uint32_t smem[];
@@ -339,18 +349,33 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
         // four independent running maxima keep the E chain short
         uint32_t e0 = V::NEG, e1 = V::NEG, e2 = V::NEG, e3 = V::NEG;
 
-        // Rows run in 16-row chunks (one 128-bit residue load per lane), fully
-        // unrolled.  Slot naming rotates with the row: at chunk row r, model
-        // cell h sits in register g[(h - r) mod H].  The diagonal dependency
-        // (cell h <- cell h-1 of the previous row) then becomes an in-place
-        // update g[s] = f(g[s]) with compile-time s, so no register moves are
-        // needed inside the chunk; one slot permutation restores the naming
-        // after 16 rows (free when H divides 16).
-        for (uint32_t r0 = 0; r0 < rows; r0 += 16) {
-            const uint4 v = ld_stream(src + (r0 >> 4) * 512u);
-            const uint32_t wds[4] = {v.x, v.y, v.z, v.w};
+        // Rows run in RPI-row iterations, fully unrolled (RPI = 16, 8 or 4,
+        // chosen so the unrolled body stays inside the SM instruction cache).
+        // Slot naming rotates with the row: at iteration row r, model cell h
+        // sits in register g[(h - r) mod H].  The diagonal dependency (cell h
+        // <- cell h-1 of the previous row) then becomes an in-place update
+        // g[s] = f(g[s]) with compile-time s -- no register moves inside the
+        // iteration; one slot permutation restores the naming after RPI rows
+        // (free when H divides RPI).
+        constexpr int RPI = rows_per_iter<V, H>();
+        for (uint32_t r0 = 0; r0 < rows; r0 += RPI) {
+            uint32_t wds[RPI / 4];
+            const uint8_t* chunk = src + (r0 >> 4) * 512u;
+            if constexpr (RPI == 16) {
+                const uint4 v = ld_stream(chunk);
+                wds[0] = v.x;
+                wds[1] = v.y;
+                wds[2] = v.z;
+                wds[3] = v.w;
+            } else if constexpr (RPI == 8) {
+                const uint2 v = __ldcs(reinterpret_cast<const uint2*>(chunk + (r0 & 8u)));
+                wds[0] = v.x;
+                wds[1] = v.y;
+            } else {
+                wds[0] = __ldcs(reinterpret_cast<const unsigned int*>(chunk + (r0 & 12u)));
+            }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < RPI / 4; ++q) {
                 if (r0 + 4u * q >= rows) goto finished;  // warp-uniform
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
@@ -358,8 +383,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
                     const uint32_t x = (wds[q] >> (8 * b)) & 0xffu;
                     const uint32_t* tp = tab_lane + x * P;
                     // the register holding cell H-1 becomes cell 0 (stripe shift)
-                    constexpr int kTopBase = H - 1;
-                    const int stop = ((kTopBase - r) % H + H) % H;
+                    const int stop = ((H - 1 - r) % H + H) % H;
                     uint32_t up = V::NEG;
                     if constexpr (L > 1) {
                         up = __shfl_up_sync(kFull, g[stop], 1, L);
@@ -394,11 +418,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
                     }
                 }
             }
-            if constexpr (16 % H != 0) {
-                // after 16 rows cell h sits in g[(h - 16) mod H]: rename back
+            if constexpr (RPI % H != 0) {
+                // after RPI rows cell h sits in g[(h - RPI) mod H]: rename back
                 uint32_t t[H];
 #pragma unroll
-                for (int h = 0; h < H; ++h) t[h] = g[((h - 16) % H + H) % H];
+                for (int h = 0; h < H; ++h) t[h] = g[((h - RPI) % H + H) % H];
 #pragma unroll
                 for (int h = 0; h < H; ++h) g[h] = t[h];
             }
