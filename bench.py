@@ -229,6 +229,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--models", default="", help="override model lengths, e.g. 1000,2405")
     ap.add_argument("--algs", default="", help="override algorithms: msv, ssv or both")
+    ap.add_argument("--backend", default=os.environ.get("LHMM_DIST_BACKEND", "nccl"),
+                    help="torch.distributed backend for N>1 (gloo lets ranks share one GPU)")
     ap.add_argument("--lanes", type=int, default=0)
     ap.add_argument("--rows", type=int, default=0)
     args = ap.parse_args()
@@ -250,11 +252,17 @@ def main():
     rank, world, local = dist_env()
     if world != args.gpus:
         log(f"note: WORLD_SIZE={world} but --gpus={args.gpus}; using WORLD_SIZE")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
+    comm_dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.backend)
+            comm_dev = torch.device("cpu")
     desc, wl_alg, models_m, nseq, gen = WORKLOADS[args.workload]
     variant = {"auto": P.Variant.Auto, "dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16,
                "swar8": P.Variant.Swar8}[args.variant]
@@ -301,20 +309,20 @@ def main():
                 per_launch[k].append(st["device_ms"])
         return launches
 
+    gathered = {"validated": False}
+
     def gather_results():
-        """Per-sequence raw + pass bytes of every scan to rank 0 (NCCL gather)."""
+        """Per-sequence raw + pass bytes of every scan to rank 0 (one gather per
+        scan; NCCL over NVLink on the box, gloo when ranks share a GPU)."""
         if world == 1:
             return
-        counts = torch.tensor([n_local], device="cuda")
-        allc = [torch.zeros_like(counts) for _ in range(world)]
-        dist.all_gather(allc, counts)
-        mx = int(max(int(c) for c in allc))
+        from paper_1707_09683_b200.shard import gather_to_rank0
+        gi = gidx.to(comm_dev)
         for k in range(len(scans)):
-            buf = torch.zeros(2, mx, dtype=torch.uint8, device="cuda")
-            buf[0, :n_local] = outs[k][0][:n_local]
-            buf[1, :n_local] = outs[k][1][:n_local]
-            glist = [torch.zeros_like(buf) for _ in range(world)] if rank == 0 else None
-            dist.gather(buf, glist, dst=0)
+            gather_to_rank0(dist, outs[k][0][:n_local].to(comm_dev),
+                            outs[k][1][:n_local].to(comm_dev), gi, db.count, as_numpy=False,
+                            validate=not gathered["validated"])
+        gathered["validated"] = True
 
     for _ in range(args.warmup):
         step(False)
@@ -337,9 +345,9 @@ def main():
         if dist:
             dist.barrier()
     ms = ev0.elapsed_time(ev1)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=comm_dev)
     cells_local = sum(dbstats["residues"] * m for _, m, _ in scans) * args.steps
-    cells_t = torch.tensor([float(cells_local)], dtype=torch.float64, device="cuda")
+    cells_t = torch.tensor([float(cells_local)], dtype=torch.float64, device=comm_dev)
     if dist:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         dist.all_reduce(cells_t, op=dist.ReduceOp.SUM)
@@ -351,11 +359,13 @@ def main():
     e2e = None
     if not args.no_e2e:
         def e2e_step():
-            s.upload_database()  # H2D of the packed (pinned) database
+            # H2D of the packed (pinned) database overlapped with the first
+            # scan (lhmm_scan_streamed), the other models on the resident
+            # copy; every scan ends with the D2H of its raw + pass bytes
             d2h = 0
             for k, (pid, m, a) in enumerate(scans):
                 s.select_profile(pid)
-                rep = s.scan(opt_for(a))  # kernel + D2H of raw and pass bytes
+                rep = s.scan_streamed(opt_for(a), 8) if k == 0 else s.scan(opt_for(a))
                 d2h += 2 * int(rep.raw.size)
             return d2h
         for _ in range(max(1, args.warmup)):
@@ -370,13 +380,15 @@ def main():
             d2h = e2e_step()
         e1.record(stream)
         torch.cuda.synchronize()
-        ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=comm_dev)
         if dist:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         h2d = dbstats["packed_bytes"] + 16 * dbstats["tiles"] * 32
         e2e = {"value": round(total_cells / (float(ems.item()) * 1e-3) / 1e9, 3), "unit": "GCUPS",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "path": "C ABI lhmm_upload_database + lhmm_scan (host outputs) per model"}
+               "path": "C ABI: lhmm_scan_streamed (H2D of the packed pinned database in 8 "
+                        "pieces overlapped with the first scan) + lhmm_scan per further model, "
+                        "host outputs"}
 
     if rank != 0:
         if dist:

@@ -173,6 +173,14 @@ int lhmm_scan(lhmm_context* ctx, const lhmm_scan_options* opt, uint8_t* raw_out,
 int lhmm_scan_device(lhmm_context* ctx, const lhmm_scan_options* opt, uint8_t* d_raw,
                      uint8_t* d_pass, lhmm_scan_stats* stats);
 
+/* End-to-end scan from the packed HOST image: the database bytes are copied
+ * host->device in `segments` byte-balanced pieces on a copy stream while each
+ * piece is scanned as soon as it lands (H2D overlapped with the kernels);
+ * raw/pass are host arrays as in lhmm_scan.  device_ms spans the first copy
+ * to the last kernel. */
+int lhmm_scan_streamed(lhmm_context* ctx, const lhmm_scan_options* opt, int segments,
+                       uint8_t* raw_out, uint8_t* pass_out, lhmm_scan_stats* stats);
+
 /* SSV over all sequences, then MSV over the survivors (pass bit set),
  * compacted on the device.  ssv_raw/pass for all; msv_raw valid where
  * pass_out != 0, else 0.  Returns survivors via *rescored. */

@@ -75,6 +75,8 @@ SIGNATURES = {
     "lhmm_scan": (C.c_int, [vp, C.POINTER(ScanOptionsC), u8p, u8p, C.POINTER(ScanStatsC)]),
     "lhmm_scan_device": (C.c_int, [vp, C.POINTER(ScanOptionsC), vp, vp,
                                    C.POINTER(ScanStatsC)]),
+    "lhmm_scan_streamed": (C.c_int, [vp, C.POINTER(ScanOptionsC), C.c_int, u8p, u8p,
+                                     C.POINTER(ScanStatsC)]),
     "lhmm_filter_pipeline": (C.c_int, [vp, C.c_double, C.c_int, u8p, u8p, u8p, u64p,
                                        C.POINTER(ScanStatsC), C.POINTER(ScanStatsC)]),
     "lhmm_rng_create": (C.c_int, [C.c_uint64, C.POINTER(vp)]),

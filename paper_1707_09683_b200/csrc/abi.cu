@@ -1,6 +1,7 @@
 // abi.cu -- the C ABI (include/lhmm_b200.h): device context, profile and
 // database residency, geometry policy and the scan launch.
 #include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -224,6 +225,8 @@ struct lhmm_context {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t copy_stream = nullptr;   // H2D of streamed scans
+    std::vector<cudaEvent_t> seg_events;
     int sm_count = 0, sm_clock_khz = 0, cc_major = 0, cc_minor = 0;
 
     // profiles (slot 0 is what lhmm_set_profile replaces)
@@ -243,6 +246,18 @@ struct lhmm_context {
     DevBuf<uint8_t> d_raw, d_pass;
 
     std::map<std::tuple<int, int, uint32_t, uint32_t, size_t>, int> occupancy;
+
+    // on-device pipeline scratch (survivor compaction)
+    struct Pipe {
+        DevBuf<uint32_t> flags, pos, new_lens, new_out, src_slot;
+        DevBuf<uint64_t> tile_bytes, new_off;
+        DevBuf<uint8_t> db, msv, msv_pass, temp;
+        void release() {
+            flags.release(); pos.release(); new_lens.release(); new_out.release();
+            src_slot.release(); tile_bytes.release(); new_off.release(); db.release();
+            msv.release(); msv_pass.release(); temp.release();
+        }
+    } pipe;
 };
 
 namespace {
@@ -284,9 +299,26 @@ int upload_db(lhmm_context* c) {
     return LHMM_OK;
 }
 
+// segments == 0: scan the resident database.  segments > 0: upload the
+// packed host image in `segments` byte-balanced pieces on the copy stream
+// while the compute stream scans each piece as soon as it has landed (one
+// launch per piece) -- the end-to-end path with H2D overlapped.
+// A device-resident tile set to scan: the context's database, or a derived
+// one (the pipeline's compacted survivors).
+struct DbView {
+    const uint8_t* db;
+    const uint64_t* tile_off;
+    const uint32_t* lens;
+    const uint32_t* out_idx;
+    uint64_t n_tiles, residues, sequences;
+};
+
 int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8_t* d_pass,
-            lhmm_scan_stats* st) {
+            lhmm_scan_stats* st, int segments = 0, const DbView* view = nullptr) {
     if (!c || !opt) return set_error(LHMM_ERR_CONTRACT, "null argument");
+    const DbView v = view ? *view
+                          : DbView{c->d_db.ptr, c->d_tile_off.ptr, c->d_lens.ptr, c->d_out_idx.ptr,
+                                   c->db.n_tiles, c->db.residues, c->db.n_local};
     if (c->current < 0) return set_error(LHMM_ERR_CONTRACT, "no profile set");
     if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
     if (opt->alg != LHMM_MSV && opt->alg != LHMM_SSV)
@@ -299,7 +331,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (L != 0 && (L > 32 || (L & (L - 1))))
         return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,32]");
     if (H == 0) {
-        Choice ch = choose_geometry(pf.m, opt->alg, variant, L, c->db.n_tiles, c->sm_count);
+        Choice ch = choose_geometry(pf.m, opt->alg, variant, L, v.n_tiles, c->sm_count);
         if (!ch.L)
             return set_error(LHMM_ERR_DATA,
                              "no instantiated geometry covers model length " + std::to_string(pf.m));
@@ -309,7 +341,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     } else {
         if (variant == LHMM_VARIANT_AUTO) variant = LHMM_VARIANT_FP16;
         if (L == 0) {
-            Choice ch = choose_geometry(pf.m, opt->alg, variant, 0, c->db.n_tiles, c->sm_count);
+            Choice ch = choose_geometry(pf.m, opt->alg, variant, 0, v.n_tiles, c->sm_count);
             L = ch.L ? ch.L : 1;
         }
     }
@@ -375,17 +407,17 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (int rc = c->d_counter.reserve(1)) return rc;
 
     lhmm::KParams p{};
-    p.db = c->d_db.ptr;
-    p.tile_off = c->d_tile_off.ptr;
-    p.lens = c->d_lens.ptr;
-    p.out_idx = c->d_out_idx.ptr;
+    p.db = v.db;
+    p.tile_off = v.tile_off;
+    p.lens = v.lens;
+    p.out_idx = v.out_idx;
     p.base_tab = lit->second.base.ptr;
     p.rawmin_tab = lit->second.rawmin.ptr;
     p.table = tab.buf.ptr;
     p.raw_out = d_raw;
     p.pass_out = d_pass;
     p.counter = c->d_counter.ptr;
-    p.n_items = uint32_t(c->db.n_tiles * L);
+    p.n_items = uint32_t(v.n_tiles * L);
     p.table_bytes = uint32_t(table_bytes);
     p.res_stride = tab.res_stride;
     p.copy_stride = tab.copy_stride;
@@ -411,14 +443,66 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     const uint64_t need = (uint64_t(p.n_items) + warps_per_cta - 1) / warps_per_cta;
     cfg.grid = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(c->sm_count) * bps, need)));
 
-    CUDA_TRY(cudaMemsetAsync(c->d_counter.ptr, 0, sizeof(uint32_t), c->stream));
-    CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
     uint32_t launches = 0;
-    if (p.n_items > 0) {
-        if (fn(lhmm::kOpLaunch, int(H), &cfg, &p) != 0)
-            return set_error(LHMM_ERR_CUDA, std::string("kernel launch failed: ") +
-                                                cudaGetErrorString(cudaGetLastError()));
-        launches = 1;
+    if (segments <= 0) {
+        CUDA_TRY(cudaMemsetAsync(c->d_counter.ptr, 0, sizeof(uint32_t), c->stream));
+        CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+        if (p.n_items > 0) {
+            if (fn(lhmm::kOpLaunch, int(H), &cfg, &p) != 0)
+                return set_error(LHMM_ERR_CUDA, std::string("kernel launch failed: ") +
+                                                    cudaGetErrorString(cudaGetLastError()));
+            launches = 1;
+        }
+    } else {
+        if (view) return set_error(LHMM_ERR_CONTRACT, "streamed scans need the resident database");
+        auto& db = c->db;
+        const uint64_t T = db.n_tiles;
+        if (int rc = c->d_db.reserve(db.data_bytes)) return rc;
+        if (c->seg_events.size() < size_t(segments)) {
+            for (auto e : c->seg_events) cudaEventDestroy(e);
+            c->seg_events.assign(size_t(segments), nullptr);
+            for (auto& e : c->seg_events)
+                CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+        CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev0, 0));
+        // per-tile side arrays first (small), then the residue bytes piecewise
+        CUDA_TRY(cudaMemcpyAsync(c->d_tile_off.ptr, db.tile_off.data(), T * sizeof(uint64_t),
+                                 cudaMemcpyHostToDevice, c->copy_stream));
+        CUDA_TRY(cudaMemcpyAsync(c->d_lens.ptr, db.lens.data(), db.lens.size() * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, c->copy_stream));
+        CUDA_TRY(cudaMemcpyAsync(c->d_out_idx.ptr, db.out_idx.data(),
+                                 db.out_idx.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                 c->copy_stream));
+        uint64_t t0 = 0;
+        for (int k = 0; k < segments && t0 < T; ++k) {
+            // byte-balanced boundary: first tile whose offset reaches the k+1-th share
+            const uint64_t goal = db.data_bytes * uint64_t(k + 1) / uint64_t(segments);
+            uint64_t t1 = k + 1 == segments ? T
+                                            : uint64_t(std::lower_bound(db.tile_off.begin(),
+                                                                        db.tile_off.end(), goal) -
+                                                       db.tile_off.begin());
+            t1 = std::max(t1, t0 + 1);
+            const uint64_t b0 = db.tile_off[t0];
+            const uint64_t b1 = t1 < T ? db.tile_off[t1] : db.data_bytes;
+            CUDA_TRY(cudaMemcpyAsync(c->d_db.ptr + b0, db.data + b0, b1 - b0,
+                                     cudaMemcpyHostToDevice, c->copy_stream));
+            CUDA_TRY(cudaEventRecord(c->seg_events[size_t(k)], c->copy_stream));
+            CUDA_TRY(cudaStreamWaitEvent(c->stream, c->seg_events[size_t(k)], 0));
+            lhmm::KParams ps = p;
+            ps.tile_base = uint32_t(t0);
+            ps.n_items = uint32_t((t1 - t0) * L);
+            lhmm::LaunchCfg cs = cfg;
+            const uint64_t need_s = (uint64_t(ps.n_items) + warps_per_cta - 1) / warps_per_cta;
+            cs.grid = int(std::max<uint64_t>(
+                1, std::min<uint64_t>(uint64_t(c->sm_count) * bps, need_s)));
+            CUDA_TRY(cudaMemsetAsync(c->d_counter.ptr, 0, sizeof(uint32_t), c->stream));
+            if (fn(lhmm::kOpLaunch, int(H), &cs, &ps) != 0)
+                return set_error(LHMM_ERR_CUDA, std::string("kernel launch failed: ") +
+                                                    cudaGetErrorString(cudaGetLastError()));
+            ++launches;
+            t0 = t1;
+        }
     }
     CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
     CUDA_TRY(cudaEventSynchronize(c->ev1));
@@ -427,9 +511,9 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (st) {
         std::memset(st, 0, sizeof(*st));
         st->device_ms = ms;
-        st->sequences = c->db.n_local;
-        st->residues = c->db.residues;
-        st->cells = c->db.residues * uint64_t(pf.m);
+        st->sequences = v.sequences;
+        st->residues = v.residues;
+        st->cells = v.residues * uint64_t(pf.m);
         st->gcups = ms > 0 ? double(st->cells) / (ms * 1e-3) / 1e9 : 0.0;
         st->lanes = L;
         st->rows = H;
@@ -438,6 +522,149 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         st->grid = uint32_t(cfg.grid);
         st->threads = uint32_t(cfg.threads);
         st->smem_bytes = uint32_t(table_bytes);
+    }
+    return LHMM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// on-device filter pipeline (filter_pipeline, src/engine.cpp:596-657):
+// SSV over the resident database -> stream-compact the survivors (pass bit:
+// pValue <= t || overflow) into new length-binned tiles -> MSV over them.
+
+__global__ void pipe_flags(const uint32_t* __restrict__ out_idx, const uint8_t* __restrict__ pass,
+                           uint32_t nslots, uint32_t* __restrict__ flags) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nslots) return;
+    const uint32_t o = out_idx[i];
+    flags[i] = (o != lhmm::kNoOutput && pass[o]) ? 1u : 0u;
+}
+
+// Survivors keep their sorted (length-descending) order, so the new tiles
+// are length-binned too.
+__global__ void pipe_meta(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ pos,
+                          const uint32_t* __restrict__ lens, const uint32_t* __restrict__ out_idx,
+                          uint32_t nslots, uint32_t* __restrict__ new_lens,
+                          uint32_t* __restrict__ new_out, uint32_t* __restrict__ src_slot) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nslots || !flags[i]) return;
+    const uint32_t j = pos[i];
+    new_lens[j] = lens[i];
+    new_out[j] = out_idx[i];
+    src_slot[j] = i;
+}
+
+__global__ void pipe_tile_bytes(const uint32_t* __restrict__ new_lens, uint32_t ntiles,
+                                uint64_t* __restrict__ bytes) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    bytes[t] = uint64_t((new_lens[t * 32u] + 15u) / 16u) * 512u;
+}
+
+// one warp per survivor: copy its 16-byte residue chunks between layouts
+__global__ void pipe_gather(const uint8_t* __restrict__ old_db, const uint64_t* __restrict__ old_off,
+                            const uint32_t* __restrict__ src_slot,
+                            const uint32_t* __restrict__ new_lens,
+                            const uint64_t* __restrict__ new_off, uint32_t nsurv,
+                            uint8_t* __restrict__ new_db) {
+    const uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) / 32u;
+    const uint32_t lane = threadIdx.x & 31u;
+    if (j >= nsurv) return;
+    const uint32_t s = src_slot[j];
+    const uint32_t nch = (new_lens[j] + 15u) / 16u;
+    const uint8_t* src = old_db + old_off[s / 32u] + (s % 32u) * 16u;
+    uint8_t* dst = new_db + new_off[j / 32u] + (j % 32u) * 16u;
+    for (uint32_t c = lane; c < nch; c += 32u)
+        *reinterpret_cast<uint4*>(dst + c * 512u) = *reinterpret_cast<const uint4*>(src + c * 512u);
+}
+
+int run_pipeline(lhmm_context* c, double threshold, int variant, uint8_t* ssv_raw, uint8_t* pass,
+                 uint8_t* msv_raw, uint64_t* rescored, lhmm_scan_stats* sst,
+                 lhmm_scan_stats* mst) {
+    if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
+    if (c->current < 0) return set_error(LHMM_ERR_CONTRACT, "no profile set");
+    if (threshold < 0.0 || threshold > 1.0)
+        return set_error(LHMM_ERR_CONTRACT, "pipeline threshold must lie in [0,1]");
+    auto& db = c->db;
+    const uint64_t n = db.n_local;
+    lhmm_scan_options o{};
+    o.alg = LHMM_SSV;
+    o.variant = variant;
+    o.threshold = threshold;
+    if (int rc = do_scan(c, &o, c->d_raw.ptr, c->d_pass.ptr, sst)) return rc;
+
+    const uint32_t nslots = uint32_t(db.n_tiles * 32);
+    auto& P = c->pipe;
+    if (int rc = P.flags.reserve(nslots)) return rc;
+    if (int rc = P.pos.reserve(nslots)) return rc;
+    if (int rc = P.new_lens.reserve(nslots)) return rc;
+    if (int rc = P.new_out.reserve(nslots)) return rc;
+    if (int rc = P.src_slot.reserve(nslots)) return rc;
+    if (int rc = P.msv.reserve(std::max<uint64_t>(n, 1))) return rc;
+    if (int rc = P.msv_pass.reserve(std::max<uint64_t>(n, 1))) return rc;
+    cudaStream_t s = c->stream;
+    const int TB = 256;
+    pipe_flags<<<(nslots + TB - 1) / TB, TB, 0, s>>>(c->d_out_idx.ptr, c->d_pass.ptr, nslots,
+                                                     P.flags.ptr);
+    size_t tmp = 0;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, P.flags.ptr, P.pos.ptr, nslots, s));
+    if (int rc = P.temp.reserve(tmp + 16)) return rc;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(P.temp.ptr, tmp, P.flags.ptr, P.pos.ptr, nslots, s));
+    uint32_t last_pos = 0, last_flag = 0;
+    CUDA_TRY(cudaMemcpyAsync(&last_pos, P.pos.ptr + nslots - 1, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&last_flag, P.flags.ptr + nslots - 1, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const uint32_t nsurv = last_pos + last_flag;
+    *rescored = nsurv;
+    CUDA_TRY(cudaMemsetAsync(P.msv.ptr, 0, std::max<uint64_t>(n, 1), s));
+    if (mst) std::memset(mst, 0, sizeof(*mst));
+    if (nsurv > 0) {
+        const uint32_t ntiles = (nsurv + 31u) / 32u;
+        CUDA_TRY(cudaMemsetAsync(P.new_lens.ptr, 0, size_t(ntiles) * 32 * 4, s));
+        CUDA_TRY(cudaMemsetAsync(P.new_out.ptr, 0xff, size_t(ntiles) * 32 * 4, s));
+        pipe_meta<<<(nslots + TB - 1) / TB, TB, 0, s>>>(P.flags.ptr, P.pos.ptr, c->d_lens.ptr,
+                                                        c->d_out_idx.ptr, nslots, P.new_lens.ptr,
+                                                        P.new_out.ptr, P.src_slot.ptr);
+        if (int rc = P.tile_bytes.reserve(ntiles + 1)) return rc;
+        if (int rc = P.new_off.reserve(ntiles + 1)) return rc;
+        CUDA_TRY(cudaMemsetAsync(P.tile_bytes.ptr + ntiles, 0, 8, s));
+        pipe_tile_bytes<<<(ntiles + TB - 1) / TB, TB, 0, s>>>(P.new_lens.ptr, ntiles,
+                                                              P.tile_bytes.ptr);
+        size_t tmp2 = 0;
+        CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, P.tile_bytes.ptr, P.new_off.ptr,
+                                               ntiles + 1, s));
+        if (int rc = P.temp.reserve(std::max(tmp, tmp2) + 16)) return rc;
+        CUDA_TRY(cub::DeviceScan::ExclusiveSum(P.temp.ptr, tmp2, P.tile_bytes.ptr, P.new_off.ptr,
+                                               ntiles + 1, s));
+        uint64_t total = 0;
+        CUDA_TRY(cudaMemcpyAsync(&total, P.new_off.ptr + ntiles, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (int rc = P.db.reserve(std::max<uint64_t>(total, 16))) return rc;
+        CUDA_TRY(cudaMemsetAsync(P.db.ptr, lhmm::kPadding, std::max<uint64_t>(total, 16), s));
+        const uint64_t threads = uint64_t(nsurv) * 32;
+        pipe_gather<<<uint32_t((threads + TB - 1) / TB), TB, 0, s>>>(
+            c->d_db.ptr, c->d_tile_off.ptr, P.src_slot.ptr, P.new_lens.ptr, P.new_off.ptr, nsurv,
+            P.db.ptr);
+        CUDA_TRY(cudaPeekAtLastError());
+        // survivor residue count for the report (host side, from lengths)
+        uint64_t surv_res = 0;
+        {
+            std::vector<uint32_t> h(size_t(ntiles) * 32);
+            CUDA_TRY(cudaMemcpyAsync(h.data(), P.new_lens.ptr, h.size() * 4,
+                                     cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            for (uint32_t v : h) surv_res += v;
+        }
+        DbView view{P.db.ptr, P.new_off.ptr, P.new_lens.ptr, P.new_out.ptr, ntiles, surv_res,
+                    nsurv};
+        lhmm_scan_options om = o;
+        om.alg = LHMM_MSV;
+        if (int rc = do_scan(c, &om, P.msv.ptr, P.msv_pass.ptr, mst, 0, &view)) return rc;
+    }
+    if (n) {
+        CUDA_TRY(cudaMemcpyAsync(ssv_raw, c->d_raw.ptr, n, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(pass, c->d_pass.ptr, n, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(msv_raw, P.msv.ptr, n, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
     }
     return LHMM_OK;
 }
@@ -478,6 +705,7 @@ int lhmm_context_create(int device, lhmm_context** out) {
                                             std::to_string(prop.major) + std::to_string(prop.minor));
     }
     if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
         delete c;
         return set_error(LHMM_ERR_CUDA, "stream/event creation failed");
@@ -499,11 +727,14 @@ int lhmm_context_destroy(lhmm_context* c) {
     c->d_lens.release();
     c->d_out_idx.release();
     for (auto& pf : c->profiles) pf.release();
+    c->pipe.release();
     c->d_counter.release();
     c->d_raw.release();
     c->d_pass.release();
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);
+    for (auto e : c->seg_events) cudaEventDestroy(e);
+    cudaStreamDestroy(c->copy_stream);
     cudaStreamDestroy(c->own_stream);
     delete c;
     return LHMM_OK;
@@ -649,9 +880,32 @@ int lhmm_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* raw, uint8
     return LHMM_OK;
 }
 
-int lhmm_filter_pipeline(lhmm_context*, double, int, uint8_t*, uint8_t*, uint8_t*, uint64_t*,
-                         lhmm_scan_stats*, lhmm_scan_stats*) {
-    return set_error(LHMM_ERR_CONTRACT, "filter_pipeline: not built yet");
+int lhmm_scan_streamed(lhmm_context* c, const lhmm_scan_options* opt, int segments,
+                       uint8_t* raw, uint8_t* pass, lhmm_scan_stats* st) {
+    if (!c) return set_error(LHMM_ERR_CONTRACT, "null context");
+    if (!raw || !pass) return set_error(LHMM_ERR_CONTRACT, "null output");
+    if (segments < 1 || segments > 64)
+        return set_error(LHMM_ERR_CONTRACT, "segments must lie in [1,64]");
+    DeviceGuard g(c->device);
+    if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
+    if (int rc = do_scan(c, opt, c->d_raw.ptr, c->d_pass.ptr, st, segments)) return rc;
+    const uint64_t n = c->db.n_local;
+    if (n) {
+        CUDA_TRY(cudaMemcpyAsync(raw, c->d_raw.ptr, n, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaMemcpyAsync(pass, c->d_pass.ptr, n, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+    }
+    return LHMM_OK;
+}
+
+int lhmm_filter_pipeline(lhmm_context* c, double threshold, int variant, uint8_t* ssv_raw,
+                         uint8_t* pass_out, uint8_t* msv_raw, uint64_t* rescored,
+                         lhmm_scan_stats* ssv_stats, lhmm_scan_stats* msv_stats) {
+    if (!c || !ssv_raw || !pass_out || !msv_raw || !rescored)
+        return set_error(LHMM_ERR_CONTRACT, "null argument");
+    DeviceGuard g(c->device);
+    return run_pipeline(c, threshold, variant, ssv_raw, pass_out, msv_raw, rescored, ssv_stats,
+                        msv_stats);
 }
 
 }  // extern "C"

@@ -57,6 +57,7 @@ struct KParams {
     uint8_t* pass_out;
     uint32_t* counter;          // work-item counter (zeroed per launch)
     uint32_t n_items;           // tiles * L
+    uint32_t tile_base;         // first tile of this launch (streamed scans)
     uint32_t table_bytes;       // multiple of 16
     uint32_t res_stride;        // words per residue row (P)
     uint32_t copy_stride;       // words between per-group replicas (0: shared)
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
         if (lane == 0) item = atomicAdd(p.counter, 1u);
         item = __shfl_sync(kFull, item, 0);
         if (item >= p.n_items) break;
-        const uint32_t tile = item / L;
+        const uint32_t tile = p.tile_base + item / L;
         const uint32_t sub = item % L;
         const uint32_t slot = sub * G + grp;
         const uint32_t sidx = tile * 32u + slot;

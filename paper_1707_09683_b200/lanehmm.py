@@ -188,6 +188,22 @@ class ScanReport:
     stats: dict = field(default_factory=dict)
 
 
+@dataclass
+class PipelineReport:
+    """engine.hpp:118-126: SSV stage over everything, MSV over the survivors."""
+    threshold: float
+    ssv_scanned: int
+    msv_rescored: int
+    ssv_seconds: float
+    msv_seconds: float
+    survivors: np.ndarray   # local indices with pValue <= t or SSV overflow
+    ssv_raw: np.ndarray     # all sequences
+    passed: np.ndarray
+    msv_raw: np.ndarray     # survivors' MSV bytes, 0 elsewhere
+    ssv_stats: dict = field(default_factory=dict)
+    msv_stats: dict = field(default_factory=dict)
+
+
 # ---------------------------------------------------------------------------
 # byte-space helpers (host, bit-identical to the reference)
 
@@ -328,6 +344,40 @@ class Scanner:
                           st.device_ms * 1e-3, st.gcups, raw[:n], passed[:n].astype(bool),
                           st.as_dict())
 
+    def scan_streamed(self, opt: ScanOptions, segments=8):
+        """End-to-end scan from the packed host image with the H2D copy
+        overlapped with the kernels (lhmm_scan_streamed)."""
+        raw = np.zeros(max(self.n_local, 1), dtype=np.uint8)
+        passed = np.zeros(max(self.n_local, 1), dtype=np.uint8)
+        st = _native.ScanStatsC()
+        oc = opt.c()
+        _check(_native.lib().lhmm_scan_streamed(self._ctx, C.byref(oc), segments,
+                                                raw.ctypes.data_as(_native.u8p),
+                                                passed.ctypes.data_as(_native.u8p), C.byref(st)))
+        n = self.n_local
+        return ScanReport(opt.alg, st.lanes, st.rows, st.variant, st.sequences, st.residues,
+                          st.device_ms * 1e-3, st.gcups, raw[:n], passed[:n].astype(bool),
+                          st.as_dict())
+
+    def filter_pipeline(self, threshold, variant=Variant.Auto):
+        """SSV over the resident database, survivors (pValue <= t or overflow)
+        compacted on the device, MSV over the survivors (lhmm_filter_pipeline).
+        Returns a PipelineReport."""
+        n = max(self.n_local, 1)
+        ssv = np.zeros(n, np.uint8)
+        passed = np.zeros(n, np.uint8)
+        msv = np.zeros(n, np.uint8)
+        resc = C.c_uint64()
+        s1, s2 = _native.ScanStatsC(), _native.ScanStatsC()
+        _check(_native.lib().lhmm_filter_pipeline(
+            self._ctx, float(threshold), int(variant), ssv.ctypes.data_as(_native.u8p),
+            passed.ctypes.data_as(_native.u8p), msv.ctypes.data_as(_native.u8p), C.byref(resc),
+            C.byref(s1), C.byref(s2)))
+        k = self.n_local
+        return PipelineReport(float(threshold), k, resc.value, s1.device_ms * 1e-3,
+                              s2.device_ms * 1e-3, np.flatnonzero(passed[:k]), ssv[:k],
+                              passed[:k].astype(bool), msv[:k], s1.as_dict(), s2.as_dict())
+
     def scan_device(self, opt: ScanOptions, raw_ptr: int, pass_ptr: int):
         """Outputs stay on the device (e.g. torch.uint8 tensors' data_ptr())."""
         st = _native.ScanStatsC()
@@ -357,6 +407,19 @@ def scan_database(hmm: ProfileHMM, costs: CostMatrix, db: SequenceDB, q: QuantPa
         s.set_profile(costs, q, hmm.lambda_, hmm.tau)
         s.set_database(db)
         return s.scan(opt)
+
+
+def filter_pipeline(hmm: ProfileHMM, costs: CostMatrix, db: SequenceDB, threshold: float,
+                    q: QuantParams, opt: ScanOptions = None, device=0) -> PipelineReport:
+    """engine.hpp:130-132 -- SSV over `db`, then MSV rescoring of every
+    sequence with pValue <= threshold or SSV overflow, on the device."""
+    if threshold < 0.0 or threshold > 1.0:
+        raise ContractError("pipeline threshold must lie in [0,1]")
+    variant = opt.variant if opt is not None else Variant.Auto
+    with Scanner(device) as s:
+        s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        s.set_database(db)
+        return s.filter_pipeline(threshold, variant)
 
 
 def scan_sequences_s1(hmm, costs, db, q, opt, device=0) -> ScanReport:

@@ -11,9 +11,11 @@ from __future__ import annotations
 import numpy as np
 
 
-def gather_to_rank0(dist, raw, passed, gidx, n_total, device=None):
+def gather_to_rank0(dist, raw, passed, gidx, n_total, device=None, as_numpy=True,
+                    validate=True):
     """Gather each rank's (raw, pass) bytes for its global indices `gidx`
-    into full-length arrays on rank 0 (None elsewhere).
+    into full-length arrays on rank 0 (None elsewhere); as_numpy=False keeps
+    them as tensors on the gather device.
 
     raw / passed: uint8 tensors of the shard's local outputs (local order);
     gidx: int64 tensor of the matching global indices.  Shards are padded to
@@ -37,18 +39,17 @@ def gather_to_rank0(dist, raw, passed, gidx, n_total, device=None):
     dist.gather(buf, glist, dst=0)
     if rank != 0:
         return None, None
-    out_raw = np.zeros(n_total, dtype=np.uint8)
-    out_pass = np.zeros(n_total, dtype=bool)
-    seen = np.zeros(n_total, dtype=np.int32)
-    for r, g in enumerate(glist):
-        c = int(counts[r])
-        idx = g[0, :c].cpu().numpy()
-        val = g[1, :c].cpu().numpy()
-        out_raw[idx] = (val & 0xFF).astype(np.uint8)
-        out_pass[idx] = ((val >> 8) & 1).astype(bool)
-        seen[idx] += 1
-    if not (seen == 1).all():
+    # scatter into the global arrays where the data lives (device for NCCL)
+    allg = torch.cat([g[:, :int(counts[r])] for r, g in enumerate(glist)], dim=1)
+    idx, val = allg[0], allg[1]
+    if validate and (idx.numel() != n_total or int(torch.unique(idx).numel()) != n_total):
         raise RuntimeError("shards do not partition the database")
+    out_raw = torch.zeros(n_total, dtype=torch.uint8, device=dev)
+    out_pass = torch.zeros(n_total, dtype=torch.bool, device=dev)
+    out_raw[idx] = (val & 0xFF).to(torch.uint8)
+    out_pass[idx] = ((val >> 8) & 1).to(torch.bool)
+    if as_numpy:
+        return out_raw.cpu().numpy(), out_pass.cpu().numpy()
     return out_raw, out_pass
 
 

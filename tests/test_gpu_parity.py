@@ -190,3 +190,64 @@ def test_multiple_resident_profiles(ora):
             rep = s.scan(P.ScanOptions(alg=P.Algorithm.Ssv))
             want = ora.scan_flat(1, c.bytes, db.residues, db.offsets, oq(q))
             np.testing.assert_array_equal(rep.raw, want)
+
+
+def test_streamed_scan_matches_resident_scan(ora):
+    """lhmm_scan_streamed (H2D in pieces overlapped with per-piece launches)
+    returns exactly the resident scan's scores and pass bits."""
+    rng = P.Rng(21)
+    hmm = rng.random_profile(333)
+    db = rng.lognormal_records(20000, 290, 0.65, 2)
+    q = P.QuantParams(3.0, 120, 3, 20, 20)
+    costs = P.quantize_emissions(hmm, q)
+    want = ora.scan_flat(0, costs.bytes, db.residues, db.offsets, oq(q))
+    with P.Scanner(0) as s:
+        s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        s.set_database(db)
+        for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
+            base = s.scan(P.ScanOptions(alg=alg, threshold=0.3))
+            for seg in (1, 3, 8, 64):
+                st = s.scan_streamed(P.ScanOptions(alg=alg, threshold=0.3), seg)
+                np.testing.assert_array_equal(st.raw, base.raw)
+                np.testing.assert_array_equal(st.passed, base.passed)
+                assert 1 <= st.stats["launches"] <= seg
+        np.testing.assert_array_equal(s.scan(P.ScanOptions(alg=P.Algorithm.Msv)).raw, want)
+
+
+@pytest.mark.parametrize("threshold", [0.0, 0.022, 0.3, 1.0])
+def test_device_filter_pipeline_matches_oracle(ora, threshold):
+    """filter_pipeline semantics (test_engine.cpp:406-450, acceptance
+    criterion 6): survivors are exactly {pValue <= t or overflow} of the SSV
+    stage, and each survivor's MSV byte equals the scalar oracle's."""
+    rng = P.Rng(0x5175)
+    hmm = rng.random_profile(80)
+    db = rng.random_records(3000, 20, 250, plant=(hmm, 0.2))
+    q = P.QuantParams()
+    costs = P.quantize_emissions(hmm, q)
+    rep = P.filter_pipeline(hmm, costs, db, threshold, q)
+    ssv = ora.scan_flat(1, costs.bytes, db.residues, db.offsets, oq(q))
+    msv = ora.scan_flat(0, costs.bytes, db.residues, db.offsets, oq(q))
+    lens = np.diff(db.offsets)
+    expect = np.array([ora.passes(int(r), int(n), hmm.lambda_, hmm.tau, oq(q), 1, threshold)
+                       for r, n in zip(ssv, lens)])
+    np.testing.assert_array_equal(rep.ssv_raw, ssv)
+    np.testing.assert_array_equal(rep.passed, expect)
+    assert rep.msv_rescored == int(expect.sum()) == rep.survivors.size
+    np.testing.assert_array_equal(rep.msv_raw[expect], msv[expect])
+    assert (rep.msv_raw[~expect] == 0).all()
+
+
+def test_device_pipeline_matches_reference_library(ref):
+    """Against the unmodified reference filter_pipeline (oracle/_ref)."""
+    rng = P.Rng(42)
+    hmm = rng.random_profile(48)
+    db = rng.random_records(400, 30, 200, plant=(hmm, 0.15))
+    q = P.QuantParams()
+    costs = P.quantize_emissions(hmm, q)
+    for t in (0.0, 0.02, 0.2, 1.0):
+        ssv, msv, surv = ref.filter_pipeline(hmm.match_scores.reshape(-1), hmm.lambda_, hmm.tau,
+                                             costs.bytes, oq(q), db.residues, db.offsets, t)
+        rep = P.filter_pipeline(hmm, costs, db, t, q)
+        np.testing.assert_array_equal(rep.ssv_raw, ssv)
+        np.testing.assert_array_equal(rep.passed, surv)
+        np.testing.assert_array_equal(rep.msv_raw, msv)
