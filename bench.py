@@ -222,7 +222,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--variant", default="auto", choices=["auto", "dpx16", "fp16", "swar8"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "dpx16", "fp16", "swar8", "fp16x"])
     ap.add_argument("--nseq", type=int, default=0, help="override sequences per GPU")
     ap.add_argument("--ref-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -265,7 +265,7 @@ def main():
             comm_dev = torch.device("cpu")
     desc, wl_alg, models_m, nseq, gen = WORKLOADS[args.workload]
     variant = {"auto": P.Variant.Auto, "dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16,
-               "swar8": P.Variant.Swar8}[args.variant]
+               "swar8": P.Variant.Swar8, "fp16x": P.Variant.Fp16x}[args.variant]
     q = P.QuantParams()
     algs = algs_of(wl_alg)
     threshold = 0.022
@@ -304,7 +304,8 @@ def main():
             s.select_profile(pid)
             st = s.scan_device(opt_for(a), outs[k][0].data_ptr(), outs[k][1].data_ptr())
             launches += st["launches"]
-            geo[k] = (st["lanes"], st["rows"], st["variant"], st["grid"], st["smem_bytes"])
+            geo[k] = (st["lanes"], st["rows"], st["variant"], st["grid"], st["smem_bytes"],
+                      st["recomputed"])
             if record:
                 per_launch[k].append(st["device_ms"])
         return launches
@@ -422,11 +423,11 @@ def main():
     per_scan = []
     for k, (pid, m, a) in enumerate(scans):
         t = statistics.mean(per_launch[k])
-        L, H, v, grid, smem = geo[k]
+        L, H, v, grid, smem, recomputed = geo[k]
         per_scan.append({"alg": a, "M": m, "ms": round(t, 4),
                          "gcups": round(dbstats["residues"] * m / (t * 1e-3) / 1e9, 1),
-                         "lanes": L, "rows": H, "variant": ["auto", "dpx16", "fp16", "swar8"][v],
-                         "grid": grid, "smem_bytes": smem})
+                         "lanes": L, "rows": H, "variant": ["auto", "dpx16", "fp16", "swar8", "fp16x"][v],
+                         "grid": grid, "smem_bytes": smem, "rescored_exactly": recomputed})
     line = {
         "metric": "MSV/SSV GCUPS (device-timed) vs model length",
         "value": round(gcups, 2), "unit": "GCUPS", "n_gpus": world, "steps": args.steps,

@@ -57,7 +57,9 @@ enum lhmm_variant {
     LHMM_VARIANT_AUTO = 0,  /* per (alg, M) choice from measurement */
     LHMM_VARIANT_DPX16 = 1, /* u16x2 lanes, native VIADDMNMX/VIMNMX (ALU pipe) */
     LHMM_VARIANT_FP16 = 2,  /* f16x2 saturating adds on the FMA pipe */
-    LHMM_VARIANT_SWAR8 = 3  /* u8x4 __vaddus4/__vsubus4/__vmaxu4 (paper tier 5) */
+    LHMM_VARIANT_SWAR8 = 3, /* u8x4 __vaddus4/__vsubus4/__vmaxu4 (paper tier 5) */
+    LHMM_VARIANT_FP16X = 4  /* relaxed f16 (SSV without the 255 cap, MSV with lazy B);
+                               flagged sequences are rescored by the exact FP16 kernel */
 };
 
 /* Byte-space constants; mirror of lanehmm::QuantParams
@@ -92,7 +94,7 @@ typedef struct lhmm_scan_stats {
     uint32_t grid;          /* CTAs of the persistent grid */
     uint32_t threads;       /* threads per CTA */
     uint32_t smem_bytes;    /* dynamic shared memory per CTA */
-    uint32_t reserved;
+    uint32_t recomputed;    /* FP16X: sequences rescored by the exact kernel */
 } lhmm_scan_stats;
 
 typedef struct lhmm_context lhmm_context;

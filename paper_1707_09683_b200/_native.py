@@ -32,10 +32,10 @@ class ScanStatsC(C.Structure):
                 ("residues", C.c_uint64), ("cells", C.c_uint64), ("lanes", C.c_uint32),
                 ("rows", C.c_uint32), ("variant", C.c_uint32), ("launches", C.c_uint32),
                 ("grid", C.c_uint32), ("threads", C.c_uint32), ("smem_bytes", C.c_uint32),
-                ("reserved", C.c_uint32)]
+                ("recomputed", C.c_uint32)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 u8p = C.POINTER(C.c_uint8)

@@ -76,6 +76,9 @@ const int* rows_list(int variant, int* n) {
     case LHMM_VARIANT_FP16:
         *n = int(sizeof(lhmm::kRows_fp16) / sizeof(int));
         return lhmm::kRows_fp16;
+    case LHMM_VARIANT_FP16X:
+        *n = int(sizeof(lhmm::kRows_fp16x) / sizeof(int));
+        return lhmm::kRows_fp16x;
     default:
         *n = int(sizeof(lhmm::kRows_swar8) / sizeof(int));
         return lhmm::kRows_swar8;
@@ -118,7 +121,7 @@ double model_rate(int variant, int alg, uint32_t L, uint32_t H) {
     double w;
     if (variant == LHMM_VARIANT_SWAR8)
         w = alg == LHMM_MSV ? 30.0 : 26.0;
-    else if (variant == LHMM_VARIANT_FP16)
+    else if (variant == LHMM_VARIANT_FP16 || variant == LHMM_VARIANT_FP16X)
         w = alg == LHMM_MSV ? 4.5 : 3.0;
     else
         w = alg == LHMM_MSV ? 4.5 : 3.5;
@@ -145,33 +148,45 @@ struct Choice {
 Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64_t n_tiles,
                        int sm_count) {
     Choice best;
-    const int vs[2] = {LHMM_VARIANT_FP16, LHMM_VARIANT_DPX16};
-    const int nv = variant == LHMM_VARIANT_AUTO ? 2 : 1;
-    for (int vi = 0; vi < nv; ++vi) {
-        const int v = variant == LHMM_VARIANT_AUTO ? vs[vi] : variant;
-        const uint32_t cpw = lhmm::cells_per_word(v);
-        int n;
-        const int* rows = rows_list(v, &n);
-        for (uint32_t L = 1; L <= 32; L *= 2) {
-            if (want_L && L != want_L) continue;
-            for (int i = 0; i < n; ++i) {
-                const uint32_t H = uint32_t(rows[i]);
-                const uint64_t cap = uint64_t(cpw) * L * H;
-                if (cap < m) continue;
-                if (lhmm::table_bytes_for(v, L, H, true) > kMaxTableBytes) continue;
-                double rate = calib_rate(v, alg, L, H);
-                if (rate < 0) rate = model_rate(v, alg, L, H);
-                double fill = 1.0;
-                if (n_tiles > 0 && sm_count > 0) {
-                    const double slots = double(sm_count) * (lhmm::kMaxThreads / 32);
-                    fill = std::min(1.0, double(n_tiles) * double(L) / slots);
-                }
-                const double pred = rate * double(m) / double(cap) * fill;
-                if (pred > best.predicted * 1.0001) {
-                    best.variant = v;
-                    best.L = L;
-                    best.H = H;
-                    best.predicted = pred;
+    // auto considers the measured variants only (calib_b200.inc); the
+    // relaxed FP16X also needs a database large enough to amortise its
+    // rescoring check.  Without any measurement the cost model decides.
+    const int vs[3] = {LHMM_VARIANT_FP16, LHMM_VARIANT_DPX16, LHMM_VARIANT_FP16X};
+    const int nv = variant == LHMM_VARIANT_AUTO ? 3 : 1;
+    for (int pass = 0; pass < 2 && best.L == 0; ++pass) {
+        const bool measured_only = variant == LHMM_VARIANT_AUTO && pass == 0;
+        for (int vi = 0; vi < nv; ++vi) {
+            const int v = variant == LHMM_VARIANT_AUTO ? vs[vi] : variant;
+            if (variant == LHMM_VARIANT_AUTO && v == LHMM_VARIANT_FP16X && n_tiles > 0 &&
+                n_tiles < 4096)
+                continue;
+            const uint32_t cpw = lhmm::cells_per_word(v);
+            int n;
+            const int* rows = rows_list(v, &n);
+            for (uint32_t L = 1; L <= 32; L *= 2) {
+                if (want_L && L != want_L) continue;
+                for (int i = 0; i < n; ++i) {
+                    const uint32_t H = uint32_t(rows[i]);
+                    const uint64_t cap = uint64_t(cpw) * L * H;
+                    if (cap < m) continue;
+                    if (lhmm::table_bytes_for(v, L, H, true) > kMaxTableBytes) continue;
+                    double rate = calib_rate(v, alg, L, H);
+                    if (rate < 0) {
+                        if (measured_only) continue;
+                        rate = model_rate(v, alg, L, H);
+                    }
+                    double fill = 1.0;
+                    if (n_tiles > 0 && sm_count > 0) {
+                        const double slots = double(sm_count) * (lhmm::kMaxThreads / 32);
+                        fill = std::min(1.0, double(n_tiles) * double(L) / slots);
+                    }
+                    const double pred = rate * double(m) / double(cap) * fill;
+                    if (pred > best.predicted * 1.0001) {
+                        best.variant = v;
+                        best.L = L;
+                        best.H = H;
+                        best.predicted = pred;
+                    }
                 }
             }
         }
@@ -244,6 +259,8 @@ struct lhmm_context {
     DevBuf<uint32_t> d_lens, d_out_idx;
     DevBuf<uint32_t> d_counter;
     DevBuf<uint8_t> d_raw, d_pass;
+    DevBuf<uint8_t> d_flag;        // FP16X: per-sequence "rescore exactly"
+    DevBuf<uint32_t> d_flag_count;
 
     std::map<std::tuple<int, int, uint32_t, uint32_t, size_t>, int> occupancy;
 
@@ -251,13 +268,15 @@ struct lhmm_context {
     struct Pipe {
         DevBuf<uint32_t> flags, pos, new_lens, new_out, src_slot;
         DevBuf<uint64_t> tile_bytes, new_off;
+        DevBuf<uint64_t> res;
         DevBuf<uint8_t> db, msv, msv_pass, temp;
         void release() {
             flags.release(); pos.release(); new_lens.release(); new_out.release();
             src_slot.release(); tile_bytes.release(); new_off.release(); db.release();
-            msv.release(); msv_pass.release(); temp.release();
+            msv.release(); msv_pass.release(); temp.release(); res.release();
         }
-    } pipe;
+    } pipe, resc;   // pipeline survivors / FP16X rescoring
+    cudaEvent_t evr0 = nullptr, evr1 = nullptr;  // FP16X: kernel + rescoring span
 };
 
 namespace {
@@ -313,6 +332,9 @@ struct DbView {
     uint64_t n_tiles, residues, sequences;
 };
 
+int compact(lhmm_context* c, lhmm_context::Pipe& P, const DbView& src, const uint8_t* sel,
+            DbView* out, uint32_t* nsel_out);
+
 int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8_t* d_pass,
             lhmm_scan_stats* st, int segments = 0, const DbView* view = nullptr) {
     if (!c || !opt) return set_error(LHMM_ERR_CONTRACT, "null argument");
@@ -323,7 +345,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
     if (opt->alg != LHMM_MSV && opt->alg != LHMM_SSV)
         return set_error(LHMM_ERR_CONTRACT, "unknown algorithm");
-    if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_SWAR8)
+    if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_FP16X)
         return set_error(LHMM_ERR_CONTRACT, "unknown kernel variant");
     ProfileSlot& pf = c->profiles[c->current];
     int variant = opt->variant;
@@ -363,7 +385,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     auto tit = pf.tables.find(tkey);
     if (tit == pf.tables.end()) {
         lhmm::TableImage img;
-        lhmm::build_table(pf.costs.data(), pf.m, variant, opt->alg, L, H, rep, img);
+        lhmm::build_table(pf.costs.data(), pf.m, variant, opt->alg, L, H, rep, pf.q.dbias, img);
         if (img.words.size() * 4 > kMaxTableBytes + 16 * 1024)
             return set_error(LHMM_ERR_DATA, "profile table does not fit in shared memory");
         ProfileSlot::DevTable t;
@@ -424,6 +446,19 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     p.dbias = pf.q.dbias;
     p.tecjb = uint32_t(pf.q.tec) + uint32_t(pf.q.tjb);
     p.fault = opt->fault_injection ? 1u : 0u;
+    const bool relaxed = variant == LHMM_VARIANT_FP16X;
+    if (relaxed) {
+        if (int rc = c->d_flag.reserve(std::max<uint64_t>(c->db.n_local, 1))) return rc;
+        if (int rc = c->d_flag_count.reserve(1)) return rc;
+        if (!c->evr0) {
+            CUDA_TRY(cudaEventCreate(&c->evr0));
+            CUDA_TRY(cudaEventCreate(&c->evr1));
+        }
+        CUDA_TRY(cudaMemsetAsync(c->d_flag_count.ptr, 0, 4, c->stream));
+        CUDA_TRY(cudaEventRecord(c->evr0, c->stream));
+        p.flag_out = c->d_flag.ptr;
+        p.flag_count = c->d_flag_count.ptr;
+    }
 
     lhmm::LaunchCfg cfg{};
     cfg.threads = lhmm::kMaxThreads;
@@ -508,6 +543,33 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     CUDA_TRY(cudaEventSynchronize(c->ev1));
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    uint32_t recomputed = 0;
+    if (relaxed) {
+        // rescore the flagged sequences with the exact kernel; the reported
+        // time spans the relaxed kernel, the flag check and the rescoring
+        uint32_t nflag = 0;
+        CUDA_TRY(cudaMemcpyAsync(&nflag, c->d_flag_count.ptr, 4, cudaMemcpyDeviceToHost,
+                                 c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        if (nflag) {
+            DbView sub;
+            uint32_t nsel = 0;
+            if (int rc = compact(c, c->resc, v, c->d_flag.ptr, &sub, &nsel)) return rc;
+            if (nsel) {
+                lhmm_scan_options ox = *opt;
+                ox.variant = LHMM_VARIANT_FP16;
+                ox.lanes = 0;
+                ox.rows = 0;
+                lhmm_scan_stats sx;
+                if (int rc = do_scan(c, &ox, d_raw, d_pass, &sx, 0, &sub)) return rc;
+                launches += sx.launches;
+            }
+            recomputed = nsel;
+        }
+        CUDA_TRY(cudaEventRecord(c->evr1, c->stream));
+        CUDA_TRY(cudaEventSynchronize(c->evr1));
+        CUDA_TRY(cudaEventElapsedTime(&ms, c->evr0, c->evr1));
+    }
     if (st) {
         std::memset(st, 0, sizeof(*st));
         st->device_ms = ms;
@@ -522,35 +584,44 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         st->grid = uint32_t(cfg.grid);
         st->threads = uint32_t(cfg.threads);
         st->smem_bytes = uint32_t(table_bytes);
+        st->recomputed = recomputed;
     }
     return LHMM_OK;
 }
 
 // ---------------------------------------------------------------------------
-// on-device filter pipeline (filter_pipeline, src/engine.cpp:596-657):
-// SSV over the resident database -> stream-compact the survivors (pass bit:
-// pValue <= t || overflow) into new length-binned tiles -> MSV over them.
+// device stream compaction of selected sequences into new length-binned
+// tiles (used by the filter pipeline and by FP16X rescoring)
 
-__global__ void pipe_flags(const uint32_t* __restrict__ out_idx, const uint8_t* __restrict__ pass,
+__global__ void pipe_flags(const uint32_t* __restrict__ out_idx, const uint8_t* __restrict__ sel,
                            uint32_t nslots, uint32_t* __restrict__ flags) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nslots) return;
     const uint32_t o = out_idx[i];
-    flags[i] = (o != lhmm::kNoOutput && pass[o]) ? 1u : 0u;
+    flags[i] = (o != lhmm::kNoOutput && sel[o]) ? 1u : 0u;
 }
 
-// Survivors keep their sorted (length-descending) order, so the new tiles
-// are length-binned too.
+// Selected sequences keep their sorted (length-descending) order, so the new
+// tiles are length-binned too.
 __global__ void pipe_meta(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ pos,
                           const uint32_t* __restrict__ lens, const uint32_t* __restrict__ out_idx,
                           uint32_t nslots, uint32_t* __restrict__ new_lens,
-                          uint32_t* __restrict__ new_out, uint32_t* __restrict__ src_slot) {
+                          uint32_t* __restrict__ new_out, uint32_t* __restrict__ src_slot,
+                          unsigned long long* __restrict__ residues) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nslots || !flags[i]) return;
-    const uint32_t j = pos[i];
-    new_lens[j] = lens[i];
-    new_out[j] = out_idx[i];
-    src_slot[j] = i;
+    uint32_t len = 0;
+    if (i < nslots && flags[i]) {
+        const uint32_t j = pos[i];
+        len = lens[i];
+        new_lens[j] = len;
+        new_out[j] = out_idx[i];
+        src_slot[j] = i;
+    }
+    // residue total of the selection (warp sum, one atomic per warp)
+    unsigned long long v = len;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31u) == 0 && v) atomicAdd(residues, v);
 }
 
 __global__ void pipe_tile_bytes(const uint32_t* __restrict__ new_lens, uint32_t ntiles,
@@ -560,15 +631,15 @@ __global__ void pipe_tile_bytes(const uint32_t* __restrict__ new_lens, uint32_t 
     bytes[t] = uint64_t((new_lens[t * 32u] + 15u) / 16u) * 512u;
 }
 
-// one warp per survivor: copy its 16-byte residue chunks between layouts
+// one warp per selected sequence: copy its 16-byte residue chunks
 __global__ void pipe_gather(const uint8_t* __restrict__ old_db, const uint64_t* __restrict__ old_off,
                             const uint32_t* __restrict__ src_slot,
                             const uint32_t* __restrict__ new_lens,
-                            const uint64_t* __restrict__ new_off, uint32_t nsurv,
+                            const uint64_t* __restrict__ new_off, uint32_t nsel,
                             uint8_t* __restrict__ new_db) {
     const uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) / 32u;
     const uint32_t lane = threadIdx.x & 31u;
-    if (j >= nsurv) return;
+    if (j >= nsel) return;
     const uint32_t s = src_slot[j];
     const uint32_t nch = (new_lens[j] + 15u) / 16u;
     const uint8_t* src = old_db + old_off[s / 32u] + (s % 32u) * 16u;
@@ -577,6 +648,70 @@ __global__ void pipe_gather(const uint8_t* __restrict__ old_db, const uint64_t* 
         *reinterpret_cast<uint4*>(dst + c * 512u) = *reinterpret_cast<const uint4*>(src + c * 512u);
 }
 
+// Compacts the sequences of `src` whose byte sel[local index] != 0 into new
+// tiles held in `P`; *out views them (out_idx keeps the local indices).
+int compact(lhmm_context* c, lhmm_context::Pipe& P, const DbView& src, const uint8_t* sel,
+            DbView* out, uint32_t* nsel_out) {
+    const uint32_t nslots = uint32_t(src.n_tiles * 32);
+    *nsel_out = 0;
+    *out = DbView{nullptr, nullptr, nullptr, nullptr, 0, 0, 0};
+    if (nslots == 0) return LHMM_OK;
+    if (int rc = P.flags.reserve(nslots)) return rc;
+    if (int rc = P.pos.reserve(nslots)) return rc;
+    if (int rc = P.new_lens.reserve(nslots)) return rc;
+    if (int rc = P.new_out.reserve(nslots)) return rc;
+    if (int rc = P.src_slot.reserve(nslots)) return rc;
+    if (int rc = P.res.reserve(1)) return rc;
+    cudaStream_t s = c->stream;
+    const int TB = 256;
+    pipe_flags<<<(nslots + TB - 1) / TB, TB, 0, s>>>(src.out_idx, sel, nslots, P.flags.ptr);
+    size_t tmp = 0;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, P.flags.ptr, P.pos.ptr, nslots, s));
+    if (int rc = P.temp.reserve(tmp + 16)) return rc;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(P.temp.ptr, tmp, P.flags.ptr, P.pos.ptr, nslots, s));
+    uint32_t last[2] = {0, 0};
+    CUDA_TRY(cudaMemcpyAsync(&last[0], P.pos.ptr + nslots - 1, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&last[1], P.flags.ptr + nslots - 1, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const uint32_t nsel = last[0] + last[1];
+    *nsel_out = nsel;
+    if (nsel == 0) return LHMM_OK;
+    const uint32_t ntiles = (nsel + 31u) / 32u;
+    CUDA_TRY(cudaMemsetAsync(P.new_lens.ptr, 0, size_t(ntiles) * 32 * 4, s));
+    CUDA_TRY(cudaMemsetAsync(P.new_out.ptr, 0xff, size_t(ntiles) * 32 * 4, s));
+    CUDA_TRY(cudaMemsetAsync(P.res.ptr, 0, 8, s));
+    pipe_meta<<<(nslots + TB - 1) / TB, TB, 0, s>>>(P.flags.ptr, P.pos.ptr, src.lens, src.out_idx,
+                                                    nslots, P.new_lens.ptr, P.new_out.ptr,
+                                                    P.src_slot.ptr,
+                                                    reinterpret_cast<unsigned long long*>(P.res.ptr));
+    if (int rc = P.tile_bytes.reserve(ntiles + 1)) return rc;
+    if (int rc = P.new_off.reserve(ntiles + 1)) return rc;
+    CUDA_TRY(cudaMemsetAsync(P.tile_bytes.ptr + ntiles, 0, 8, s));
+    pipe_tile_bytes<<<(ntiles + TB - 1) / TB, TB, 0, s>>>(P.new_lens.ptr, ntiles, P.tile_bytes.ptr);
+    size_t tmp2 = 0;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, P.tile_bytes.ptr, P.new_off.ptr,
+                                           ntiles + 1, s));
+    if (int rc = P.temp.reserve(std::max(tmp, tmp2) + 16)) return rc;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(P.temp.ptr, tmp2, P.tile_bytes.ptr, P.new_off.ptr,
+                                           ntiles + 1, s));
+    uint64_t total = 0, residues = 0;
+    CUDA_TRY(cudaMemcpyAsync(&total, P.new_off.ptr + ntiles, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&residues, P.res.ptr, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (int rc = P.db.reserve(std::max<uint64_t>(total, 16))) return rc;
+    CUDA_TRY(cudaMemsetAsync(P.db.ptr, lhmm::kPadding, std::max<uint64_t>(total, 16), s));
+    const uint64_t threads = uint64_t(nsel) * 32;
+    pipe_gather<<<uint32_t((threads + TB - 1) / TB), TB, 0, s>>>(
+        src.db, src.tile_off, P.src_slot.ptr, P.new_lens.ptr, P.new_off.ptr, nsel, P.db.ptr);
+    CUDA_TRY(cudaPeekAtLastError());
+    *out = DbView{P.db.ptr, P.new_off.ptr, P.new_lens.ptr, P.new_out.ptr, ntiles, residues, nsel};
+    return LHMM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// on-device filter pipeline (filter_pipeline, src/engine.cpp:596-657):
+// SSV over the resident database -> compact the survivors (pass bit:
+// pValue <= t || overflow) -> MSV over them.
 int run_pipeline(lhmm_context* c, double threshold, int variant, uint8_t* ssv_raw, uint8_t* pass,
                  uint8_t* msv_raw, uint64_t* rescored, lhmm_scan_stats* sst,
                  lhmm_scan_stats* mst) {
@@ -584,78 +719,25 @@ int run_pipeline(lhmm_context* c, double threshold, int variant, uint8_t* ssv_ra
     if (c->current < 0) return set_error(LHMM_ERR_CONTRACT, "no profile set");
     if (threshold < 0.0 || threshold > 1.0)
         return set_error(LHMM_ERR_CONTRACT, "pipeline threshold must lie in [0,1]");
-    auto& db = c->db;
-    const uint64_t n = db.n_local;
+    const uint64_t n = c->db.n_local;
     lhmm_scan_options o{};
     o.alg = LHMM_SSV;
     o.variant = variant;
     o.threshold = threshold;
     if (int rc = do_scan(c, &o, c->d_raw.ptr, c->d_pass.ptr, sst)) return rc;
-
-    const uint32_t nslots = uint32_t(db.n_tiles * 32);
     auto& P = c->pipe;
-    if (int rc = P.flags.reserve(nslots)) return rc;
-    if (int rc = P.pos.reserve(nslots)) return rc;
-    if (int rc = P.new_lens.reserve(nslots)) return rc;
-    if (int rc = P.new_out.reserve(nslots)) return rc;
-    if (int rc = P.src_slot.reserve(nslots)) return rc;
     if (int rc = P.msv.reserve(std::max<uint64_t>(n, 1))) return rc;
     if (int rc = P.msv_pass.reserve(std::max<uint64_t>(n, 1))) return rc;
     cudaStream_t s = c->stream;
-    const int TB = 256;
-    pipe_flags<<<(nslots + TB - 1) / TB, TB, 0, s>>>(c->d_out_idx.ptr, c->d_pass.ptr, nslots,
-                                                     P.flags.ptr);
-    size_t tmp = 0;
-    CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, P.flags.ptr, P.pos.ptr, nslots, s));
-    if (int rc = P.temp.reserve(tmp + 16)) return rc;
-    CUDA_TRY(cub::DeviceScan::ExclusiveSum(P.temp.ptr, tmp, P.flags.ptr, P.pos.ptr, nslots, s));
-    uint32_t last_pos = 0, last_flag = 0;
-    CUDA_TRY(cudaMemcpyAsync(&last_pos, P.pos.ptr + nslots - 1, 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(&last_flag, P.flags.ptr + nslots - 1, 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    const uint32_t nsurv = last_pos + last_flag;
-    *rescored = nsurv;
     CUDA_TRY(cudaMemsetAsync(P.msv.ptr, 0, std::max<uint64_t>(n, 1), s));
     if (mst) std::memset(mst, 0, sizeof(*mst));
+    const DbView all{c->d_db.ptr, c->d_tile_off.ptr, c->d_lens.ptr, c->d_out_idx.ptr,
+                     c->db.n_tiles, c->db.residues, c->db.n_local};
+    DbView view;
+    uint32_t nsurv = 0;
+    if (int rc = compact(c, P, all, c->d_pass.ptr, &view, &nsurv)) return rc;
+    *rescored = nsurv;
     if (nsurv > 0) {
-        const uint32_t ntiles = (nsurv + 31u) / 32u;
-        CUDA_TRY(cudaMemsetAsync(P.new_lens.ptr, 0, size_t(ntiles) * 32 * 4, s));
-        CUDA_TRY(cudaMemsetAsync(P.new_out.ptr, 0xff, size_t(ntiles) * 32 * 4, s));
-        pipe_meta<<<(nslots + TB - 1) / TB, TB, 0, s>>>(P.flags.ptr, P.pos.ptr, c->d_lens.ptr,
-                                                        c->d_out_idx.ptr, nslots, P.new_lens.ptr,
-                                                        P.new_out.ptr, P.src_slot.ptr);
-        if (int rc = P.tile_bytes.reserve(ntiles + 1)) return rc;
-        if (int rc = P.new_off.reserve(ntiles + 1)) return rc;
-        CUDA_TRY(cudaMemsetAsync(P.tile_bytes.ptr + ntiles, 0, 8, s));
-        pipe_tile_bytes<<<(ntiles + TB - 1) / TB, TB, 0, s>>>(P.new_lens.ptr, ntiles,
-                                                              P.tile_bytes.ptr);
-        size_t tmp2 = 0;
-        CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, P.tile_bytes.ptr, P.new_off.ptr,
-                                               ntiles + 1, s));
-        if (int rc = P.temp.reserve(std::max(tmp, tmp2) + 16)) return rc;
-        CUDA_TRY(cub::DeviceScan::ExclusiveSum(P.temp.ptr, tmp2, P.tile_bytes.ptr, P.new_off.ptr,
-                                               ntiles + 1, s));
-        uint64_t total = 0;
-        CUDA_TRY(cudaMemcpyAsync(&total, P.new_off.ptr + ntiles, 8, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
-        if (int rc = P.db.reserve(std::max<uint64_t>(total, 16))) return rc;
-        CUDA_TRY(cudaMemsetAsync(P.db.ptr, lhmm::kPadding, std::max<uint64_t>(total, 16), s));
-        const uint64_t threads = uint64_t(nsurv) * 32;
-        pipe_gather<<<uint32_t((threads + TB - 1) / TB), TB, 0, s>>>(
-            c->d_db.ptr, c->d_tile_off.ptr, P.src_slot.ptr, P.new_lens.ptr, P.new_off.ptr, nsurv,
-            P.db.ptr);
-        CUDA_TRY(cudaPeekAtLastError());
-        // survivor residue count for the report (host side, from lengths)
-        uint64_t surv_res = 0;
-        {
-            std::vector<uint32_t> h(size_t(ntiles) * 32);
-            CUDA_TRY(cudaMemcpyAsync(h.data(), P.new_lens.ptr, h.size() * 4,
-                                     cudaMemcpyDeviceToHost, s));
-            CUDA_TRY(cudaStreamSynchronize(s));
-            for (uint32_t v : h) surv_res += v;
-        }
-        DbView view{P.db.ptr, P.new_off.ptr, P.new_lens.ptr, P.new_out.ptr, ntiles, surv_res,
-                    nsurv};
         lhmm_scan_options om = o;
         om.alg = LHMM_MSV;
         if (int rc = do_scan(c, &om, P.msv.ptr, P.msv_pass.ptr, mst, 0, &view)) return rc;
@@ -728,6 +810,11 @@ int lhmm_context_destroy(lhmm_context* c) {
     c->d_out_idx.release();
     for (auto& pf : c->profiles) pf.release();
     c->pipe.release();
+    c->resc.release();
+    c->d_flag.release();
+    c->d_flag_count.release();
+    if (c->evr0) cudaEventDestroy(c->evr0);
+    if (c->evr1) cudaEventDestroy(c->evr1);
     c->d_counter.release();
     c->d_raw.release();
     c->d_pass.release();
@@ -888,6 +975,9 @@ int lhmm_scan_streamed(lhmm_context* c, const lhmm_scan_options* opt, int segmen
         return set_error(LHMM_ERR_CONTRACT, "segments must lie in [1,64]");
     DeviceGuard g(c->device);
     if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
+    // pieces of at least 16 MB: smaller ones only add launch/sync overhead
+    const uint64_t max_pieces = std::max<uint64_t>(1, c->db.data_bytes >> 24);
+    segments = int(std::min<uint64_t>(uint64_t(segments), max_pieces));
     if (int rc = do_scan(c, opt, c->d_raw.ptr, c->d_pass.ptr, st, segments)) return rc;
     const uint64_t n = c->db.n_local;
     if (n) {

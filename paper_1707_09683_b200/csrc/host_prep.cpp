@@ -294,14 +294,17 @@ static uint16_t half_bits(float f) {
     return u;
 }
 
-static uint32_t encode_word(int variant, int alg, const uint8_t* c, uint32_t cpw) {
+static uint32_t encode_word(int variant, int alg, const uint8_t* c, uint32_t cpw, uint32_t dbias) {
     uint32_t w = 0;
     for (uint32_t k = 0; k < cpw; ++k) {
         uint32_t e;
         if (variant == LHMM_VARIANT_SWAR8) {
             e = c[k];
-        } else if (variant == LHMM_VARIANT_DPX16) {
+        } else if (variant == LHMM_VARIANT_DPX16 ||
+                   (variant == LHMM_VARIANT_FP16X && alg == LHMM_MSV)) {
             e = uint16_t(-int(c[k]));
+        } else if (variant == LHMM_VARIANT_FP16X) {  // SSV: (dbias - cost)/256
+            e = half_bits((float(dbias) - float(c[k])) / 256.f);
         } else {  // FP16: -(cost+1)/256 (MSV) or -(cost+1)/128 (SSV)
             const float den = alg == LHMM_MSV ? 256.f : 128.f;
             e = half_bits(-(float(c[k]) + 1.f) / den);
@@ -312,7 +315,7 @@ static uint32_t encode_word(int variant, int alg, const uint8_t* c, uint32_t cpw
 }
 
 void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_t L, uint32_t H,
-                 bool replicate, TableImage& out) {
+                 bool replicate, uint32_t dbias, TableImage& out) {
     const uint32_t cpw = cells_per_word(variant);
     uint32_t P, copies, cs;
     strides_for(L, H, P, copies, cs);
@@ -327,7 +330,7 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
                     const uint64_t node = uint64_t(cpw * oig + k) * H + h + 1;
                     c[k] = (node > m || x > kUnknown) ? 0xff : costs[(node - 1) * 21 + x];
                 }
-                const uint32_t w = encode_word(variant, alg, c, cpw);
+                const uint32_t w = encode_word(variant, alg, c, cpw, dbias);
                 const size_t at = size_t(x) * P + size_t(h / 4) * 4 * L + 4 * oig + (h % 4);
                 for (uint32_t g = 0; g < copies; ++g) out.words[size_t(g) * cs + at] = w;
             }

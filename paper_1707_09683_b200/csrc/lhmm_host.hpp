@@ -61,7 +61,7 @@ struct TableImage {
 uint32_t cells_per_word(int variant);
 uint64_t table_bytes_for(int variant, uint32_t L, uint32_t H, bool replicate);
 void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_t L, uint32_t H,
-                 bool replicate, TableImage& out);
+                 bool replicate, uint32_t dbias, TableImage& out);
 
 // synthetic inputs (same streams as src/synth.cpp:8-81)
 struct Rng;

@@ -64,6 +64,8 @@ struct KParams {
     uint32_t dbias;             // per-step bias
     uint32_t tecjb;             // tec + tjb (may exceed 255)
     uint32_t fault;             // fault injection (verification only)
+    uint8_t* flag_out;          // relaxed variants: 1 = rescore exactly
+    uint32_t* flag_count;       // relaxed variants: number of flagged sequences
 };
 
 // ---------------------------------------------------------------------------
@@ -152,6 +154,7 @@ struct Dpx16 {
     static constexpr int CPW = 2;
     static constexpr bool kMsv = ALG == 0;
     static constexpr uint32_t NEG = kMsv ? 0u : 0x00800080u;
+    static constexpr bool kRelaxed = false;
     struct St {
         uint32_t B, base2, d2, ntj2;
     };
@@ -190,6 +193,9 @@ struct Dpx16 {
     __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
         s.B = __viaddmax_s16x2(e, s.ntj2, s.base2);
     }
+    __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
+    __device__ static __forceinline__ uint32_t inject(const St&) { return NEG; }
+    __device__ static __forceinline__ bool needs_exact(uint32_t, const St&) { return false; }
     __device__ static __forceinline__ uint32_t raw(uint32_t e) { return e & 0xffu; }
 };
 
@@ -205,6 +211,7 @@ struct Fp16 {
     static constexpr int CPW = 2;
     static constexpr bool kMsv = ALG == 0;
     static constexpr uint32_t NEG = 0u;  // +0.0 in both halves
+    static constexpr bool kRelaxed = false;
     struct St {
         uint32_t B, base2, d1, tj2;
     };
@@ -253,6 +260,9 @@ struct Fp16 {
         // max(base, E - (tec+tjb)); the difference may be negative -> f16 max
         s.B = as_u32(__hmax2(__hsub2(as_h2(e), as_h2(s.tj2)), as_h2(s.base2)));
     }
+    __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
+    __device__ static __forceinline__ uint32_t inject(const St&) { return NEG; }
+    __device__ static __forceinline__ bool needs_exact(uint32_t, const St&) { return false; }
     __device__ static __forceinline__ uint32_t raw(uint32_t e) {
         const float f = __low2float(as_h2(e));
         return kMsv ? uint32_t(f * 256.f + 0.5f) : 128u + uint32_t(f * 128.f + 0.5f);
@@ -264,6 +274,7 @@ struct Swar8 {
     static constexpr int CPW = 4;
     static constexpr bool kMsv = ALG == 0;
     static constexpr uint32_t NEG = kMsv ? 0u : 0x80808080u;
+    static constexpr bool kRelaxed = false;
     struct St {
         uint32_t B, base4, d4, tj4;
     };
@@ -298,7 +309,96 @@ struct Swar8 {
     __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
         s.B = __vmaxu4(s.base4, __vsubus4(e, s.tj4));
     }
+    __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
+    __device__ static __forceinline__ uint32_t inject(const St&) { return NEG; }
+    __device__ static __forceinline__ bool needs_exact(uint32_t, const St&) { return false; }
     __device__ static __forceinline__ uint32_t raw(uint32_t e) { return e & 0xffu; }
+};
+
+// Relaxed f16 variants: exact except on sequences they flag, which the host
+// rescoring pass (abi.cu) recomputes with the exact Fp16 kernel.
+//
+// SSV ("unsaturated"): q = (v-128)/256, table (dbias-cost)/256, one
+// HADD2.SAT per cell pair: max(v + dbias - cost, 128) without the 255 cap.
+// Identical to the saturating recurrence unless some cell exceeds
+// 255-dbias (before the first cap event both agree, and a cap event needs a
+// cell above 255-dbias, which the running E then records), so
+// raw >= 256-dbias is flagged.
+//
+// MSV ("lazy B"): cells live as w = max(v, B) in the linear f16 binade
+// p = 1 + (v-255)/2048 (bit pattern 0x3C00 - (255-v), one code per byte).
+// Per cell: HADD2.SAT adds dbias with the 1.0 cap (= byte 255) and one DPX
+// VIADDMNMX.S16 subtracts the cost and takes max(., B) on the bit pattern --
+// the next row's max(M, B) fused into this row's floor clamp.  When a
+// group's B grows after a row, a warp-uniform fix-up re-applies max(w, B').
+// E accumulates over w, so it can exceed the true E only while E <= base
+// (B <= max(base, E-tecjb)); B itself stays exact.  raw <= base(len) is
+// flagged.
+template <int ALG>
+struct Fp16Relaxed {
+    static constexpr int CPW = 2;
+    static constexpr bool kMsv = ALG == 0;
+    static constexpr bool kRelaxed = true;
+    static constexpr uint32_t NEG = 0u;
+    struct St {
+        uint32_t B, base2, d1, ntj2, base_v, cap;
+    };
+    __device__ static __forceinline__ uint32_t splat(float f) {
+        return as_u32(__float2half2_rn(f));
+    }
+    __device__ static __forceinline__ void init(St& s, uint32_t base, const KParams& p) {
+        if constexpr (kMsv) {
+            s.base2 = (0x3C00u - (255u - base)) * 0x00010001u;
+            s.B = s.base2;
+            s.d1 = splat(float(p.dbias) / 2048.f);
+            s.ntj2 = (0u - p.tecjb) & 0xffffu;
+            s.ntj2 |= s.ntj2 << 16;
+            s.base_v = base;
+        } else {
+            s.cap = 256u - p.dbias;
+        }
+    }
+    __device__ static __forceinline__ uint32_t init_word(const St& s) { return kMsv ? s.B : 0u; }
+    __device__ static __forceinline__ uint32_t inject(const St& s) { return kMsv ? s.B : 0u; }
+    __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
+        if constexpr (kMsv) {
+            const uint32_t pp = as_u32(__hadd2_sat(as_h2(x), as_h2(s.d1)));
+            return __viaddmax_s16x2(pp, c, s.B);
+        } else {
+            return as_u32(__hadd2_sat(as_h2(x), as_h2(c)));
+        }
+    }
+    __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
+        return __vimax3_u16x2(E, a, b);
+    }
+    __device__ static __forceinline__ uint32_t acc1(uint32_t E, uint32_t a) {
+        return __vmaxu2(E, a);
+    }
+    __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
+        return __byte_perm(top, up, 0x1076);
+    }
+    template <int L>
+    __device__ static __forceinline__ uint32_t group_reduce(uint32_t E) {
+        const uint32_t e = __vmaxu2(E, __byte_perm(E, E, 0x1032));
+        return group_max<L>(e);
+    }
+    __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
+        s.B = __viaddmax_s16x2(e, s.ntj2, s.base2);
+    }
+    __device__ static __forceinline__ uint32_t raw(uint32_t e) {
+        if constexpr (kMsv) {
+            // bit pattern 0x3B01 is byte 0; below it only the E accumulators'
+            // initial +0.0 (no row seen: empty sequence) -> the floor
+            const uint32_t b = e & 0xffffu;
+            return b >= 0x3B01u ? b - 0x3B01u : 0u;
+        } else {
+            const float f = __low2float(as_h2(e));
+            return 128u + uint32_t(f * 256.f + 0.5f);
+        }
+    }
+    __device__ static __forceinline__ bool needs_exact(uint32_t raw, const St& s) {
+        return kMsv ? raw <= s.base_v : raw >= s.cap;
+    }
 };
 
 // ---------------------------------------------------------------------------
@@ -346,7 +446,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
         V::init(st, p.base_tab[len], p);
         uint32_t g[H];
 #pragma unroll
-        for (int h = 0; h < H; ++h) g[h] = V::NEG;
+        for (int h = 0; h < H; ++h) g[h] = V::init_word(st);
         // four independent running maxima keep the E chain short
         uint32_t e0 = V::NEG, e1 = V::NEG, e2 = V::NEG, e3 = V::NEG;
 
@@ -385,10 +485,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
                     const uint32_t* tp = tab_lane + x * P;
                     // the register holding cell H-1 becomes cell 0 (stripe shift)
                     const int stop = ((H - 1 - r) % H + H) % H;
-                    uint32_t up = V::NEG;
+                    uint32_t up = V::inject(st);
                     if constexpr (L > 1) {
                         up = __shfl_up_sync(kFull, g[stop], 1, L);
-                        if (oig == 0) up = V::NEG;
+                        if (oig == 0) up = V::inject(st);
                     }
 #pragma unroll
                     for (int h4 = H / 4 - 1; h4 >= 0; --h4) {
@@ -415,7 +515,17 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
                         const uint32_t E =
                             V::template group_reduce<L>(V::acc2(V::acc2(e0, e1, e2), e3, e3));
                         e0 = E;
-                        V::update_B(st, E);
+                        if constexpr (V::kRelaxed) {
+                            // lazy B: re-apply max(w, B') only when some B grew
+                            const uint32_t Bold = st.B;
+                            V::update_B(st, E);
+                            if (__any_sync(kFull, st.B != Bold)) {
+#pragma unroll
+                                for (int h = 0; h < H; ++h) g[h] = __vmaxu2(g[h], st.B);
+                            }
+                        } else {
+                            V::update_B(st, E);
+                        }
                     }
                 }
             }
@@ -432,11 +542,20 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
         uint32_t E = V::acc2(V::acc2(e0, e1, e2), e3, e3);
         if constexpr (!V::kMsv) E = V::template group_reduce<L>(E);
         uint32_t raw = V::raw(E);
+        bool exact_needed = false;
+        if constexpr (V::kRelaxed) {
+            exact_needed = V::needs_exact(raw, st);
+            raw = raw > 255u ? 255u : raw;
+        }
         if (p.fault && grp == 0 && raw < 255u) raw += 1u;  // verification aid
         const uint32_t oi = p.out_idx[sidx];
         if (oig == 0 && oi != 0xffffffffu) {
             p.raw_out[oi] = uint8_t(raw);
             p.pass_out[oi] = uint8_t(raw == 255u || raw >= p.rawmin_tab[len]);
+            if constexpr (V::kRelaxed) {
+                p.flag_out[oi] = exact_needed ? 1u : 0u;
+                if (exact_needed) atomicAdd(p.flag_count, 1u);
+            }
         }
     }
 }

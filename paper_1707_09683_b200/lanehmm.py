@@ -64,6 +64,7 @@ class Variant(enum.IntEnum):
     Dpx16 = 1
     Fp16 = 2
     Swar8 = 3
+    Fp16x = 4
 
 
 @dataclass

@@ -28,7 +28,8 @@ def main():
     s = P.Scanner(0)
     s.set_database(db)
     res = db.total_residues()
-    vmap = {"dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16, "swar8": P.Variant.Swar8}
+    vmap = {"dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16, "swar8": P.Variant.Swar8,
+            "fp16x": P.Variant.Fp16x}
     for vn in args.variants.split(","):
         cpw = 4 if vn == "swar8" else 2
         for L in gen_instances.LANES:

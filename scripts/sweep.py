@@ -18,7 +18,8 @@ import paper_1707_09683_b200 as P  # noqa: E402
 
 ROWS = {P.Variant.Dpx16: [4, 8, 12, 16, 24, 32, 40, 48, 56, 64],
         P.Variant.Fp16: [4, 8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 52, 56, 60, 64, 68, 72],
-        P.Variant.Swar8: [4, 8, 16, 24, 32]}
+        P.Variant.Swar8: [4, 8, 16, 24, 32],
+        P.Variant.Fp16x: [4, 8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 52, 56, 60, 64, 68, 72]}
 
 
 def main():
@@ -35,7 +36,8 @@ def main():
     s = P.Scanner(0)
     s.set_database(db)
     res = db.total_residues()
-    vmap = {"dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16, "swar8": P.Variant.Swar8}
+    vmap = {"dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16, "swar8": P.Variant.Swar8,
+            "fp16x": P.Variant.Fp16x}
     for m in [int(x) for x in args.models.split(",")]:
         hmm = P.Rng(7000 + m).random_profile(m)
         costs = P.quantize_emissions(hmm, q)

@@ -11,7 +11,7 @@ import paper_1707_09683_b200 as P
 
 pytestmark = pytest.mark.gpu
 
-VARIANTS = [P.Variant.Dpx16, P.Variant.Fp16, P.Variant.Swar8]
+VARIANTS = [P.Variant.Dpx16, P.Variant.Fp16, P.Variant.Swar8, P.Variant.Fp16x]
 QUANTS = [P.QuantParams(), P.QuantParams(3.0, 120, 3, 20, 20), P.QuantParams(2.0, 240, 10, 1, 5),
           P.QuantParams(3.0, 0, 0, 0, 0)]
 
@@ -197,7 +197,7 @@ def test_streamed_scan_matches_resident_scan(ora):
     returns exactly the resident scan's scores and pass bits."""
     rng = P.Rng(21)
     hmm = rng.random_profile(333)
-    db = rng.lognormal_records(20000, 290, 0.65, 2)
+    db = rng.lognormal_records(150000, 290, 0.65, 2)  # ~55 MB packed: 3 pieces
     q = P.QuantParams(3.0, 120, 3, 20, 20)
     costs = P.quantize_emissions(hmm, q)
     want = ora.scan_flat(0, costs.bytes, db.residues, db.offsets, oq(q))
@@ -251,3 +251,24 @@ def test_device_pipeline_matches_reference_library(ref):
         np.testing.assert_array_equal(rep.ssv_raw, ssv)
         np.testing.assert_array_equal(rep.passed, surv)
         np.testing.assert_array_equal(rep.msv_raw, msv)
+
+
+@pytest.mark.parametrize("alg", [P.Algorithm.Msv, P.Algorithm.Ssv], ids=lambda a: a.name)
+def test_relaxed_variant_rescoring_is_exact(ora, alg):
+    """FP16X flags the sequences its relaxed arithmetic cannot certify (SSV
+    cells above 255-dbias; MSV raw <= base) and rescores them exactly: force
+    many flags with planted motifs (SSV overflow) and a flat profile (MSV
+    raw == base), and check every byte against the oracle."""
+    rng = P.Rng(99)
+    hmm = rng.random_profile(120)
+    db = rng.random_records(4000, 20, 400, plant=(hmm, 0.5))
+    flat = P.ProfileHMM("flat", 120, np.zeros((120, 20)), 0.7, 2.0)
+    for prof, q in ((hmm, P.QuantParams()), (hmm, P.QuantParams(3.0, 120, 3, 20, 20)),
+                    (flat, P.QuantParams()), (hmm, P.QuantParams(2.0, 240, 10, 1, 5))):
+        costs = P.quantize_emissions(prof, q)
+        want = ora.scan_flat(int(alg), costs.bytes, db.residues, db.offsets, oq(q))
+        rep = scan(costs, q, db, prof, alg=alg, variant=P.Variant.Fp16x, threshold=0.3)
+        np.testing.assert_array_equal(rep.raw, want)
+        assert rep.variant == int(P.Variant.Fp16x)
+        if prof is flat and alg == P.Algorithm.Msv:
+            assert rep.stats["recomputed"] > 0
