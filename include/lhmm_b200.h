@@ -21,11 +21,19 @@
  *                               src/engine.cpp:488-594, include/lanehmm/engine.hpp:90-101
  *   lhmm_filter_pipeline     <- filter_pipeline         src/engine.cpp:596-657, include/lanehmm/engine.hpp:130-132
  *   lhmm_rng_* / lhmm_synth_* <- synth::*               src/synth.cpp:8-81, include/lanehmm/synth.hpp
+ *   lhmm_ingest_fasta[_file] <- ingest_fasta / ingest_fasta_file src/seqdb.cpp:35-83, include/lanehmm/seqdb.hpp:58-59
+ *   lhmm_read_block_db       <- read_block_db (+ reconstruct_sequences) src/seqdb.cpp:319-385, 229-250
+ *   lhmm_write_block_db      <- write_block_db          src/seqdb.cpp:281-317, include/lanehmm/seqdb.hpp:75
+ *   lhmm_pack_blocks         <- pack_blocks (Algorithm 1) src/seqdb.cpp:109-188, include/lanehmm/seqdb.hpp:70
+ *   lhmm_balance_stats       <- balance_stats           src/seqdb.cpp:190-227, include/lanehmm/seqdb.hpp:72
+ *   lhmm_parse_profile       <- parse_profile           src/profile.cpp:49-123, include/lanehmm/profile.hpp:71
+ *   lhmm_serialize_profile   <- serialize_profile       src/profile.cpp:125-142, include/lanehmm/profile.hpp:72
  *
  * Error convention: every function returns LHMM_OK (0) or a status; the
  * message of the last failure on the calling thread is lhmm_last_error().
- * LHMM_ERR_CONTRACT corresponds to the reference's ContractError and
- * LHMM_ERR_DATA to DataError (include/lanehmm/errors.hpp:10-32).
+ * LHMM_ERR_CONTRACT corresponds to the reference's ContractError,
+ * LHMM_ERR_DATA to DataError and LHMM_ERR_PARSE to ParseError
+ * (include/lanehmm/errors.hpp:10-32).
  *
  * Threading: a context is bound to one device and one stream and is not
  * thread-safe; separate contexts are independent.
@@ -47,7 +55,8 @@ enum lhmm_status {
     LHMM_ERR_CONTRACT = 1, /* caller broke a precondition (ContractError) */
     LHMM_ERR_DATA = 2,     /* malformed data (DataError) */
     LHMM_ERR_CUDA = 3,     /* CUDA runtime / launch failure */
-    LHMM_ERR_NOMEM = 4     /* host or device allocation failed */
+    LHMM_ERR_NOMEM = 4,    /* host or device allocation failed */
+    LHMM_ERR_PARSE = 5     /* malformed text input (ParseError; message "line N: ...") */
 };
 
 enum lhmm_alg { LHMM_MSV = 0, LHMM_SSV = 1 };
@@ -204,6 +213,67 @@ int lhmm_synth_lognormal_records(lhmm_rng* rng, uint64_t count, double median, d
                                  uint64_t min_len, uint64_t* total);
 int lhmm_synth_plant_motifs(lhmm_rng* rng, const double* scores, uint32_t m, double fraction);
 int lhmm_synth_take(lhmm_rng* rng, uint8_t* residues, uint64_t* offsets /* count+1 */);
+
+/* ---- sequence sets and the reference's on-disk formats -------------------
+ * A sequence set owns flat residue codes (nseq+1 u64 offsets) and ids
+ * (concatenated bytes + nseq+1 u64 offsets); feed its view to
+ * lhmm_set_database.  A set read from an LHMM block database, or produced by
+ * lhmm_pack_blocks, also carries the block layout: its sequences are in
+ * (block, column, ordinal) order -- the reference's hit order -- with
+ * block_rows[blocks] and column_counts[blocks * lanes]. */
+typedef struct lhmm_seqset lhmm_seqset;
+
+/* balance_stats (BalanceStats, include/lanehmm/seqdb.hpp:44-52) */
+typedef struct lhmm_balance {
+    double avg_m, sd_m;             /* block heights */
+    double avg_endings, sd_endings; /* sequences per block */
+    double prr;                     /* '#' padding bytes / real residues */
+    uint64_t total_seqs, total_residues;
+} lhmm_balance;
+
+/* ids/id_offsets may be NULL: ids default to "s<k>". */
+int lhmm_seqset_create(const uint8_t* residues, const uint64_t* offsets, uint64_t nseq,
+                       const char* ids, const uint64_t* id_offsets, lhmm_seqset** out);
+int lhmm_seqset_destroy(lhmm_seqset* set);
+/* Borrowed pointers, valid until the set is destroyed (any may be NULL). */
+int lhmm_seqset_view(const lhmm_seqset* set, uint64_t* nseq, uint64_t* nres,
+                     const uint8_t** residues, const uint64_t** offsets, const char** ids,
+                     const uint64_t** id_offsets);
+/* blocks = 0 when the set has no block layout. */
+int lhmm_seqset_layout(const lhmm_seqset* set, uint32_t* lanes, uint64_t* blocks,
+                       const uint64_t** block_rows, const uint32_t** column_counts);
+/* Attach an explicit block layout (e.g. a BlockSet built by hand). */
+int lhmm_seqset_set_layout(lhmm_seqset* set, uint32_t lanes, uint64_t blocks,
+                           const uint64_t* block_rows, const uint32_t* column_counts);
+
+/* FASTA: first whitespace-delimited header token is the id ("seq<k>" when
+ * empty); letters case-insensitive, non-canonical -> unknown (20).  Errors
+ * are DATA with the reference's messages. */
+int lhmm_ingest_fasta(const char* text, size_t len, lhmm_seqset** out);
+int lhmm_ingest_fasta_file(const char* path, lhmm_seqset** out);
+
+/* LHMM block database (docs/formats.md).  The reader checks magic, version,
+ * truncation and every block's CRC32 like the reference, and additionally
+ * the column streams (the engine's structural checks, src/engine.cpp:404-440)
+ * so that a set that reads is scannable. */
+int lhmm_read_block_db(const char* path, lhmm_seqset** out);
+/* Writes the set's block layout; byte-identical to write_block_db of the
+ * same BlockSet. */
+int lhmm_write_block_db(const lhmm_seqset* set, const char* path);
+/* Algorithm 1 packing into block_count blocks of `lanes` containers. */
+int lhmm_pack_blocks(const lhmm_seqset* set, uint64_t block_count, uint32_t lanes,
+                     lhmm_seqset** out);
+int lhmm_balance_stats(const lhmm_seqset* set, lhmm_balance* stats);
+
+/* ---- profile text format (docs/formats.md) --------------------------------
+ * Call with scores == NULL to learn *length, then with a LENG x 20 buffer.
+ * Errors are LHMM_ERR_PARSE with the reference's "line N: ..." messages. */
+int lhmm_parse_profile(const char* text, size_t len, uint32_t* length, double* lambda,
+                       double* tau, double* scores, size_t scores_cap, char* name,
+                       size_t name_cap);
+/* *needed = text length; written (NUL-terminated) when cap > *needed. */
+int lhmm_serialize_profile(const char* name, uint32_t m, const double* scores, double lambda,
+                           double tau, char* out, size_t cap, size_t* needed);
 
 #ifdef __cplusplus
 }

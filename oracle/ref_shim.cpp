@@ -10,7 +10,9 @@
 //   - the reference CPU engine scan_database / scan_sequences_s1
 //     (src/engine.cpp:496-594) with the reference geometry policy
 //     (src/select.cpp:16-48) -- the CPU baseline timed beside the GPU;
-//   - filter_pipeline (src/engine.cpp:596-657).
+//   - filter_pipeline (src/engine.cpp:596-657);
+//   - the database / profile I/O (src/seqdb.cpp:35-385, src/profile.cpp:49-142)
+//     that the native ingest (csrc/seqdb_io.cpp) is checked against.
 // Nothing in the product path links this file.
 #include <algorithm>
 #include <chrono>
@@ -21,7 +23,11 @@
 #include <string>
 #include <vector>
 
+#include <sstream>
+
 #include "lanehmm/engine.hpp"
+#include "lanehmm/profile.hpp"
+#include "lanehmm/seqdb.hpp"
 #include "lanehmm/oracle.hpp"
 #include "lanehmm/select.hpp"
 #include "lanehmm/synth.hpp"
@@ -247,6 +253,112 @@ long ref_filter_pipeline(const double* scores, uint32_t m, double lambda, double
         g_err = e.what();
         return -1;
     }
+}
+
+// --- database / profile I/O (src/seqdb.cpp, src/profile.cpp) -----------------
+// Records <-> flat arrays with ids (blob + offsets)
+void* ref_records_from_flat(const uint8_t* residues, const uint64_t* offsets, uint64_t nseq,
+                            const char* ids, const uint64_t* id_off) {
+    auto* r = new Records;
+    r->recs.resize(nseq);
+    for (uint64_t k = 0; k < nseq; ++k) {
+        r->recs[k].id.assign(ids + id_off[k], ids + id_off[k + 1]);
+        r->recs[k].residues.assign(residues + offsets[k], residues + offsets[k + 1]);
+    }
+    return r;
+}
+uint64_t ref_records_id_bytes(void* records) {
+    uint64_t n = 0;
+    for (const auto& r : static_cast<Records*>(records)->recs) n += r.id.size();
+    return n;
+}
+void ref_records_ids(void* records, char* blob, uint64_t* id_off) {
+    uint64_t pos = 0, k = 0;
+    for (const auto& r : static_cast<Records*>(records)->recs) {
+        id_off[k++] = pos;
+        std::memcpy(blob + pos, r.id.data(), r.id.size());
+        pos += r.id.size();
+    }
+    id_off[k] = pos;
+}
+void* ref_ingest_fasta(const char* text, uint64_t len) {
+    try {
+        std::istringstream in(std::string(text, len));
+        auto* r = new Records;
+        r->recs = ingest_fasta(in);
+        return r;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+// pack_blocks + write_block_db; stats7 = balance_stats fields.  0 / -1.
+int ref_pack_write(void* records, uint64_t block_count, uint32_t lanes, const char* path,
+                   double* stats7) {
+    try {
+        BlockSet bs = pack_blocks(static_cast<Records*>(records)->recs, block_count, lanes);
+        write_block_db(bs, path);
+        BalanceStats st = balance_stats(bs);
+        double v[7] = {st.avgM, st.sdM, st.avgEndings, st.sdEndings, st.prr,
+                       double(st.totalSeqs), double(st.totalResidues)};
+        std::memcpy(stats7, v, sizeof v);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+// read_block_db + reconstruct_sequences (+ balance_stats of the read set)
+void* ref_read_block_db(const char* path, double* stats7) {
+    try {
+        BlockSet bs = read_block_db(path);
+        BalanceStats st = balance_stats(bs);
+        double v[7] = {st.avgM, st.sdM, st.avgEndings, st.sdEndings, st.prr,
+                       double(st.totalSeqs), double(st.totalResidues)};
+        std::memcpy(stats7, v, sizeof v);
+        auto* r = new Records;
+        r->recs = reconstruct_sequences(bs);
+        return r;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+// parse_profile: returns LENG (scores copied when cap allows) or -1
+long ref_parse_profile(const char* text, uint64_t len, double* lambda, double* tau,
+                       double* scores, uint64_t cap, char* name, uint64_t name_cap) {
+    try {
+        ProfileHMM h = parse_profile(std::string(text, len));
+        *lambda = h.lambda;
+        *tau = h.tau;
+        if (scores && cap >= h.matchScores.size())
+            std::memcpy(scores, h.matchScores.data(), h.matchScores.size() * sizeof(double));
+        if (name && name_cap) {
+            size_t k = std::min<size_t>(name_cap - 1, h.name.size());
+            std::memcpy(name, h.name.data(), k);
+            name[k] = 0;
+        }
+        return long(h.length);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+// serialize_profile into out (cap bytes); returns the text length
+uint64_t ref_serialize_profile(const char* name, uint32_t m, const double* scores, double lambda,
+                               double tau, char* out, uint64_t cap) {
+    ProfileHMM h;
+    h.name = name;
+    h.length = m;
+    h.lambda = lambda;
+    h.tau = tau;
+    h.matchScores.assign(scores, scores + size_t(m) * kAminoCount);
+    std::string t = serialize_profile(h);
+    if (out && cap > t.size()) {
+        std::memcpy(out, t.data(), t.size());
+        out[t.size()] = 0;
+    }
+    return t.size();
 }
 
 }  // extern "C"

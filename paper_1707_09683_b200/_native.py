@@ -38,6 +38,12 @@ class ScanStatsC(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class BalanceC(C.Structure):
+    _fields_ = [("avg_m", C.c_double), ("sd_m", C.c_double), ("avg_endings", C.c_double),
+                ("sd_endings", C.c_double), ("prr", C.c_double), ("total_seqs", C.c_uint64),
+                ("total_residues", C.c_uint64)]
+
+
 u8p = C.POINTER(C.c_uint8)
 u64p = C.POINTER(C.c_uint64)
 u32p = C.POINTER(C.c_uint32)
@@ -88,6 +94,22 @@ SIGNATURES = {
                                                C.c_uint64, u64p]),
     "lhmm_synth_plant_motifs": (C.c_int, [vp, f64p, C.c_uint32, C.c_double]),
     "lhmm_synth_take": (C.c_int, [vp, u8p, u64p]),
+    "lhmm_seqset_create": (C.c_int, [u8p, u64p, C.c_uint64, C.c_char_p, u64p, C.POINTER(vp)]),
+    "lhmm_seqset_destroy": (C.c_int, [vp]),
+    "lhmm_seqset_view": (C.c_int, [vp, u64p, u64p, C.POINTER(u8p), C.POINTER(u64p),
+                                   C.POINTER(C.c_void_p), C.POINTER(u64p)]),
+    "lhmm_seqset_layout": (C.c_int, [vp, u32p, u64p, C.POINTER(u64p), C.POINTER(u32p)]),
+    "lhmm_seqset_set_layout": (C.c_int, [vp, C.c_uint32, C.c_uint64, u64p, u32p]),
+    "lhmm_ingest_fasta": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(vp)]),
+    "lhmm_ingest_fasta_file": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "lhmm_read_block_db": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "lhmm_write_block_db": (C.c_int, [vp, C.c_char_p]),
+    "lhmm_pack_blocks": (C.c_int, [vp, C.c_uint64, C.c_uint32, C.POINTER(vp)]),
+    "lhmm_balance_stats": (C.c_int, [vp, C.POINTER(BalanceC)]),
+    "lhmm_parse_profile": (C.c_int, [C.c_char_p, C.c_size_t, u32p, f64p, f64p, f64p, C.c_size_t,
+                                     C.c_char_p, C.c_size_t]),
+    "lhmm_serialize_profile": (C.c_int, [C.c_char_p, C.c_uint32, f64p, C.c_double, C.c_double,
+                                         C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
 }
 
 _lib = None

@@ -83,7 +83,7 @@ def build(verbose=False, jobs=None, defines=(), tag=""):
             list(ex.map(lambda so: _compile(so[0], so[1], verbose), todo))
     if todo or not os.path.exists(LIB):
         cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fPIC,-fopenmp", "-o", LIB] + objs + \
-            ["-lgomp"]
+            ["-lgomp", "-lz"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

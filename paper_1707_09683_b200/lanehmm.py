@@ -37,6 +37,10 @@ class DataError(RuntimeError):
     """Structurally invalid data (errors.hpp:23-27)."""
 
 
+class ParseError(RuntimeError):
+    """Malformed input text, "line N: ..." (errors.hpp:10-20)."""
+
+
 class CudaError(RuntimeError):
     pass
 
@@ -51,6 +55,8 @@ def _check(rc):
         raise DataError(msg)
     if rc == 4:
         raise MemoryError(msg)
+    if rc == 5:
+        raise ParseError(msg)
     raise CudaError(msg)
 
 
