@@ -88,6 +88,9 @@ typedef struct lhmm_scan_options {
     uint32_t rows;      /* striped rows H per lane; 0 = auto */
     double threshold;   /* pass iff pValue <= threshold || overflow; in [0,1] */
     int fault_injection;/* verification aid: corrupts one lane's E (ScanOptions.faultInjection) */
+    int reorder_mode;   /* 0: -inf injected at stripe 0 (normative); 1: the paper's literal
+                           wrap of the top stripe (ReorderMode::PaperWrap, a non-normative
+                           study mode, src/vwarp.cpp:27-64) */
 } lhmm_scan_options;
 
 typedef struct lhmm_scan_stats {

@@ -24,7 +24,8 @@ class Quant(C.Structure):
 
 class ScanOptionsC(C.Structure):
     _fields_ = [("alg", C.c_int), ("variant", C.c_int), ("lanes", C.c_uint32),
-                ("rows", C.c_uint32), ("threshold", C.c_double), ("fault_injection", C.c_int)]
+                ("rows", C.c_uint32), ("threshold", C.c_double), ("fault_injection", C.c_int),
+                ("reorder_mode", C.c_int)]
 
 
 class ScanStatsC(C.Structure):

@@ -347,6 +347,8 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         return set_error(LHMM_ERR_CONTRACT, "unknown algorithm");
     if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_FP16X)
         return set_error(LHMM_ERR_CONTRACT, "unknown kernel variant");
+    if (opt->reorder_mode != 0 && opt->reorder_mode != 1)
+        return set_error(LHMM_ERR_CONTRACT, "unknown reorder mode");
     ProfileSlot& pf = c->profiles[c->current];
     int variant = opt->variant;
     uint32_t L = opt->lanes, H = opt->rows;
@@ -446,6 +448,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     p.dbias = pf.q.dbias;
     p.tecjb = uint32_t(pf.q.tec) + uint32_t(pf.q.tjb);
     p.fault = opt->fault_injection ? 1u : 0u;
+    p.wrap = opt->reorder_mode == 1 ? 1u : 0u;
     const bool relaxed = variant == LHMM_VARIANT_FP16X;
     if (relaxed) {
         if (int rc = c->d_flag.reserve(std::max<uint64_t>(c->db.n_local, 1))) return rc;

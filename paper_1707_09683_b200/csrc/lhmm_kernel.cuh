@@ -64,6 +64,7 @@ struct KParams {
     uint32_t dbias;             // per-step bias
     uint32_t tecjb;             // tec + tjb (may exceed 255)
     uint32_t fault;             // fault injection (verification only)
+    uint32_t wrap;              // paper-literal stripe wrap instead of -inf injection
     uint8_t* flag_out;          // relaxed variants: 1 = rescore exactly
     uint32_t* flag_count;       // relaxed variants: number of flagged sequences
 };
@@ -428,6 +429,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
     const uint32_t grp = lane / L;
     const uint32_t P = p.res_stride;
     const uint32_t* tab_lane = smem + (grp % COPIES) * p.copy_stride + 4u * oig;
+    // stripe-shift source: the previous lane of the group; lane 0 of a group
+    // gets -inf (normative) or, in the paper's wrap mode, the last lane's top
+    const uint32_t shift_src = (lane & ~uint32_t(L - 1)) | ((lane + L - 1) & uint32_t(L - 1));
+    const bool inject_here = oig == 0 && !p.wrap;
 
     for (;;) {
         uint32_t item = 0;
@@ -485,10 +490,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
                     const uint32_t* tp = tab_lane + x * P;
                     // the register holding cell H-1 becomes cell 0 (stripe shift)
                     const int stop = ((H - 1 - r) % H + H) % H;
-                    uint32_t up = V::inject(st);
+                    uint32_t up;
                     if constexpr (L > 1) {
-                        up = __shfl_up_sync(kFull, g[stop], 1, L);
-                        if (oig == 0) up = V::inject(st);
+                        up = __shfl_sync(kFull, g[stop], shift_src);
+                        if (inject_here) up = V::inject(st);
+                    } else {
+                        up = inject_here ? V::inject(st) : g[stop];
                     }
 #pragma unroll
                     for (int h4 = H / 4 - 1; h4 >= 0; --h4) {

@@ -18,7 +18,8 @@
 // Differences: the B200 engine picks its own device geometry (results are
 // geometry-independent and bit-exact); the requested Geometry is validated
 // exactly as the reference does.  ReorderMode::PaperWrap (a non-normative CPU
-// study mode) is rejected with ContractError.
+// study mode) maps to the kernel's wrap mode: stripe 0 takes the
+// top stripe's value instead of -inf, on the B200 striping.
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
@@ -166,7 +167,7 @@ struct DeviceScan {
 
 // Scans a flat set on the device; caller holds g_mu.
 DeviceScan device_scan(const CostMatrix& costs, const Flat& flat, const QuantParams& q,
-                       double lambda, double tau, Algorithm alg, bool fault) {
+                       double lambda, double tau, Algorithm alg, bool fault, bool wrap = false) {
     DeviceScan ds;
     const uint64_t n = flat.protos.size();
     ds.raw.assign(n, 0);
@@ -184,6 +185,7 @@ DeviceScan device_scan(const CostMatrix& costs, const Flat& flat, const QuantPar
     o.variant = LHMM_VARIANT_AUTO;
     o.threshold = 1.0;
     o.fault_injection = fault ? 1 : 0;
+    o.reorder_mode = wrap ? 1 : 0;
     std::vector<uint8_t> pass(n);
     lhmm_scan_stats st{};
     check(lhmm_scan(c, &o, ds.raw.data(), pass.data(), &st));
@@ -212,13 +214,6 @@ std::vector<uint64_t> static_partition(uint64_t n, int workers) {
     const uint64_t q = n / uint64_t(workers), r = n % uint64_t(workers);
     for (int w = 0; w < workers; ++w) per[size_t(w)] = q + (uint64_t(w) < r ? 1 : 0);
     return per;
-}
-
-void check_options(const ScanOptions& opt) {
-    if (opt.reorderMode != vwarp::ReorderMode::InjectNegInf)
-        throw ContractError(
-            "PaperWrap reorder is a CPU study mode; the B200 engine implements the normative "
-            "-inf injection only");
 }
 
 }  // namespace
@@ -263,13 +258,12 @@ HitResult finalize_hit(uint8_t raw, uint64_t seqLen, double lambda, double tau,
 std::vector<HitResult> scan_block(const KernelParams& kp, const BlockSet& bs, uint32_t blockIndex) {
     kp.validate();
     if (blockIndex >= bs.blocks.size()) throw ContractError("block index out of range");
-    if (kp.reorderMode != vwarp::ReorderMode::InjectNegInf)
-        throw ContractError("PaperWrap reorder is not supported by the B200 engine");
     Flat flat;
     flatten_block(bs, blockIndex, flat);
     const CostMatrix costs = costs_from_striped(*kp.profile);
     std::lock_guard<std::mutex> lk(g_mu);
-    DeviceScan ds = device_scan(costs, flat, kp.quant, kp.lambda, kp.tau, kp.alg, kp.faultInjection);
+    DeviceScan ds = device_scan(costs, flat, kp.quant, kp.lambda, kp.tau, kp.alg, kp.faultInjection,
+                                 kp.reorderMode == vwarp::ReorderMode::PaperWrap);
     return make_hits(flat, ds, kp.lambda, kp.tau, kp.quant, kp.alg);
 }
 
@@ -280,7 +274,6 @@ ScanReport scan_database(const ProfileHMM& hmm, const CostMatrix& costs, const B
         throw DataError("geometry capacity " + std::to_string(g.capacity()) +
                         " below model length " + std::to_string(costs.modelLength));
     q.validate();
-    check_options(opt);
 
     ScanReport report;
     report.alg = opt.alg;
@@ -301,7 +294,8 @@ ScanReport scan_database(const ProfileHMM& hmm, const CostMatrix& costs, const B
     DeviceScan ds;
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        ds = device_scan(costs, flat, q, hmm.lambda, hmm.tau, opt.alg, opt.faultInjection);
+        ds = device_scan(costs, flat, q, hmm.lambda, hmm.tau, opt.alg, opt.faultInjection,
+                         opt.reorderMode == vwarp::ReorderMode::PaperWrap);
     }
     report.elapsedSeconds = ds.seconds;
     report.gcups = ds.seconds > 0.0 ? double(report.totalResidues) * costs.modelLength /
@@ -318,7 +312,6 @@ ScanReport scan_sequences_s1(const ProfileHMM& hmm, const CostMatrix& costs,
     if (records.empty()) throw DataError("no sequences to scan");
     Geometry g = minimal_geometry(1, costs.modelLength);
     q.validate();
-    check_options(opt);
     ScanReport report;
     report.alg = opt.alg;
     report.geometry = g;
@@ -337,7 +330,8 @@ ScanReport scan_sequences_s1(const ProfileHMM& hmm, const CostMatrix& costs,
     DeviceScan ds;
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        ds = device_scan(costs, flat, q, hmm.lambda, hmm.tau, opt.alg, opt.faultInjection);
+        ds = device_scan(costs, flat, q, hmm.lambda, hmm.tau, opt.alg, opt.faultInjection,
+                         opt.reorderMode == vwarp::ReorderMode::PaperWrap);
     }
     report.totalResidues = flat.residue_count;
     report.elapsedSeconds = ds.seconds;
@@ -383,7 +377,8 @@ PipelineReport filter_pipeline(const ProfileHMM& hmm, const CostMatrix& costs, c
         {
             std::lock_guard<std::mutex> lk(g_mu);
             ds = device_scan(costs, surv, q, hmm.lambda, hmm.tau, Algorithm::Msv,
-                             opt.faultInjection);
+                             opt.faultInjection,
+                             opt.reorderMode == vwarp::ReorderMode::PaperWrap);
         }
         rep.msvSeconds = ds.seconds;
         auto msv = make_hits(surv, ds, hmm.lambda, hmm.tau, q, Algorithm::Msv);

@@ -161,13 +161,15 @@ class ScanOptions:
     rows: int = 0
     threshold: float = 0.02
     fault_injection: bool = False
+    paper_wrap: bool = False  # ReorderMode::PaperWrap (non-normative study mode)
     workers: int = 1    # accepted for interface parity; must be >= 1
 
     def c(self):
         if self.workers < 1:
             raise ContractError("worker count must be >= 1")
         return _native.ScanOptionsC(int(self.alg), int(self.variant), self.lanes, self.rows,
-                                    float(self.threshold), int(bool(self.fault_injection)))
+                                    float(self.threshold), int(bool(self.fault_injection)),
+                                    int(bool(self.paper_wrap)))
 
 
 @dataclass

@@ -60,10 +60,9 @@ def run_unit(path, *args):
 
 @pytest.mark.gpu
 def test_reference_unit_tests_on_b200_engine():
-    """test_engine.cpp / test_select.cpp through the B200 engine.  Only the
-    ReorderMode::PaperWrap case is excluded: that non-normative CPU study
-    mode is rejected by the drop-in."""
-    n, failed, out = run_unit(UNIT_B200, "file=test_engine,test_select", "skip=paper-literal")
+    """test_engine.cpp / test_select.cpp through the B200 engine, every case
+    (ReorderMode::PaperWrap included: the kernel's wrap mode)."""
+    n, failed, out = run_unit(UNIT_B200, "file=test_engine,test_select")
     assert n >= 20 and failed == 0, out
 
 

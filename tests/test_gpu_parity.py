@@ -272,3 +272,53 @@ def test_relaxed_variant_rescoring_is_exact(ora, alg):
         assert rep.variant == int(P.Variant.Fp16x)
         if prof is flat and alg == P.Algorithm.Msv:
             assert rep.stats["recomputed"] > 0
+
+
+def wrap_model(alg, costs, m, seq, q, base):
+    """The kernel's paper-wrap semantics (ReorderMode::PaperWrap analogue,
+    src/vwarp.cpp:27-64) on a model whose striped capacity equals m: node 1
+    takes node m's previous-row value instead of -inf."""
+    c = costs.reshape(m, 21).astype(np.int32)
+    floor = 0 if alg == P.Algorithm.Msv else 0x80
+    M = np.full(m, floor, np.int32)
+    E, B = floor, base
+    for x in seq:
+        prev = np.concatenate(([M[-1]], M[:-1]))
+        if alg == P.Algorithm.Msv:
+            v = np.minimum(np.maximum(prev, B) + q.dbias, 255) - c[:, x]
+            M = np.maximum(v, 0)
+            E = max(E, int(M.max()))
+            B = max(base, E - q.tec - q.tjb)
+        else:
+            v = np.minimum(prev + q.dbias, 255) - c[:, x]
+            M = np.maximum(v, 0x80)
+            E = max(E, int(M.max()))
+    return E
+
+
+@pytest.mark.parametrize("variant", [P.Variant.Fp16, P.Variant.Dpx16, P.Variant.Swar8],
+                         ids=lambda v: v.name)
+@pytest.mark.parametrize("alg", [P.Algorithm.Msv, P.Algorithm.Ssv], ids=lambda a: a.name)
+def test_paper_wrap_mode(ora, variant, alg):
+    """The non-normative wrap study mode runs, matches its model, and differs
+    from the normative (oracle-exact) -inf injection on a consensus-heavy
+    instance (test_engine.cpp:265-278)."""
+    cpw = 4 if variant == P.Variant.Swar8 else 2
+    q = P.QuantParams(3.0, 120, 3, 20, 20)
+    for L, H in ((1, 8), (2, 8), (8, 4), (32, 4)):
+        m = cpw * L * H
+        rng = P.Rng(38 + L)
+        hmm = rng.random_profile(m)
+        hmm.match_scores[:] = np.where(np.arange(20)[None, :] == 0, 3.0, -3.0)
+        db = rng.random_records(48, 30, 90, plant=(hmm, 0.5))
+        costs = P.quantize_emissions(hmm, q)
+        normative = scan(costs, q, db, hmm, alg=alg, variant=variant, lanes=L, rows=H)
+        wrapped = scan(costs, q, db, hmm, alg=alg, variant=variant, lanes=L, rows=H,
+                       paper_wrap=True)
+        want = ora.scan_flat(int(alg), costs.bytes, db.residues, db.offsets, oq(q))
+        np.testing.assert_array_equal(normative.raw, want)
+        lens = db.lengths()
+        model = [wrap_model(alg, costs.bytes, m, db.sequence(k),
+                            q, P.engine_sequence_base(int(lens[k]), q)) for k in range(db.count)]
+        np.testing.assert_array_equal(wrapped.raw, np.array(model, np.uint8), err_msg=f"L={L}")
+        assert (wrapped.raw != normative.raw).any()
