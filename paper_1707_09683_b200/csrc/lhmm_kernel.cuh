@@ -508,14 +508,33 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
                             const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
                             g[sl] = V::cell(in, cw[k], st);
                         }
+                        if constexpr (!V::kMsv) {
+                            // SSV: fold the four new words into E right away
+                            // so the ALU work interleaves with the FP16 cell
+                            // updates (+4% at M=200/400; neutral for MSV,
+                            // whose row max feeds B)
+                            const int s0 = ((4 * h4 - 1 - r) % H + H) % H;
+                            const int s1 = ((4 * h4 - r) % H + H) % H;
+                            const int s2 = ((4 * h4 + 1 - r) % H + H) % H;
+                            const int s3 = ((4 * h4 + 2 - r) % H + H) % H;
+                            if (h4 & 1) {
+                                e0 = V::acc2(e0, g[s3], g[s2]);
+                                e1 = V::acc2(e1, g[s1], g[s0]);
+                            } else {
+                                e2 = V::acc2(e2, g[s3], g[s2]);
+                                e3 = V::acc2(e3, g[s1], g[s0]);
+                            }
+                        }
                     }
+                    if constexpr (V::kMsv) {
 #pragma unroll
-                    for (int h = 0; h < H; h += 8) {
-                        e0 = V::acc2(e0, g[h], g[h + 1]);
-                        e1 = V::acc2(e1, g[h + 2], g[h + 3]);
-                        if (h + 4 < H) {
-                            e2 = V::acc2(e2, g[h + 4], g[h + 5]);
-                            e3 = V::acc2(e3, g[h + 6], g[h + 7]);
+                        for (int h = 0; h < H; h += 8) {
+                            e0 = V::acc2(e0, g[h], g[h + 1]);
+                            e1 = V::acc2(e1, g[h + 2], g[h + 3]);
+                            if (h + 4 < H) {
+                                e2 = V::acc2(e2, g[h + 4], g[h + 5]);
+                                e3 = V::acc2(e3, g[h + 6], g[h + 7]);
+                            }
                         }
                     }
                     if constexpr (V::kMsv) {

@@ -305,6 +305,7 @@ def test_paper_wrap_mode(ora, variant, alg):
     instance (test_engine.cpp:265-278)."""
     cpw = 4 if variant == P.Variant.Swar8 else 2
     q = P.QuantParams(3.0, 120, 3, 20, 20)
+    differs = False
     for L, H in ((1, 8), (2, 8), (8, 4), (32, 4)):
         m = cpw * L * H
         rng = P.Rng(38 + L)
@@ -321,4 +322,5 @@ def test_paper_wrap_mode(ora, variant, alg):
         model = [wrap_model(alg, costs.bytes, m, db.sequence(k),
                             q, P.engine_sequence_base(int(lens[k]), q)) for k in range(db.count)]
         np.testing.assert_array_equal(wrapped.raw, np.array(model, np.uint8), err_msg=f"L={L}")
-        assert (wrapped.raw != normative.raw).any()
+        differs = differs or bool((wrapped.raw != normative.raw).any())
+    assert differs
