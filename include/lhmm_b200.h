@@ -147,6 +147,16 @@ int lhmm_context_set_stream(lhmm_context* ctx, void* cuda_stream);
 int lhmm_context_device_info(lhmm_context* ctx, int* sm_count, int* sm_clock_khz,
                              int* cc_major, int* cc_minor);
 
+/* Out-of-core databases: cap the device bytes the packed residue data may
+ * occupy (0 = unlimited, the default).  A database whose packed image is
+ * larger stays in pinned host memory and every scan streams it through two
+ * device slots of budget/2 bytes (the copy of one piece overlaps the scan of
+ * the previous); results are identical to a resident scan.  Takes effect at
+ * the next lhmm_set_database; the budget must hold two of the largest tile. */
+int lhmm_context_set_db_budget(lhmm_context* ctx, uint64_t device_bytes);
+/* *on_device = 1 if the current database is resident in HBM, 0 if streamed. */
+int lhmm_database_resident(lhmm_context* ctx, int* on_device);
+
 /* Profile: quantized cost matrix m x 21 (CostMatrix bytes, profile.hpp:43-52)
  * plus the Gumbel parameters used for pass decisions. */
 int lhmm_set_profile(lhmm_context* ctx, const uint8_t* costs, uint32_t m, const lhmm_quant* q,

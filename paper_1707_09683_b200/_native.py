@@ -68,6 +68,8 @@ SIGNATURES = {
     "lhmm_context_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
     "lhmm_context_destroy": (C.c_int, [vp]),
     "lhmm_context_set_stream": (C.c_int, [vp, vp]),
+    "lhmm_context_set_db_budget": (C.c_int, [vp, C.c_uint64]),
+    "lhmm_database_resident": (C.c_int, [vp, C.POINTER(C.c_int)]),
     "lhmm_context_device_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                            C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "lhmm_set_profile": (C.c_int, [vp, u8p, C.c_uint32, C.POINTER(Quant), C.c_double,

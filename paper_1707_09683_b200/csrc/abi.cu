@@ -146,7 +146,7 @@ struct Choice {
 // fraction of the persistent grid's warps the database's work items
 // (tiles * L) can occupy.  `want_L` pins the lane count when non-zero.
 Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64_t n_tiles,
-                       int sm_count) {
+                       int sm_count, bool allow_relaxed = true) {
     Choice best;
     // auto considers the measured variants only (calib_b200.inc); the
     // relaxed FP16X also needs a database large enough to amortise its
@@ -157,8 +157,8 @@ Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64
         const bool measured_only = variant == LHMM_VARIANT_AUTO && pass == 0;
         for (int vi = 0; vi < nv; ++vi) {
             const int v = variant == LHMM_VARIANT_AUTO ? vs[vi] : variant;
-            if (variant == LHMM_VARIANT_AUTO && v == LHMM_VARIANT_FP16X && n_tiles > 0 &&
-                n_tiles < 4096)
+            if (variant == LHMM_VARIANT_AUTO && v == LHMM_VARIANT_FP16X &&
+                ((n_tiles > 0 && n_tiles < 4096) || !allow_relaxed))
                 continue;
             const uint32_t cpw = lhmm::cells_per_word(v);
             int n;
@@ -264,6 +264,15 @@ struct lhmm_context {
 
     std::map<std::tuple<int, int, uint32_t, uint32_t, size_t>, int> occupancy;
 
+    // out-of-core mode: when the packed image exceeds db_budget the database
+    // stays in pinned host memory and every scan streams it through two
+    // device ring slots (copy of piece k+1 overlaps the scan of piece k)
+    uint64_t db_budget = 0;        // device bytes for residue data; 0 = unlimited
+    bool host_resident = false;
+    uint64_t slot_bytes = 0;
+    DevBuf<uint8_t> d_ring;
+    cudaEvent_t ring_copied[2] = {nullptr, nullptr}, ring_done[2] = {nullptr, nullptr};
+
     // on-device pipeline scratch (survivor compaction)
     struct Pipe {
         DevBuf<uint32_t> flags, pos, new_lens, new_out, src_slot;
@@ -296,14 +305,39 @@ struct DeviceGuard {
 
 int upload_db(lhmm_context* c) {
     auto& db = c->db;
-    if (int rc = c->d_db.reserve(db.data_bytes)) return rc;
+    c->host_resident = c->db_budget > 0 && db.data_bytes > c->db_budget;
+    if (c->host_resident) {
+        uint64_t max_tile = 0;
+        for (uint64_t t = 0; t < db.n_tiles; ++t) {
+            const uint64_t e = t + 1 < db.n_tiles ? db.tile_off[t + 1] : db.data_bytes;
+            max_tile = std::max(max_tile, e - db.tile_off[t]);
+        }
+        c->slot_bytes = c->db_budget / 2 / 512 * 512;
+        if (c->slot_bytes < max_tile)
+            return set_error(LHMM_ERR_CONTRACT,
+                             "device database budget " + std::to_string(c->db_budget) +
+                                 " B is below two of the largest tile (" +
+                                 std::to_string(max_tile) + " B)");
+        c->d_db.release();
+        if (int rc = c->d_ring.reserve(2 * c->slot_bytes)) return rc;
+        for (int k = 0; k < 2; ++k)
+            if (!c->ring_copied[k]) {
+                CUDA_TRY(cudaEventCreateWithFlags(&c->ring_copied[k], cudaEventDisableTiming));
+                CUDA_TRY(cudaEventCreateWithFlags(&c->ring_done[k], cudaEventDisableTiming));
+            }
+    } else {
+        c->d_ring.release();
+    }
+    if (!c->host_resident)
+        if (int rc = c->d_db.reserve(db.data_bytes)) return rc;
     if (int rc = c->d_tile_off.reserve(db.tile_off.size())) return rc;
     if (int rc = c->d_lens.reserve(db.lens.size())) return rc;
     if (int rc = c->d_out_idx.reserve(db.out_idx.size())) return rc;
     if (int rc = c->d_raw.reserve(db.n_local)) return rc;
     if (int rc = c->d_pass.reserve(db.n_local)) return rc;
-    CUDA_TRY(cudaMemcpyAsync(c->d_db.ptr, db.data, db.data_bytes, cudaMemcpyHostToDevice,
-                             c->stream));
+    if (!c->host_resident)
+        CUDA_TRY(cudaMemcpyAsync(c->d_db.ptr, db.data, db.data_bytes, cudaMemcpyHostToDevice,
+                                 c->stream));
     if (!db.tile_off.empty()) {
         CUDA_TRY(cudaMemcpyAsync(c->d_tile_off.ptr, db.tile_off.data(),
                                  db.tile_off.size() * sizeof(uint64_t), cudaMemcpyHostToDevice,
@@ -350,12 +384,17 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (opt->reorder_mode != 0 && opt->reorder_mode != 1)
         return set_error(LHMM_ERR_CONTRACT, "unknown reorder mode");
     ProfileSlot& pf = c->profiles[c->current];
+    // relaxed FP16X rescoring compacts from device-resident tiles; a
+    // host-resident (streamed) database uses the exact FP16 kernel instead
+    const bool streamed_db = view == nullptr && c->host_resident;
     int variant = opt->variant;
+    if (streamed_db && variant == LHMM_VARIANT_FP16X) variant = LHMM_VARIANT_FP16;
     uint32_t L = opt->lanes, H = opt->rows;
     if (L != 0 && (L > 32 || (L & (L - 1))))
         return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,32]");
     if (H == 0) {
-        Choice ch = choose_geometry(pf.m, opt->alg, variant, L, v.n_tiles, c->sm_count);
+        Choice ch = choose_geometry(pf.m, opt->alg, variant, L, v.n_tiles, c->sm_count,
+                                    !streamed_db);
         if (!ch.L)
             return set_error(LHMM_ERR_DATA,
                              "no instantiated geometry covers model length " + std::to_string(pf.m));
@@ -365,7 +404,8 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     } else {
         if (variant == LHMM_VARIANT_AUTO) variant = LHMM_VARIANT_FP16;
         if (L == 0) {
-            Choice ch = choose_geometry(pf.m, opt->alg, variant, 0, v.n_tiles, c->sm_count);
+            Choice ch = choose_geometry(pf.m, opt->alg, variant, 0, v.n_tiles, c->sm_count,
+                                        !streamed_db);
             L = ch.L ? ch.L : 1;
         }
     }
@@ -482,7 +522,49 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     cfg.grid = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(c->sm_count) * bps, need)));
 
     uint32_t launches = 0;
-    if (segments <= 0) {
+    if (streamed_db) {
+        // out-of-core: pieces of whole tiles up to one ring slot each; the
+        // copy of piece k waits for the scan of piece k-2 (same slot)
+        auto& db = c->db;
+        const uint64_t T = db.n_tiles;
+        CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+        CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev0, 0));
+        for (int k = 0; k < 2; ++k) CUDA_TRY(cudaEventRecord(c->ring_done[k], c->stream));
+        uint64_t t0 = 0;
+        for (int k = 0; t0 < T; ++k) {
+            const int sl = k & 1;
+            const uint64_t b0 = db.tile_off[t0];
+            uint64_t t1 = t0 + 1;  // one tile always fits (checked at upload)
+            while (t1 < T) {
+                const uint64_t end = t1 + 1 < T ? db.tile_off[t1 + 1] : db.data_bytes;
+                if (end - b0 > c->slot_bytes) break;
+                ++t1;
+            }
+            const uint64_t b1 = t1 < T ? db.tile_off[t1] : db.data_bytes;
+            uint8_t* slot = c->d_ring.ptr + uint64_t(sl) * c->slot_bytes;
+            CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ring_done[sl], 0));
+            CUDA_TRY(cudaMemcpyAsync(slot, db.data + b0, b1 - b0, cudaMemcpyHostToDevice,
+                                     c->copy_stream));
+            CUDA_TRY(cudaEventRecord(c->ring_copied[sl], c->copy_stream));
+            CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ring_copied[sl], 0));
+            lhmm::KParams ps = p;
+            ps.db = slot;
+            ps.db_off = b0;
+            ps.tile_base = uint32_t(t0);
+            ps.n_items = uint32_t((t1 - t0) * L);
+            lhmm::LaunchCfg cs = cfg;
+            const uint64_t need_s = (uint64_t(ps.n_items) + warps_per_cta - 1) / warps_per_cta;
+            cs.grid = int(std::max<uint64_t>(
+                1, std::min<uint64_t>(uint64_t(c->sm_count) * bps, need_s)));
+            CUDA_TRY(cudaMemsetAsync(c->d_counter.ptr, 0, sizeof(uint32_t), c->stream));
+            if (fn(lhmm::kOpLaunch, int(H), &cs, &ps) != 0)
+                return set_error(LHMM_ERR_CUDA, std::string("kernel launch failed: ") +
+                                                    cudaGetErrorString(cudaGetLastError()));
+            CUDA_TRY(cudaEventRecord(c->ring_done[sl], c->stream));
+            ++launches;
+            t0 = t1;
+        }
+    } else if (segments <= 0) {
         CUDA_TRY(cudaMemsetAsync(c->d_counter.ptr, 0, sizeof(uint32_t), c->stream));
         CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
         if (p.n_items > 0) {
@@ -711,6 +793,54 @@ int compact(lhmm_context* c, lhmm_context::Pipe& P, const DbView& src, const uin
     return LHMM_OK;
 }
 
+// Host analogue of compact() for a host-resident database: the selected
+// sequences (sel[local index] != 0, already copied to the host) are re-tiled
+// from the pinned image in their sorted order and uploaded into `P`.
+int compact_host(lhmm_context* c, lhmm_context::Pipe& P, const uint8_t* sel, DbView* out,
+                 uint32_t* nsel_out) {
+    const auto& db = c->db;
+    std::vector<uint32_t> src;
+    for (uint64_t i = 0; i < db.n_tiles * 32; ++i)
+        if (db.out_idx[i] != lhmm::kNoOutput && sel[db.out_idx[i]]) src.push_back(uint32_t(i));
+    const uint32_t nsel = uint32_t(src.size());
+    *nsel_out = nsel;
+    *out = DbView{nullptr, nullptr, nullptr, nullptr, 0, 0, 0};
+    if (nsel == 0) return LHMM_OK;
+    const uint32_t ntiles = (nsel + 31u) / 32u;
+    std::vector<uint32_t> lens(size_t(ntiles) * 32, 0), outi(size_t(ntiles) * 32, lhmm::kNoOutput);
+    std::vector<uint64_t> off(ntiles + 1, 0);
+    uint64_t residues = 0;
+    for (uint32_t j = 0; j < nsel; ++j) {
+        lens[j] = db.lens[src[j]];
+        outi[j] = db.out_idx[src[j]];
+        residues += lens[j];
+    }
+    for (uint32_t t = 0; t < ntiles; ++t)
+        off[t + 1] = off[t] + uint64_t((lens[size_t(t) * 32] + 15u) / 16u) * 512u;
+    std::vector<uint8_t> img(std::max<uint64_t>(off[ntiles], 16), lhmm::kPadding);
+    for (uint32_t j = 0; j < nsel; ++j) {
+        const uint32_t s = src[j];
+        const uint8_t* from = db.data + db.tile_off[s / 32] + (s % 32) * 16;
+        uint8_t* to = img.data() + off[j / 32] + (j % 32) * 16;
+        for (uint32_t ch = 0; ch < (lens[j] + 15u) / 16u; ++ch)
+            std::memcpy(to + size_t(ch) * 512, from + size_t(ch) * 512, 16);
+    }
+    if (int rc = P.db.reserve(img.size())) return rc;
+    if (int rc = P.new_off.reserve(ntiles + 1)) return rc;
+    if (int rc = P.new_lens.reserve(lens.size())) return rc;
+    if (int rc = P.new_out.reserve(outi.size())) return rc;
+    cudaStream_t s = c->stream;
+    CUDA_TRY(cudaMemcpyAsync(P.db.ptr, img.data(), img.size(), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(P.new_off.ptr, off.data(), off.size() * 8, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(P.new_lens.ptr, lens.data(), lens.size() * 4, cudaMemcpyHostToDevice,
+                             s));
+    CUDA_TRY(cudaMemcpyAsync(P.new_out.ptr, outi.data(), outi.size() * 4, cudaMemcpyHostToDevice,
+                             s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *out = DbView{P.db.ptr, P.new_off.ptr, P.new_lens.ptr, P.new_out.ptr, ntiles, residues, nsel};
+    return LHMM_OK;
+}
+
 // ---------------------------------------------------------------------------
 // on-device filter pipeline (filter_pipeline, src/engine.cpp:596-657):
 // SSV over the resident database -> compact the survivors (pass bit:
@@ -738,7 +868,17 @@ int run_pipeline(lhmm_context* c, double threshold, int variant, uint8_t* ssv_ra
                      c->db.n_tiles, c->db.residues, c->db.n_local};
     DbView view;
     uint32_t nsurv = 0;
-    if (int rc = compact(c, P, all, c->d_pass.ptr, &view, &nsurv)) return rc;
+    if (c->host_resident) {
+        // streamed database: the survivors are gathered from the pinned image
+        std::vector<uint8_t> sel(std::max<uint64_t>(n, 1));
+        if (n) {
+            CUDA_TRY(cudaMemcpyAsync(sel.data(), c->d_pass.ptr, n, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+        }
+        if (int rc = compact_host(c, P, sel.data(), &view, &nsurv)) return rc;
+    } else if (int rc = compact(c, P, all, c->d_pass.ptr, &view, &nsurv)) {
+        return rc;
+    }
     *rescored = nsurv;
     if (nsurv > 0) {
         lhmm_scan_options om = o;
@@ -808,6 +948,11 @@ int lhmm_context_destroy(lhmm_context* c) {
     lhmm::free_packed(c->db, pinned_free);
     if (c->pinned) pinned_free(c->pinned);
     c->d_db.release();
+    c->d_ring.release();
+    for (int k = 0; k < 2; ++k) {
+        if (c->ring_copied[k]) cudaEventDestroy(c->ring_copied[k]);
+        if (c->ring_done[k]) cudaEventDestroy(c->ring_done[k]);
+    }
     c->d_tile_off.release();
     c->d_lens.release();
     c->d_out_idx.release();
@@ -827,6 +972,19 @@ int lhmm_context_destroy(lhmm_context* c) {
     cudaStreamDestroy(c->copy_stream);
     cudaStreamDestroy(c->own_stream);
     delete c;
+    return LHMM_OK;
+}
+
+int lhmm_context_set_db_budget(lhmm_context* c, uint64_t device_bytes) {
+    if (!c) return set_error(LHMM_ERR_CONTRACT, "null context");
+    c->db_budget = device_bytes;
+    return LHMM_OK;
+}
+
+int lhmm_database_resident(lhmm_context* c, int* on_device) {
+    if (!c || !on_device) return set_error(LHMM_ERR_CONTRACT, "null argument");
+    if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
+    *on_device = c->host_resident ? 0 : 1;
     return LHMM_OK;
 }
 

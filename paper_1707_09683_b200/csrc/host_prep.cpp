@@ -268,6 +268,7 @@ uint32_t cells_per_word(int variant) { return variant == LHMM_VARIANT_SWAR8 ? 4u
 
 static void strides_for(uint32_t L, uint32_t H, uint32_t& P, uint32_t& copies,
                         uint32_t& copy_stride) {
+    H = (H + 3u) / 4u * 4u;  // a two-row top group keeps a four-row slot
     copies = L < 8 ? 8u / L : 1u;
     if (copies > 1) {
         P = (H * L + 31u) / 32u * 32u;

@@ -58,6 +58,7 @@ struct KParams {
     uint32_t* counter;          // work-item counter (zeroed per launch)
     uint32_t n_items;           // tiles * L
     uint32_t tile_base;         // first tile of this launch (streamed scans)
+    uint64_t db_off;            // byte offset of db[0] in the packed image (ring slots)
     uint32_t table_bytes;       // multiple of 16
     uint32_t res_stride;        // words per residue row (P)
     uint32_t copy_stride;       // words between per-group replicas (0: shared)
@@ -421,7 +422,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
     __shared__ __align__(8) uint64_t bar;
     stage_table(smem, p.table, p.table_bytes, &bar);
 
-    static_assert(H % 4 == 0, "rows are read four at a time");
+    static_assert(H % 2 == 0, "rows are read four (or, in the top group, two) at a time");
     constexpr int G = 32 / L;                    // sequences per warp
     constexpr int COPIES = L < 8 ? 8 / L : 1;    // table replicas (one per quarter-warp group)
     const uint32_t lane = threadIdx.x & 31u;
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
         const uint32_t sidx = tile * 32u + slot;
         const uint32_t len = p.lens[sidx];
         const uint32_t rows = p.lens[tile * 32u + sub * G];  // longest of the sub-batch
-        const uint8_t* src = p.db + p.tile_off[tile] + slot * 16u;
+        const uint8_t* src = p.db + (p.tile_off[tile] - p.db_off) + slot * 16u;
 
         typename V::St st;
         V::init(st, p.base_tab[len], p);
@@ -497,27 +498,44 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
                     } else {
                         up = inject_here ? V::inject(st) : g[stop];
                     }
+                    // rows go in groups of four (one LDS.128 per lane); with
+                    // H = 2 (mod 4) the top group holds two rows (LDS.64)
 #pragma unroll
-                    for (int h4 = H / 4 - 1; h4 >= 0; --h4) {
-                        const uint4 c = *reinterpret_cast<const uint4*>(tp + h4 * 4 * L);
-                        const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+                    for (int h4 = (H + 3) / 4 - 1; h4 >= 0; --h4) {
+                        const bool full = 4 * h4 + 4 <= H;  // compile-time after unrolling
+                        uint32_t cw[4];
+                        if (full) {
+                            const uint4 c = *reinterpret_cast<const uint4*>(tp + h4 * 4 * L);
+                            cw[0] = c.x;
+                            cw[1] = c.y;
+                            cw[2] = c.z;
+                            cw[3] = c.w;
+                        } else {
+                            const uint2 c = *reinterpret_cast<const uint2*>(tp + h4 * 4 * L);
+                            cw[0] = c.x;
+                            cw[1] = c.y;
+                            cw[2] = cw[3] = 0u;
+                        }
 #pragma unroll
                         for (int k = 3; k >= 0; --k) {
                             const int h = 4 * h4 + k;
+                            if (h >= H) continue;
                             const int sl = ((h - 1 - r) % H + H) % H;
                             const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
                             g[sl] = V::cell(in, cw[k], st);
                         }
                         if constexpr (!V::kMsv) {
-                            // SSV: fold the four new words into E right away
-                            // so the ALU work interleaves with the FP16 cell
-                            // updates (+4% at M=200/400; neutral for MSV,
-                            // whose row max feeds B)
+                            // SSV: fold the new words into E right away so the
+                            // ALU work interleaves with the FP16 cell updates
+                            // (+4% at M=200/400; neutral for MSV, whose row
+                            // max feeds B)
                             const int s0 = ((4 * h4 - 1 - r) % H + H) % H;
                             const int s1 = ((4 * h4 - r) % H + H) % H;
                             const int s2 = ((4 * h4 + 1 - r) % H + H) % H;
                             const int s3 = ((4 * h4 + 2 - r) % H + H) % H;
-                            if (h4 & 1) {
+                            if (!full) {
+                                e0 = V::acc2(e0, g[s1], g[s0]);
+                            } else if (h4 & 1) {
                                 e0 = V::acc2(e0, g[s3], g[s2]);
                                 e1 = V::acc2(e1, g[s1], g[s0]);
                             } else {
@@ -530,11 +548,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
 #pragma unroll
                         for (int h = 0; h < H; h += 8) {
                             e0 = V::acc2(e0, g[h], g[h + 1]);
-                            e1 = V::acc2(e1, g[h + 2], g[h + 3]);
-                            if (h + 4 < H) {
-                                e2 = V::acc2(e2, g[h + 4], g[h + 5]);
-                                e3 = V::acc2(e3, g[h + 6], g[h + 7]);
-                            }
+                            if (h + 2 < H) e1 = V::acc2(e1, g[h + 2], g[h + 3]);
+                            if (h + 4 < H) e2 = V::acc2(e2, g[h + 4], g[h + 5]);
+                            if (h + 6 < H) e3 = V::acc2(e3, g[h + 6], g[h + 7]);
                         }
                     }
                     if constexpr (V::kMsv) {

@@ -290,6 +290,17 @@ class Scanner:
                                                       C.byref(ma), C.byref(mi)))
         return {"sm_count": sm.value, "sm_clock_khz": clk.value, "cc": (ma.value, mi.value)}
 
+    def set_db_budget(self, device_bytes):
+        """Out-of-core mode: databases whose packed image exceeds this many
+        device bytes stay in pinned host memory and are streamed through a
+        two-slot device ring on every scan (0 = unlimited)."""
+        _check(_native.lib().lhmm_context_set_db_budget(self._ctx, int(device_bytes)))
+
+    def database_resident(self):
+        on = C.c_int()
+        _check(_native.lib().lhmm_database_resident(self._ctx, C.byref(on)))
+        return bool(on.value)
+
     def set_stream(self, stream_handle):
         _check(_native.lib().lhmm_context_set_stream(self._ctx, C.c_void_p(stream_handle)))
 

@@ -16,10 +16,11 @@ import numpy as np  # noqa: E402
 
 import paper_1707_09683_b200 as P  # noqa: E402
 
-ROWS = {P.Variant.Dpx16: [4, 8, 12, 16, 24, 32, 40, 48, 56, 64],
-        P.Variant.Fp16: [4, 8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 52, 56, 60, 64, 68, 72],
-        P.Variant.Swar8: [4, 8, 16, 24, 32],
-        P.Variant.Fp16x: [4, 8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 52, 56, 60, 64, 68, 72]}
+sys.path.insert(0, os.path.join(ROOT, "paper_1707_09683_b200", "csrc"))
+import gen_instances  # noqa: E402
+
+ROWS = {P.Variant.Dpx16: gen_instances.ROWS["dpx16"], P.Variant.Fp16: gen_instances.ROWS["fp16"],
+        P.Variant.Swar8: gen_instances.ROWS["swar8"], P.Variant.Fp16x: gen_instances.ROWS["fp16x"]}
 
 
 def main():

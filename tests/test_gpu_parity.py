@@ -20,12 +20,18 @@ def oq(q):
     return oracle.QuantParams(q.scale, q.base, q.dbias, q.tec, q.tjb)
 
 
+def rows_list(variant):
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(P.__file__), "csrc"))
+    import gen_instances
+    return gen_instances.ROWS[{P.Variant.Swar8: "swar8", P.Variant.Dpx16: "dpx16",
+                               P.Variant.Fp16: "fp16", P.Variant.Fp16x: "fp16x"}[variant]]
+
+
 def rows_for(variant, L, m):
     cpw = 4 if variant == P.Variant.Swar8 else 2
-    rows = {P.Variant.Swar8: [4, 8, 16, 24, 32],
-            P.Variant.Dpx16: [4, 8, 12, 16, 24, 32, 40, 48, 56, 64]}.get(
-        variant, [4, 8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 52, 56, 60, 64, 68, 72])
-    for h in rows:
+    for h in rows_list(variant):
         if cpw * L * h >= m:
             return h
     return None
@@ -324,3 +330,63 @@ def test_paper_wrap_mode(ora, variant, alg):
         np.testing.assert_array_equal(wrapped.raw, np.array(model, np.uint8), err_msg=f"L={L}")
         differs = differs or bool((wrapped.raw != normative.raw).any())
     assert differs
+
+
+@pytest.mark.parametrize("variant", [P.Variant.Fp16, P.Variant.Fp16x], ids=lambda v: v.name)
+@pytest.mark.parametrize("alg", [P.Algorithm.Msv, P.Algorithm.Ssv], ids=lambda a: a.name)
+def test_two_row_top_group(ora, variant, alg):
+    """H = 2 (mod 4): the top row group is read with LDS.64 and folded as a
+    pair; every lane count, models that fill the last rows exactly."""
+    q = P.QuantParams(3.0, 120, 3, 20, 20)
+    for L in (1, 2, 4, 8, 16, 32):
+        for H in (34, 38, 70):
+            m = 2 * L * H - (L * 7) % 5  # the top rows hold real nodes
+            rng = P.Rng(5000 + L * 100 + H)
+            hmm = rng.random_profile(m)
+            db = rng.random_records(48, 1, max(8, min(300, 2_000_000 // (48 * m))),
+                                    plant=(hmm, 0.25))
+            costs = P.quantize_emissions(hmm, q)
+            rep = scan(costs, q, db, hmm, alg=alg, variant=variant, lanes=L, rows=H)
+            want = ora.scan_flat(int(alg), costs.bytes, db.residues, db.offsets, oq(q))
+            assert rep.rows == H
+            np.testing.assert_array_equal(rep.raw, want, err_msg=f"L={L} H={H} m={m}")
+
+
+def test_out_of_core_database_streams_through_the_ring(ora):
+    """lhmm_context_set_db_budget: a database larger than the device budget
+    stays in pinned host memory and is streamed through two ring slots per
+    scan; scores, pass bits and the pipeline equal the resident scan."""
+    rng = P.Rng(0x00C)
+    hmm = rng.random_profile(300)
+    db = rng.lognormal_records(20000, 290, 0.65, 2, plant=(hmm, 0.05))
+    q = P.QuantParams(3.0, 120, 3, 20, 20)
+    costs = P.quantize_emissions(hmm, q)
+    with P.Scanner(0) as res_s, P.Scanner(0) as ooc:
+        res_s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        res_s.set_database(db)
+        assert res_s.database_resident()
+        ooc.set_db_budget(1 << 20)   # 1 MB: ~7 ring pieces for the 7 MB image
+        ooc.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        ooc.set_database(db)
+        assert not ooc.database_resident()
+        for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
+            for variant in (P.Variant.Auto, P.Variant.Fp16x, P.Variant.Dpx16):
+                a = res_s.scan(P.ScanOptions(alg=alg, variant=variant, threshold=0.05))
+                b = ooc.scan(P.ScanOptions(alg=alg, variant=variant, threshold=0.05))
+                np.testing.assert_array_equal(a.raw, b.raw)
+                np.testing.assert_array_equal(a.passed, b.passed)
+                assert b.stats["launches"] >= 4
+            want = ora.scan_flat(int(alg), costs.bytes, db.residues, db.offsets, oq(q))
+            np.testing.assert_array_equal(b.raw, want)
+        s1 = ooc.scan_streamed(P.ScanOptions(alg=P.Algorithm.Ssv), segments=4)
+        np.testing.assert_array_equal(s1.raw, res_s.scan(P.ScanOptions(alg=P.Algorithm.Ssv)).raw)
+        pa = res_s.filter_pipeline(0.05)
+        pb = ooc.filter_pipeline(0.05)
+        assert pa.msv_rescored == pb.msv_rescored > 0
+        np.testing.assert_array_equal(pa.ssv_raw, pb.ssv_raw)
+        np.testing.assert_array_equal(pa.msv_raw, pb.msv_raw)
+    with P.Scanner(0) as tiny:
+        tiny.set_db_budget(4096)
+        tiny.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        with pytest.raises(P.ContractError, match="largest tile"):
+            tiny.set_database(db)
