@@ -359,14 +359,18 @@ def main():
     # ---- end to end through the C ABI with host buffers --------------------
     e2e = None
     if not args.no_e2e:
+        # the database upload is overlapped with the longest scan (largest M),
+        # which hides the copy best; the other scans run on the resident copy
+        e2e_order = sorted(scans, key=lambda sc: -sc[1])
+
         def e2e_step():
-            # H2D of the packed (pinned) database overlapped with the first
-            # scan (lhmm_scan_streamed), the other models on the resident
-            # copy; every scan ends with the D2H of its raw + pass bytes
+            # H2D of the packed (pinned) database streamed under the largest
+            # model's scan (lhmm_scan_streamed), the other models on the
+            # resident copy; every scan ends with the D2H of its raw + pass bytes
             d2h = 0
-            for k, (pid, m, a) in enumerate(scans):
+            for k, (pid, m, a) in enumerate(e2e_order):
                 s.select_profile(pid)
-                rep = s.scan_streamed(opt_for(a), 8) if k == 0 else s.scan(opt_for(a))
+                rep = s.scan_streamed(opt_for(a), 16) if k == 0 else s.scan(opt_for(a))
                 d2h += 2 * int(rep.raw.size)
             return d2h
         for _ in range(max(1, args.warmup)):
@@ -387,9 +391,9 @@ def main():
         h2d = dbstats["packed_bytes"] + 16 * dbstats["tiles"] * 32
         e2e = {"value": round(total_cells / (float(ems.item()) * 1e-3) / 1e9, 3), "unit": "GCUPS",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "path": "C ABI: lhmm_scan_streamed (H2D of the packed pinned database in 8 "
-                        "pieces overlapped with the first scan) + lhmm_scan per further model, "
-                        "host outputs"}
+               "path": "C ABI: lhmm_scan_streamed (H2D of the packed pinned database in up "
+                        "to 16 pieces overlapped with the largest model's scan) + lhmm_scan per "
+                        "further model, host outputs"}
 
     if rank != 0:
         if dist:

@@ -332,6 +332,17 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
                     c[k] = (node > m || x > kUnknown) ? 0xff : costs[(node - 1) * 21 + x];
                 }
                 const uint32_t w = encode_word(variant, alg, c, cpw, dbias);
+                if (H % 4 == 2 && h / 4 == H / 4) {
+                    // two-row top group, read with LDS.64: lanes' word pairs
+                    // packed densely (2*oig); with L < 16 the two
+                    // quarter-warps of a 16-lane wavefront read separate
+                    // halves of the group's 4L-word slot -- conflict-free
+                    const size_t top = size_t(x) * P + size_t(H / 4) * 4 * L + 2 * oig + (h % 4);
+                    for (uint32_t g = 0; g < copies; ++g)
+                        for (uint32_t qw = 0; qw < (L < 16 ? 2u : 1u); ++qw)
+                            out.words[size_t(g) * cs + top + qw * 2 * L] = w;
+                    continue;
+                }
                 const size_t at = size_t(x) * P + size_t(h / 4) * 4 * L + 4 * oig + (h % 4);
                 for (uint32_t g = 0; g < copies; ++g) out.words[size_t(g) * cs + at] = w;
             }

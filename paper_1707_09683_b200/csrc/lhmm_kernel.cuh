@@ -35,6 +35,7 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+
 namespace lhmm {
 
 constexpr uint32_t kFull = 0xffffffffu;
@@ -157,6 +158,7 @@ struct Dpx16 {
     static constexpr bool kMsv = ALG == 0;
     static constexpr uint32_t NEG = kMsv ? 0u : 0x00800080u;
     static constexpr bool kRelaxed = false;
+    static constexpr bool kTwoMode = false;
     struct St {
         uint32_t B, base2, d2, ntj2;
     };
@@ -167,6 +169,7 @@ struct Dpx16 {
         s.ntj2 = (0u - p.tecjb) & 0xffffu;
         s.ntj2 |= s.ntj2 << 16;
     }
+    template <bool LAZY = false>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
         if constexpr (kMsv) {
             uint32_t y = __viaddmin_u16x2(__vmaxu2(x, s.B), s.d2, 0x00ff00ffu);
@@ -196,6 +199,7 @@ struct Dpx16 {
         s.B = __viaddmax_s16x2(e, s.ntj2, s.base2);
     }
     __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
+    template <bool LAZY = false>
     __device__ static __forceinline__ uint32_t inject(const St&) { return NEG; }
     __device__ static __forceinline__ bool needs_exact(uint32_t, const St&) { return false; }
     __device__ static __forceinline__ uint32_t raw(uint32_t e) { return e & 0xffu; }
@@ -214,6 +218,7 @@ struct Fp16 {
     static constexpr bool kMsv = ALG == 0;
     static constexpr uint32_t NEG = 0u;  // +0.0 in both halves
     static constexpr bool kRelaxed = false;
+    static constexpr bool kTwoMode = false;
     struct St {
         uint32_t B, base2, d1, tj2;
     };
@@ -232,6 +237,7 @@ struct Fp16 {
         }
         s.B = s.base2;
     }
+    template <bool LAZY = false>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
         if constexpr (kMsv) {
             const uint32_t m = __vmaxu2(x, s.B);
@@ -263,6 +269,7 @@ struct Fp16 {
         s.B = as_u32(__hmax2(__hsub2(as_h2(e), as_h2(s.tj2)), as_h2(s.base2)));
     }
     __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
+    template <bool LAZY = false>
     __device__ static __forceinline__ uint32_t inject(const St&) { return NEG; }
     __device__ static __forceinline__ bool needs_exact(uint32_t, const St&) { return false; }
     __device__ static __forceinline__ uint32_t raw(uint32_t e) {
@@ -277,6 +284,7 @@ struct Swar8 {
     static constexpr bool kMsv = ALG == 0;
     static constexpr uint32_t NEG = kMsv ? 0u : 0x80808080u;
     static constexpr bool kRelaxed = false;
+    static constexpr bool kTwoMode = false;
     struct St {
         uint32_t B, base4, d4, tj4;
     };
@@ -286,6 +294,7 @@ struct Swar8 {
         s.d4 = p.dbias * 0x01010101u;
         s.tj4 = (p.tecjb > 255u ? 255u : p.tecjb) * 0x01010101u;
     }
+    template <bool LAZY = false>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
         if constexpr (kMsv) {
             return __vsubus4(__vaddus4(__vmaxu4(x, s.B), s.d4), c);
@@ -312,69 +321,114 @@ struct Swar8 {
         s.B = __vmaxu4(s.base4, __vsubus4(e, s.tj4));
     }
     __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
+    template <bool LAZY = false>
     __device__ static __forceinline__ uint32_t inject(const St&) { return NEG; }
     __device__ static __forceinline__ bool needs_exact(uint32_t, const St&) { return false; }
     __device__ static __forceinline__ uint32_t raw(uint32_t e) { return e & 0xffu; }
 };
 
-// Relaxed f16 variants: exact except on sequences they flag, which the host
-// rescoring pass (abi.cu) recomputes with the exact Fp16 kernel.
-//
-// SSV ("unsaturated"): q = (v-128)/256, table (dbias-cost)/256, one
-// HADD2.SAT per cell pair: max(v + dbias - cost, 128) without the 255 cap.
-// Identical to the saturating recurrence unless some cell exceeds
-// 255-dbias (before the first cap event both agree, and a cap event needs a
-// cell above 255-dbias, which the running E then records), so
-// raw >= 256-dbias is flagged.
-//
-// MSV ("lazy B"): cells live as w = max(v, B) in the linear f16 binade
-// p = 1 + (v-255)/2048 (bit pattern 0x3C00 - (255-v), one code per byte).
-// Per cell: HADD2.SAT adds dbias with the 1.0 cap (= byte 255) and one DPX
-// VIADDMNMX.S16 subtracts the cost and takes max(., B) on the bit pattern --
-// the next row's max(M, B) fused into this row's floor clamp.  When a
-// group's B grows after a row, a warp-uniform fix-up re-applies max(w, B').
-// E accumulates over w, so it can exceed the true E only while E <= base
-// (B <= max(base, E-tecjb)); B itself stays exact.  raw <= base(len) is
-// flagged.
+// FP16X, SSV ("relaxed"): exact except on the sequences it flags, which the
+// host rescoring pass (abi.cu) recomputes with the exact Fp16 kernel.
+// q = (v-128)/256, table (dbias-cost)/256, one HADD2.SAT per cell pair:
+// max(v + dbias - cost, 128) without the 255 cap.  Identical to the
+// saturating recurrence unless some cell exceeds 255-dbias (before the first
+// cap event both agree, and a cap event needs a cell above 255-dbias, which
+// the running E then records), so raw >= 256-dbias is flagged.
 template <int ALG>
 struct Fp16Relaxed {
+    static_assert(ALG == 1, "the relaxed form is the SSV half of FP16X; MSV uses Fp16Sat");
     static constexpr int CPW = 2;
-    static constexpr bool kMsv = ALG == 0;
+    static constexpr bool kMsv = false;
     static constexpr bool kRelaxed = true;
+    static constexpr bool kTwoMode = false;
     static constexpr uint32_t NEG = 0u;
     struct St {
-        uint32_t B, base2, d1, ntj2, base_v, cap;
+        uint32_t cap;
     };
-    __device__ static __forceinline__ uint32_t splat(float f) {
-        return as_u32(__float2half2_rn(f));
+    __device__ static __forceinline__ void init(St& s, uint32_t, const KParams& p) {
+        s.cap = 256u - p.dbias;
     }
-    __device__ static __forceinline__ void init(St& s, uint32_t base, const KParams& p) {
-        if constexpr (kMsv) {
-            s.base2 = (0x3C00u - (255u - base)) * 0x00010001u;
-            s.B = s.base2;
-            s.d1 = splat(float(p.dbias) / 2048.f);
-            s.ntj2 = (0u - p.tecjb) & 0xffffu;
-            s.ntj2 |= s.ntj2 << 16;
-            s.base_v = base;
-        } else {
-            s.cap = 256u - p.dbias;
-        }
-    }
-    __device__ static __forceinline__ uint32_t init_word(const St& s) { return kMsv ? s.B : 0u; }
-    __device__ static __forceinline__ uint32_t inject(const St& s) { return kMsv ? s.B : 0u; }
-    __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
-        if constexpr (kMsv) {
-            const uint32_t pp = as_u32(__hadd2_sat(as_h2(x), as_h2(s.d1)));
-            return __viaddmax_s16x2(pp, c, s.B);
-        } else {
-            return as_u32(__hadd2_sat(as_h2(x), as_h2(c)));
-        }
+    __device__ static __forceinline__ uint32_t init_word(const St&) { return 0u; }
+    template <bool LAZY = false>
+    __device__ static __forceinline__ uint32_t inject(const St&) { return 0u; }
+    template <bool LAZY = false>
+    __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St&) {
+        return as_u32(__hadd2_sat(as_h2(x), as_h2(c)));
     }
     __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
         return __vimax3_u16x2(E, a, b);
     }
-    __device__ static __forceinline__ uint32_t acc1(uint32_t E, uint32_t a) {
-        return __vmaxu2(E, a);
+    __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
+        return __byte_perm(top, up, 0x1076);
+    }
+    template <int L>
+    __device__ static __forceinline__ uint32_t group_reduce(uint32_t E) {
+        const uint32_t e = __vmaxu2(E, __byte_perm(E, E, 0x1032));
+        return group_max<L>(e);
+    }
+    __device__ static __forceinline__ void update_B(St&, uint32_t) {}
+    __device__ static __forceinline__ uint32_t raw(uint32_t e) {
+        const float f = __low2float(as_h2(e));
+        return 128u + uint32_t(f * 256.f + 0.5f);
+    }
+    __device__ static __forceinline__ bool needs_exact(uint32_t raw, const St& s) {
+        return raw >= s.cap;
+    }
+};
+
+// FP16X, MSV ("two-mode", exact throughout, no rescoring).  Byte v lives in
+// the linear f16 binade p = 1 + (v-255)/2048: bit pattern 0x3B01 + v, so
+// integer ops on the patterns are byte arithmetic and HADD2.SAT's 1.0 cap is
+// byte 255.  Table entries are -cost as s16.
+//   exact mode: cell = max(max(x, B) (+) dbias - cost, 0)
+//               = VIADDMNMX.S16(HADD2.SAT(HMNMX2(x, B), dbias), -cost, byte0)
+//   lazy mode:  once every sequence of the warp has E = 255, B = max(base,
+//               255 - tec - tjb) never changes again, so the cells can hold
+//               w = max(v, B) and the next row's max(x, B) folds into this
+//               row's floor clamp: w' = VIADDMNMX.S16(HADD2.SAT(w, dbias),
+//               -cost, B) -- one FP16 + one ALU op per word, no row
+//               reduction, no B update (both exact no-ops from there on).
+// The switch happens at a chunk boundary (run_chunk<.., LAZY>).  Every cell
+// of every row is still computed exactly in both modes.
+template <int ALG>
+struct Fp16Sat {
+    static_assert(ALG == 0, "the two-mode form is the MSV half of FP16X");
+    static constexpr int CPW = 2;
+    static constexpr bool kMsv = true;
+    static constexpr bool kRelaxed = false;
+    static constexpr bool kTwoMode = true;
+    static constexpr uint32_t kByte0 = 0x3B013B01u;  // byte 0 in both halves
+    static constexpr uint32_t NEG = kByte0;
+    struct St {
+        uint32_t B, base2, d1, ntj2;
+    };
+    __device__ static __forceinline__ void init(St& s, uint32_t base, const KParams& p) {
+        s.base2 = (0x3B01u + base) * 0x00010001u;
+        s.B = s.base2;
+        s.d1 = as_u32(__float2half2_rn(float(p.dbias) / 2048.f));
+        s.ntj2 = (0u - p.tecjb) & 0xffffu;
+        s.ntj2 |= s.ntj2 << 16;
+    }
+    __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
+    template <bool LAZY = false>
+    __device__ static __forceinline__ uint32_t inject(const St& s) { return LAZY ? s.B : NEG; }
+    template <bool LAZY = false>
+    __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
+        if constexpr (LAZY) {
+            const uint32_t pp = as_u32(__hadd2_sat(as_h2(x), as_h2(s.d1)));
+            return __viaddmax_s16x2(pp, c, s.B);
+        } else {
+#ifdef LHMM_SAT_VIMNMX
+            const uint32_t m = __vmaxu2(x, s.B);
+#else
+            const uint32_t m = as_u32(__hmax2(as_h2(x), as_h2(s.B)));
+#endif
+            const uint32_t pp = as_u32(__hadd2_sat(as_h2(m), as_h2(s.d1)));
+            return __viaddmax_s16x2(pp, c, kByte0);
+        }
+    }
+    __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
+        return __vimax3_u16x2(E, a, b);
     }
     __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
         return __byte_perm(top, up, 0x1076);
@@ -385,22 +439,18 @@ struct Fp16Relaxed {
         return group_max<L>(e);
     }
     __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
-        s.B = __viaddmax_s16x2(e, s.ntj2, s.base2);
+        s.B = __viaddmax_s16x2(e, s.ntj2, s.base2);  // max(E - (tec+tjb), base)
     }
-    __device__ static __forceinline__ uint32_t raw(uint32_t e) {
-        if constexpr (kMsv) {
-            // bit pattern 0x3B01 is byte 0; below it only the E accumulators'
-            // initial +0.0 (no row seen: empty sequence) -> the floor
-            const uint32_t b = e & 0xffffu;
-            return b >= 0x3B01u ? b - 0x3B01u : 0u;
-        } else {
-            const float f = __low2float(as_h2(e));
-            return 128u + uint32_t(f * 256.f + 0.5f);
-        }
+    __device__ static __forceinline__ bool saturated(uint32_t e) {
+        return (e & 0xffffu) == 0x3C00u;
     }
-    __device__ static __forceinline__ bool needs_exact(uint32_t raw, const St& s) {
-        return kMsv ? raw <= s.base_v : raw >= s.cap;
+    template <int H>
+    __device__ static __forceinline__ void enter_lazy(uint32_t (&g)[H], const St& s) {
+#pragma unroll
+        for (int h = 0; h < H; ++h) g[h] = __vmaxu2(g[h], s.B);
     }
+    __device__ static __forceinline__ uint32_t raw(uint32_t e) { return (e & 0xffffu) - 0x3B01u; }
+    __device__ static __forceinline__ bool needs_exact(uint32_t, const St&) { return false; }
 };
 
 // ---------------------------------------------------------------------------
@@ -414,6 +464,121 @@ __host__ __device__ constexpr int rows_per_iter() {
     constexpr int per_row = H * (V::kMsv ? 15 : 11) / 4 + 20;
     constexpr int words = V::CPW == 4 ? per_row * 3 : per_row;  // SWAR8 ops are emulated
     return 16 * words * 16 <= 32768 ? 16 : (8 * words * 16 <= 32768 ? 8 : 4);
+}
+
+// One chunk of RPI residue rows (fully unrolled).  Returns true when the
+// sub-batch's rows ended inside the chunk.  LAZY (two-mode MSV only): the
+// cells hold max(v, B) and B is constant -- see Fp16Sat.
+template <class V, int L, int H, int RPI, bool LAZY>
+__device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32_t& e1,
+                                          uint32_t& e2, uint32_t& e3, typename V::St& st,
+                                          const KParams& p, const uint8_t* src, uint32_t r0,
+                                          uint32_t rows, const uint32_t* tab_lane, uint32_t P,
+                                          int part_off, uint32_t shift_src, bool inject_here) {
+    uint32_t wds[RPI / 4];
+    const uint8_t* chunk = src + (r0 >> 4) * 512u;
+    if constexpr (RPI == 16) {
+        const uint4 v = ld_stream(chunk);
+        wds[0] = v.x;
+        wds[1] = v.y;
+        wds[2] = v.z;
+        wds[3] = v.w;
+    } else if constexpr (RPI == 8) {
+        const uint2 v = __ldcs(reinterpret_cast<const uint2*>(chunk + (r0 & 8u)));
+        wds[0] = v.x;
+        wds[1] = v.y;
+    } else {
+        wds[0] = __ldcs(reinterpret_cast<const unsigned int*>(chunk + (r0 & 12u)));
+    }
+#pragma unroll
+    for (int q = 0; q < RPI / 4; ++q) {
+        if (r0 + 4u * q >= rows) return true;  // warp-uniform
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int r = 4 * q + b;
+            const uint32_t x = (wds[q] >> (8 * b)) & 0xffu;
+            const uint32_t* tp = tab_lane + x * P;
+            // the register holding cell H-1 becomes cell 0 (stripe shift)
+            const int stop = ((H - 1 - r) % H + H) % H;
+            uint32_t up;
+            if constexpr (L > 1) {
+                up = __shfl_sync(kFull, g[stop], shift_src);
+                if (inject_here) up = V::template inject<LAZY>(st);
+            } else {
+                up = inject_here ? V::template inject<LAZY>(st) : g[stop];
+            }
+            // rows go in groups of four (one LDS.128 per lane); with
+            // H = 2 (mod 4) the top group holds two rows (LDS.64)
+#pragma unroll
+            for (int h4 = (H + 3) / 4 - 1; h4 >= 0; --h4) {
+                const bool full = 4 * h4 + 4 <= H;  // compile-time after unrolling
+                uint32_t cw[4];
+                if (full) {
+                    const uint4 c = *reinterpret_cast<const uint4*>(tp + h4 * 4 * L);
+                    cw[0] = c.x;
+                    cw[1] = c.y;
+                    cw[2] = c.z;
+                    cw[3] = c.w;
+                } else {
+                    // two-row top group: densely packed pairs (build_table)
+                    const uint2 c = *reinterpret_cast<const uint2*>(tp + part_off + h4 * 4 * L);
+                    cw[0] = c.x;
+                    cw[1] = c.y;
+                    cw[2] = cw[3] = 0u;
+                }
+#pragma unroll
+                for (int k = 3; k >= 0; --k) {
+                    const int h = 4 * h4 + k;
+                    if (h >= H) continue;
+                    const int sl = ((h - 1 - r) % H + H) % H;
+                    const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
+                    g[sl] = V::template cell<LAZY>(in, cw[k], st);
+                }
+                if constexpr (!V::kMsv || LAZY) {
+                    // SSV (and saturated MSV): fold the new words into E
+                    // right away so the ALU work interleaves with the FP16
+                    // cell updates (+4% at M=200/400)
+                    const int s0 = ((4 * h4 - 1 - r) % H + H) % H;
+                    const int s1 = ((4 * h4 - r) % H + H) % H;
+                    const int s2 = ((4 * h4 + 1 - r) % H + H) % H;
+                    const int s3 = ((4 * h4 + 2 - r) % H + H) % H;
+                    if (!full) {
+                        e0 = V::acc2(e0, g[s1], g[s0]);
+                    } else if (h4 & 1) {
+                        e0 = V::acc2(e0, g[s3], g[s2]);
+                        e1 = V::acc2(e1, g[s1], g[s0]);
+                    } else {
+                        e2 = V::acc2(e2, g[s3], g[s2]);
+                        e3 = V::acc2(e3, g[s1], g[s0]);
+                    }
+                }
+            }
+            if constexpr (V::kMsv && !LAZY) {
+#pragma unroll
+                for (int h = 0; h < H; h += 8) {
+                    e0 = V::acc2(e0, g[h], g[h + 1]);
+                    if (h + 2 < H) e1 = V::acc2(e1, g[h + 2], g[h + 3]);
+                    if (h + 4 < H) e2 = V::acc2(e2, g[h + 4], g[h + 5]);
+                    if (h + 6 < H) e3 = V::acc2(e3, g[h + 6], g[h + 7]);
+                }
+            }
+            if constexpr (V::kMsv && !LAZY) {
+                const uint32_t E =
+                    V::template group_reduce<L>(V::acc2(V::acc2(e0, e1, e2), e3, e3));
+                e0 = E;
+                V::update_B(st, E);
+            }
+        }
+    }
+    if constexpr (RPI % H != 0) {
+        // after RPI rows cell h sits in g[(h - RPI) mod H]: rename back
+        uint32_t t[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) t[h] = g[((h - RPI) % H + H) % H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) g[h] = t[h];
+    }
+    return false;
 }
 
 template <class V, int L, int H>
@@ -430,6 +595,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
     const uint32_t grp = lane / L;
     const uint32_t P = p.res_stride;
     const uint32_t* tab_lane = smem + (grp % COPIES) * p.copy_stride + 4u * oig;
+    // word offset of this lane's pair in a two-row top group, relative to
+    // tab_lane (see build_table): 2*oig, plus 2L for the upper quarter-warp
+    // of a 16-lane LDS.64 wavefront when L < 16
+    const int part_off = -2 * int(oig) + (L < 16 ? int((lane >> 3) & 1u) * 2 * L : 0);
     // stripe-shift source: the previous lane of the group; lane 0 of a group
     // gets -inf (normative) or, in the paper's wrap mode, the last lane's top
     const uint32_t shift_src = (lane & ~uint32_t(L - 1)) | ((lane + L - 1) & uint32_t(L - 1));
@@ -465,122 +634,28 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
         // iteration; one slot permutation restores the naming after RPI rows
         // (free when H divides RPI).
         constexpr int RPI = rows_per_iter<V, H>();
-        for (uint32_t r0 = 0; r0 < rows; r0 += RPI) {
-            uint32_t wds[RPI / 4];
-            const uint8_t* chunk = src + (r0 >> 4) * 512u;
-            if constexpr (RPI == 16) {
-                const uint4 v = ld_stream(chunk);
-                wds[0] = v.x;
-                wds[1] = v.y;
-                wds[2] = v.z;
-                wds[3] = v.w;
-            } else if constexpr (RPI == 8) {
-                const uint2 v = __ldcs(reinterpret_cast<const uint2*>(chunk + (r0 & 8u)));
-                wds[0] = v.x;
-                wds[1] = v.y;
-            } else {
-                wds[0] = __ldcs(reinterpret_cast<const unsigned int*>(chunk + (r0 & 12u)));
-            }
-#pragma unroll
-            for (int q = 0; q < RPI / 4; ++q) {
-                if (r0 + 4u * q >= rows) goto finished;  // warp-uniform
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int r = 4 * q + b;
-                    const uint32_t x = (wds[q] >> (8 * b)) & 0xffu;
-                    const uint32_t* tp = tab_lane + x * P;
-                    // the register holding cell H-1 becomes cell 0 (stripe shift)
-                    const int stop = ((H - 1 - r) % H + H) % H;
-                    uint32_t up;
-                    if constexpr (L > 1) {
-                        up = __shfl_sync(kFull, g[stop], shift_src);
-                        if (inject_here) up = V::inject(st);
-                    } else {
-                        up = inject_here ? V::inject(st) : g[stop];
-                    }
-                    // rows go in groups of four (one LDS.128 per lane); with
-                    // H = 2 (mod 4) the top group holds two rows (LDS.64)
-#pragma unroll
-                    for (int h4 = (H + 3) / 4 - 1; h4 >= 0; --h4) {
-                        const bool full = 4 * h4 + 4 <= H;  // compile-time after unrolling
-                        uint32_t cw[4];
-                        if (full) {
-                            const uint4 c = *reinterpret_cast<const uint4*>(tp + h4 * 4 * L);
-                            cw[0] = c.x;
-                            cw[1] = c.y;
-                            cw[2] = c.z;
-                            cw[3] = c.w;
-                        } else {
-                            const uint2 c = *reinterpret_cast<const uint2*>(tp + h4 * 4 * L);
-                            cw[0] = c.x;
-                            cw[1] = c.y;
-                            cw[2] = cw[3] = 0u;
-                        }
-#pragma unroll
-                        for (int k = 3; k >= 0; --k) {
-                            const int h = 4 * h4 + k;
-                            if (h >= H) continue;
-                            const int sl = ((h - 1 - r) % H + H) % H;
-                            const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
-                            g[sl] = V::cell(in, cw[k], st);
-                        }
-                        if constexpr (!V::kMsv) {
-                            // SSV: fold the new words into E right away so the
-                            // ALU work interleaves with the FP16 cell updates
-                            // (+4% at M=200/400; neutral for MSV, whose row
-                            // max feeds B)
-                            const int s0 = ((4 * h4 - 1 - r) % H + H) % H;
-                            const int s1 = ((4 * h4 - r) % H + H) % H;
-                            const int s2 = ((4 * h4 + 1 - r) % H + H) % H;
-                            const int s3 = ((4 * h4 + 2 - r) % H + H) % H;
-                            if (!full) {
-                                e0 = V::acc2(e0, g[s1], g[s0]);
-                            } else if (h4 & 1) {
-                                e0 = V::acc2(e0, g[s3], g[s2]);
-                                e1 = V::acc2(e1, g[s1], g[s0]);
-                            } else {
-                                e2 = V::acc2(e2, g[s3], g[s2]);
-                                e3 = V::acc2(e3, g[s1], g[s0]);
-                            }
-                        }
-                    }
-                    if constexpr (V::kMsv) {
-#pragma unroll
-                        for (int h = 0; h < H; h += 8) {
-                            e0 = V::acc2(e0, g[h], g[h + 1]);
-                            if (h + 2 < H) e1 = V::acc2(e1, g[h + 2], g[h + 3]);
-                            if (h + 4 < H) e2 = V::acc2(e2, g[h + 4], g[h + 5]);
-                            if (h + 6 < H) e3 = V::acc2(e3, g[h + 6], g[h + 7]);
-                        }
-                    }
-                    if constexpr (V::kMsv) {
-                        const uint32_t E =
-                            V::template group_reduce<L>(V::acc2(V::acc2(e0, e1, e2), e3, e3));
-                        e0 = E;
-                        if constexpr (V::kRelaxed) {
-                            // lazy B: re-apply max(w, B') only when some B grew
-                            const uint32_t Bold = st.B;
-                            V::update_B(st, E);
-                            if (__any_sync(kFull, st.B != Bold)) {
-#pragma unroll
-                                for (int h = 0; h < H; ++h) g[h] = __vmaxu2(g[h], st.B);
-                            }
-                        } else {
-                            V::update_B(st, E);
-                        }
-                    }
+        uint32_t r0 = 0;
+        bool done = false;
+#pragma unroll 1
+        for (; r0 < rows && !done; r0 += RPI) {
+            done = run_chunk<V, L, H, RPI, false>(g, e0, e1, e2, e3, st, p, src, r0, rows,
+                                                  tab_lane, P, part_off, shift_src, inject_here);
+            if constexpr (V::kTwoMode) {
+                // every sequence of the warp saturated (E = 255): B is constant
+                // from here on, so the cells switch to the lazy form max(v, B)
+                if (!done && __all_sync(kFull, V::saturated(e0))) {
+                    V::enter_lazy(g, st);
+                    r0 += RPI;
+                    break;
                 }
             }
-            if constexpr (RPI % H != 0) {
-                // after RPI rows cell h sits in g[(h - RPI) mod H]: rename back
-                uint32_t t[H];
-#pragma unroll
-                for (int h = 0; h < H; ++h) t[h] = g[((h - RPI) % H + H) % H];
-#pragma unroll
-                for (int h = 0; h < H; ++h) g[h] = t[h];
-            }
         }
-    finished:
+        if constexpr (V::kTwoMode) {
+#pragma unroll 1
+            for (; r0 < rows && !done; r0 += RPI)
+                done = run_chunk<V, L, H, RPI, true>(g, e0, e1, e2, e3, st, p, src, r0, rows,
+                                                     tab_lane, P, part_off, shift_src, inject_here);
+        }
         uint32_t E = V::acc2(V::acc2(e0, e1, e2), e3, e3);
         if constexpr (!V::kMsv) E = V::template group_reduce<L>(E);
         uint32_t raw = V::raw(E);

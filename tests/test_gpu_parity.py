@@ -261,10 +261,10 @@ def test_device_pipeline_matches_reference_library(ref):
 
 @pytest.mark.parametrize("alg", [P.Algorithm.Msv, P.Algorithm.Ssv], ids=lambda a: a.name)
 def test_relaxed_variant_rescoring_is_exact(ora, alg):
-    """FP16X flags the sequences its relaxed arithmetic cannot certify (SSV
-    cells above 255-dbias; MSV raw <= base) and rescores them exactly: force
-    many flags with planted motifs (SSV overflow) and a flat profile (MSV
-    raw == base), and check every byte against the oracle."""
+    """FP16X SSV flags the sequences its relaxed arithmetic cannot certify
+    (cells above 255-dbias) and rescores them exactly; FP16X MSV (two-mode)
+    is exact without rescoring.  Force many SSV flags with planted motifs and
+    check every byte against the oracle, including a flat profile."""
     rng = P.Rng(99)
     hmm = rng.random_profile(120)
     db = rng.random_records(4000, 20, 400, plant=(hmm, 0.5))
@@ -276,8 +276,32 @@ def test_relaxed_variant_rescoring_is_exact(ora, alg):
         rep = scan(costs, q, db, prof, alg=alg, variant=P.Variant.Fp16x, threshold=0.3)
         np.testing.assert_array_equal(rep.raw, want)
         assert rep.variant == int(P.Variant.Fp16x)
-        if prof is flat and alg == P.Algorithm.Msv:
+        if alg == P.Algorithm.Msv:
+            assert rep.stats["recomputed"] == 0
+        elif prof is hmm and q == P.QuantParams():
             assert rep.stats["recomputed"] > 0
+
+
+@pytest.mark.parametrize("L", [1, 2, 4, 8, 16, 32])
+def test_two_mode_msv_switch(ora, L):
+    """FP16X MSV switches a warp to the lazy-B form once all of its
+    sequences reach E = 255.  Mix saturating (planted), slowly saturating and
+    never-saturating sequences of varied lengths in the same warps, at
+    default and non-saturating parameters, and compare with the oracle."""
+    rng = P.Rng(0x5A7 + L)
+    m = 2 * L * rows_for(P.Variant.Fp16x, L, min(2 * L * 72, 700)) - L
+    hmm = rng.random_profile(m)
+    a = rng.random_records(300, 200, 900, plant=(hmm, 0.6))
+    b = rng.random_records(300, 1, 900)
+    db = P.SequenceDB.from_sequences([a.sequence(k) for k in range(a.count)] +
+                                     [b.sequence(k) for k in range(b.count)])
+    for q in (P.QuantParams(), P.QuantParams(3.0, 120, 3, 20, 20), P.QuantParams(2.0, 240, 10, 1, 5),
+              P.QuantParams(3.0, 195, 3, 0, 0)):
+        costs = P.quantize_emissions(hmm, q)
+        want = ora.scan_flat(0, costs.bytes, db.residues, db.offsets, oq(q))
+        rep = scan(costs, q, db, hmm, alg=P.Algorithm.Msv, variant=P.Variant.Fp16x, lanes=L,
+                   rows=rows_for(P.Variant.Fp16x, L, m))
+        np.testing.assert_array_equal(rep.raw, want, err_msg=f"L={L} q={q}")
 
 
 def wrap_model(alg, costs, m, seq, q, base):
