@@ -459,11 +459,26 @@ struct Fp16Sat {
 // Rows per unrolled iteration: the largest of 16/8/4 whose unrolled body
 // (~H*(3.75|2.75)+20 instructions per row for MSV|SSV, 16 B each) stays
 // within ~32 KB of SASS -- ncu showed no_instruction stalls beyond that.
-template <class V, int H>
+// Two-mode MSV (Fp16Sat) keeps two bodies resident; both use small budgets
+// (4-row chunks from H ~ 20 up): measured on B200 over L = 16/32, H = 4..72,
+// budgets of 8/8 KB average 15.6 T computed cells/s against 15.4 for 12/24 KB
+// and 14.1 for one 32 KB budget per body (profiles/r1_rpi_budget_fp16x_msv.jsonl).
+#ifndef LHMM_RPI_BUDGET
+#define LHMM_RPI_BUDGET 32768
+#endif
+#ifndef LHMM_RPI_BUDGET_EXACT2
+#define LHMM_RPI_BUDGET_EXACT2 8192
+#endif
+#ifndef LHMM_RPI_BUDGET_LAZY2
+#define LHMM_RPI_BUDGET_LAZY2 8192
+#endif
+template <class V, int H, bool LAZY = false>
 __host__ __device__ constexpr int rows_per_iter() {
-    constexpr int per_row = H * (V::kMsv ? 15 : 11) / 4 + 20;
+    constexpr int per_row = LAZY ? H * 11 / 4 + 12 : H * (V::kMsv ? 15 : 11) / 4 + 20;
     constexpr int words = V::CPW == 4 ? per_row * 3 : per_row;  // SWAR8 ops are emulated
-    return 16 * words * 16 <= 32768 ? 16 : (8 * words * 16 <= 32768 ? 8 : 4);
+    constexpr int budget = !V::kTwoMode ? LHMM_RPI_BUDGET
+                                        : (LAZY ? LHMM_RPI_BUDGET_LAZY2 : LHMM_RPI_BUDGET_EXACT2);
+    return 16 * words * 16 <= budget ? 16 : (8 * words * 16 <= budget ? 8 : 4);
 }
 
 // One chunk of RPI residue rows (fully unrolled).  Returns true when the
@@ -643,7 +658,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
             if constexpr (V::kTwoMode) {
                 // every sequence of the warp saturated (E = 255): B is constant
                 // from here on, so the cells switch to the lazy form max(v, B)
-                if (!done && __all_sync(kFull, V::saturated(e0))) {
+                // (at a row aligned to the lazy body's chunk)
+                constexpr int RPI_L = rows_per_iter<V, H, true>();
+                if (!done && ((r0 + RPI) % RPI_L) == 0 && __all_sync(kFull, V::saturated(e0))) {
                     V::enter_lazy(g, st);
                     r0 += RPI;
                     break;
@@ -651,10 +668,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
             }
         }
         if constexpr (V::kTwoMode) {
+            constexpr int RPI_L = rows_per_iter<V, H, true>();
 #pragma unroll 1
-            for (; r0 < rows && !done; r0 += RPI)
-                done = run_chunk<V, L, H, RPI, true>(g, e0, e1, e2, e3, st, p, src, r0, rows,
-                                                     tab_lane, P, part_off, shift_src, inject_here);
+            for (; r0 < rows && !done; r0 += RPI_L)
+                done = run_chunk<V, L, H, RPI_L, true>(g, e0, e1, e2, e3, st, p, src, r0, rows,
+                                                       tab_lane, P, part_off, shift_src,
+                                                       inject_here);
         }
         uint32_t E = V::acc2(V::acc2(e0, e1, e2), e3, e3);
         if constexpr (!V::kMsv) E = V::template group_reduce<L>(E);

@@ -22,7 +22,10 @@ def main():
     ap.add_argument("--nseq", type=int, default=1_000_000)
     ap.add_argument("--variants", default="fp16")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--algs", default="msv,ssv")
+    ap.add_argument("--lanes", default="", help="subset of lane counts, e.g. 16,32")
     args = ap.parse_args()
+    lanes = [int(x) for x in args.lanes.split(",")] if args.lanes else gen_instances.LANES
     db = P.Rng(0x5EED).lognormal_records(args.nseq, 290, 0.65, 2)
     q = P.QuantParams()
     s = P.Scanner(0)
@@ -32,13 +35,13 @@ def main():
             "fp16x": P.Variant.Fp16x}
     for vn in args.variants.split(","):
         cpw = 4 if vn == "swar8" else 2
-        for L in gen_instances.LANES:
+        for L in lanes:
             for H in gen_instances.ROWS[vn]:
                 cap = cpw * L * H
                 m = min(cap, 4096)
                 hmm = P.Rng(9000 + m).random_profile(m)
                 s.set_profile(P.quantize_emissions(hmm, q), q, hmm.lambda_, hmm.tau)
-                for a in ("msv", "ssv"):
+                for a in args.algs.split(","):
                     alg = P.Algorithm.Msv if a == "msv" else P.Algorithm.Ssv
                     opt = P.ScanOptions(alg=alg, variant=vmap[vn], lanes=L, rows=H)
                     try:
