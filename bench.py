@@ -222,7 +222,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--variant", default="auto", choices=["auto", "dpx16", "fp16", "swar8", "fp16x"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "dpx16", "fp16", "swar8", "fp16x",
+                                                       "fp16xalt"])
     ap.add_argument("--nseq", type=int, default=0, help="override sequences per GPU")
     ap.add_argument("--ref-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -265,7 +266,8 @@ def main():
             comm_dev = torch.device("cpu")
     desc, wl_alg, models_m, nseq, gen = WORKLOADS[args.workload]
     variant = {"auto": P.Variant.Auto, "dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16,
-               "swar8": P.Variant.Swar8, "fp16x": P.Variant.Fp16x}[args.variant]
+               "swar8": P.Variant.Swar8, "fp16x": P.Variant.Fp16x,
+               "fp16xalt": P.Variant.Fp16xAlt}[args.variant]
     q = P.QuantParams()
     algs = algs_of(wl_alg)
     threshold = 0.022
@@ -430,7 +432,7 @@ def main():
         L, H, v, grid, smem, recomputed = geo[k]
         per_scan.append({"alg": a, "M": m, "ms": round(t, 4),
                          "gcups": round(dbstats["residues"] * m / (t * 1e-3) / 1e9, 1),
-                         "lanes": L, "rows": H, "variant": ["auto", "dpx16", "fp16", "swar8", "fp16x"][v],
+                         "lanes": L, "rows": H, "variant": ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt"][v],
                          "grid": grid, "smem_bytes": smem, "rescored_exactly": recomputed})
     line = {
         "metric": "MSV/SSV GCUPS (device-timed) vs model length",

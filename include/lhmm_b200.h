@@ -67,8 +67,13 @@ enum lhmm_variant {
     LHMM_VARIANT_DPX16 = 1, /* u16x2 lanes, native VIADDMNMX/VIMNMX (ALU pipe) */
     LHMM_VARIANT_FP16 = 2,  /* f16x2 saturating adds on the FMA pipe */
     LHMM_VARIANT_SWAR8 = 3, /* u8x4 __vaddus4/__vsubus4/__vmaxu4 (paper tier 5) */
-    LHMM_VARIANT_FP16X = 4  /* relaxed f16 (SSV without the 255 cap, MSV with lazy B);
-                               flagged sequences are rescored by the exact FP16 kernel */
+    LHMM_VARIANT_FP16X = 4, /* SSV: relaxed f16 without the 255 cap, flagged sequences
+                               rescored by the exact FP16 kernel; MSV: two-mode (exact
+                               linear-f16, then lazy B once a warp's sequences saturate) */
+    LHMM_VARIANT_FP16X_ALT = 5 /* MSV: FP16X with every 4th word's cost step on the FP16
+                                  pipe instead of the ALU (same results; a code-generation
+                                  alternative picked per geometry from the calibration);
+                                  SSV: same as FP16X */
 };
 
 /* Byte-space constants; mirror of lanehmm::QuantParams

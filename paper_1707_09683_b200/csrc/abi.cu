@@ -79,6 +79,9 @@ const int* rows_list(int variant, int* n) {
     case LHMM_VARIANT_FP16X:
         *n = int(sizeof(lhmm::kRows_fp16x) / sizeof(int));
         return lhmm::kRows_fp16x;
+    case LHMM_VARIANT_FP16X_ALT:
+        *n = int(sizeof(lhmm::kRows_fp16xalt) / sizeof(int));
+        return lhmm::kRows_fp16xalt;
     default:
         *n = int(sizeof(lhmm::kRows_swar8) / sizeof(int));
         return lhmm::kRows_swar8;
@@ -121,7 +124,8 @@ double model_rate(int variant, int alg, uint32_t L, uint32_t H) {
     double w;
     if (variant == LHMM_VARIANT_SWAR8)
         w = alg == LHMM_MSV ? 30.0 : 26.0;
-    else if (variant == LHMM_VARIANT_FP16 || variant == LHMM_VARIANT_FP16X)
+    else if (variant == LHMM_VARIANT_FP16 || variant == LHMM_VARIANT_FP16X ||
+             variant == LHMM_VARIANT_FP16X_ALT)
         w = alg == LHMM_MSV ? 4.5 : 3.0;
     else
         w = alg == LHMM_MSV ? 4.5 : 3.5;
@@ -151,14 +155,22 @@ Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64
     // auto considers the measured variants only (calib_b200.inc); the
     // relaxed FP16X also needs a database large enough to amortise its
     // rescoring check.  Without any measurement the cost model decides.
-    const int vs[3] = {LHMM_VARIANT_FP16, LHMM_VARIANT_DPX16, LHMM_VARIANT_FP16X};
-    const int nv = variant == LHMM_VARIANT_AUTO ? 3 : 1;
+    // FP16X stands for both of its code forms (FP16X, FP16X_ALT): the
+    // measured table picks the faster one per geometry
+    const int vs_auto[4] = {LHMM_VARIANT_FP16, LHMM_VARIANT_DPX16, LHMM_VARIANT_FP16X,
+                            LHMM_VARIANT_FP16X_ALT};
+    const int vs_x[2] = {LHMM_VARIANT_FP16X, LHMM_VARIANT_FP16X_ALT};
+    const int* vs = variant == LHMM_VARIANT_AUTO ? vs_auto : vs_x;
+    const int nv = variant == LHMM_VARIANT_AUTO ? 4 : (variant == LHMM_VARIANT_FP16X ? 2 : 1);
     for (int pass = 0; pass < 2 && best.L == 0; ++pass) {
         const bool measured_only = variant == LHMM_VARIANT_AUTO && pass == 0;
         for (int vi = 0; vi < nv; ++vi) {
-            const int v = variant == LHMM_VARIANT_AUTO ? vs[vi] : variant;
-            if (variant == LHMM_VARIANT_AUTO && v == LHMM_VARIANT_FP16X &&
-                ((n_tiles > 0 && n_tiles < 4096) || !allow_relaxed))
+            const int v = (variant == LHMM_VARIANT_AUTO || variant == LHMM_VARIANT_FP16X)
+                              ? vs[vi] : variant;
+            if (!find_dispatch(v, alg, 1)) continue;  // FP16X_ALT: MSV only
+            const bool x = v == LHMM_VARIANT_FP16X || v == LHMM_VARIANT_FP16X_ALT;
+            if (variant == LHMM_VARIANT_AUTO && x &&
+                ((alg == LHMM_SSV && n_tiles > 0 && n_tiles < 4096) || !allow_relaxed))
                 continue;
             const uint32_t cpw = lhmm::cells_per_word(v);
             int n;
@@ -379,7 +391,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
     if (opt->alg != LHMM_MSV && opt->alg != LHMM_SSV)
         return set_error(LHMM_ERR_CONTRACT, "unknown algorithm");
-    if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_FP16X)
+    if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_FP16X_ALT)
         return set_error(LHMM_ERR_CONTRACT, "unknown kernel variant");
     if (opt->reorder_mode != 0 && opt->reorder_mode != 1)
         return set_error(LHMM_ERR_CONTRACT, "unknown reorder mode");
@@ -388,7 +400,10 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     // host-resident (streamed) database uses the exact FP16 kernel instead
     const bool streamed_db = view == nullptr && c->host_resident;
     int variant = opt->variant;
-    if (streamed_db && variant == LHMM_VARIANT_FP16X) variant = LHMM_VARIANT_FP16;
+    if (variant == LHMM_VARIANT_FP16X_ALT && opt->alg == LHMM_SSV)
+        variant = LHMM_VARIANT_FP16X;  // the ALT code form is MSV-only
+    if (streamed_db && opt->alg == LHMM_SSV && variant == LHMM_VARIANT_FP16X)
+        variant = LHMM_VARIANT_FP16;
     uint32_t L = opt->lanes, H = opt->rows;
     if (L != 0 && (L > 32 || (L & (L - 1))))
         return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,32]");
@@ -407,6 +422,11 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             Choice ch = choose_geometry(pf.m, opt->alg, variant, 0, v.n_tiles, c->sm_count,
                                         !streamed_db);
             L = ch.L ? ch.L : 1;
+            if (ch.L) variant = ch.variant;
+        } else if (variant == LHMM_VARIANT_FP16X && opt->alg == LHMM_MSV &&
+                   calib_rate(LHMM_VARIANT_FP16X_ALT, LHMM_MSV, L, H) >
+                       calib_rate(LHMM_VARIANT_FP16X, LHMM_MSV, L, H)) {
+            variant = LHMM_VARIANT_FP16X_ALT;  // the faster code form of this geometry
         }
     }
     if (L < 1 || L > 32 || (L & (L - 1)))
@@ -489,7 +509,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     p.tecjb = uint32_t(pf.q.tec) + uint32_t(pf.q.tjb);
     p.fault = opt->fault_injection ? 1u : 0u;
     p.wrap = opt->reorder_mode == 1 ? 1u : 0u;
-    const bool relaxed = variant == LHMM_VARIANT_FP16X;
+    const bool relaxed = variant == LHMM_VARIANT_FP16X && opt->alg == LHMM_SSV;
     if (relaxed) {
         if (int rc = c->d_flag.reserve(std::max<uint64_t>(c->db.n_local, 1))) return rc;
         if (int rc = c->d_flag_count.reserve(1)) return rc;

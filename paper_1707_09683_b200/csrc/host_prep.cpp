@@ -302,7 +302,8 @@ static uint32_t encode_word(int variant, int alg, const uint8_t* c, uint32_t cpw
         if (variant == LHMM_VARIANT_SWAR8) {
             e = c[k];
         } else if (variant == LHMM_VARIANT_DPX16 ||
-                   (variant == LHMM_VARIANT_FP16X && alg == LHMM_MSV)) {
+                   ((variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16X_ALT) &&
+                    alg == LHMM_MSV)) {
             e = uint16_t(-int(c[k]));
         } else if (variant == LHMM_VARIANT_FP16X) {  // SSV: (dbias - cost)/256
             e = half_bits((float(dbias) - float(c[k])) / 256.f);
@@ -331,8 +332,17 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
                     const uint64_t node = uint64_t(cpw * oig + k) * H + h + 1;
                     c[k] = (node > m || x > kUnknown) ? 0xff : costs[(node - 1) * 21 + x];
                 }
-                const uint32_t w = encode_word(variant, alg, c, cpw, dbias);
-                if (H % 4 == 2 && h / 4 == H / 4) {
+                uint32_t w = encode_word(variant, alg, c, cpw, dbias);
+                const bool top_pair = H % 4 == 2 && h / 4 == H / 4;
+                if (variant == LHMM_VARIANT_FP16X_ALT && alg == LHMM_MSV && h % 4 == 3 &&
+                    !top_pair) {
+                    // two-mode MSV, ALT form: the FP16-form word of each full
+                    // row group (lhmm_kernel.cuh fp_word) takes -cost/2048 as f16
+                    w = 0;
+                    for (uint32_t k = 0; k < cpw; ++k)
+                        w |= uint32_t(half_bits(-float(c[k]) / 2048.f)) << (16 * k);
+                }
+                if (top_pair) {
                     // two-row top group, read with LDS.64: lanes' word pairs
                     // packed densely (2*oig); with L < 16 the two
                     // quarter-warps of a 16-lane wavefront read separate

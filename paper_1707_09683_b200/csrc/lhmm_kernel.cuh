@@ -169,7 +169,7 @@ struct Dpx16 {
         s.ntj2 = (0u - p.tecjb) & 0xffffu;
         s.ntj2 |= s.ntj2 << 16;
     }
-    template <bool LAZY = false>
+    template <bool LAZY = false, bool FPW = false>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
         if constexpr (kMsv) {
             uint32_t y = __viaddmin_u16x2(__vmaxu2(x, s.B), s.d2, 0x00ff00ffu);
@@ -237,7 +237,7 @@ struct Fp16 {
         }
         s.B = s.base2;
     }
-    template <bool LAZY = false>
+    template <bool LAZY = false, bool FPW = false>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
         if constexpr (kMsv) {
             const uint32_t m = __vmaxu2(x, s.B);
@@ -294,7 +294,7 @@ struct Swar8 {
         s.d4 = p.dbias * 0x01010101u;
         s.tj4 = (p.tecjb > 255u ? 255u : p.tecjb) * 0x01010101u;
     }
-    template <bool LAZY = false>
+    template <bool LAZY = false, bool FPW = false>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
         if constexpr (kMsv) {
             return __vsubus4(__vaddus4(__vmaxu4(x, s.B), s.d4), c);
@@ -351,7 +351,7 @@ struct Fp16Relaxed {
     __device__ static __forceinline__ uint32_t init_word(const St&) { return 0u; }
     template <bool LAZY = false>
     __device__ static __forceinline__ uint32_t inject(const St&) { return 0u; }
-    template <bool LAZY = false>
+    template <bool LAZY = false, bool FPW = false>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St&) {
         return as_u32(__hadd2_sat(as_h2(x), as_h2(c)));
     }
@@ -390,7 +390,7 @@ struct Fp16Relaxed {
 //               reduction, no B update (both exact no-ops from there on).
 // The switch happens at a chunk boundary (run_chunk<.., LAZY>).  Every cell
 // of every row is still computed exactly in both modes.
-template <int ALG>
+template <int ALG, int FPE = 0>
 struct Fp16Sat {
     static_assert(ALG == 0, "the two-mode form is the MSV half of FP16X");
     static constexpr int CPW = 2;
@@ -398,6 +398,9 @@ struct Fp16Sat {
     static constexpr bool kRelaxed = false;
     static constexpr bool kTwoMode = true;
     static constexpr uint32_t kByte0 = 0x3B013B01u;  // byte 0 in both halves
+    // FPE = 4 (FP16X_ALT): one word in four (h % 4 == 3 of full row groups)
+    // uses the FP16 form; FPE = 0 (FP16X): none
+    static constexpr int kFpEvery = FPE;
     static constexpr uint32_t NEG = kByte0;
     struct St {
         uint32_t B, base2, d1, ntj2;
@@ -412,19 +415,19 @@ struct Fp16Sat {
     __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
     template <bool LAZY = false>
     __device__ static __forceinline__ uint32_t inject(const St& s) { return LAZY ? s.B : NEG; }
-    template <bool LAZY = false>
+    template <bool LAZY = false, bool FPW = false>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
-        if constexpr (LAZY) {
-            const uint32_t pp = as_u32(__hadd2_sat(as_h2(x), as_h2(s.d1)));
-            return __viaddmax_s16x2(pp, c, s.B);
+        // FPW words (every kFpEvery-th row of a group, see kFpEvery) take
+        // their cost as the f16 value -cost/2048 and subtract / clamp on the
+        // FP16 pipe instead of the ALU: that balances the two pipes
+        const uint32_t m =
+            LAZY ? x : as_u32(__hmax2(as_h2(x), as_h2(s.B)));
+        const uint32_t pp = as_u32(__hadd2_sat(as_h2(m), as_h2(s.d1)));
+        const uint32_t floor = LAZY ? s.B : kByte0;
+        if constexpr (FPW) {
+            return as_u32(__hmax2(__hadd2(as_h2(pp), as_h2(c)), as_h2(floor)));
         } else {
-#ifdef LHMM_SAT_VIMNMX
-            const uint32_t m = __vmaxu2(x, s.B);
-#else
-            const uint32_t m = as_u32(__hmax2(as_h2(x), as_h2(s.B)));
-#endif
-            const uint32_t pp = as_u32(__hadd2_sat(as_h2(m), as_h2(s.d1)));
-            return __viaddmax_s16x2(pp, c, kByte0);
+            return __viaddmax_s16x2(pp, c, floor);
         }
     }
     __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
@@ -479,6 +482,17 @@ __host__ __device__ constexpr int rows_per_iter() {
     constexpr int budget = !V::kTwoMode ? LHMM_RPI_BUDGET
                                         : (LAZY ? LHMM_RPI_BUDGET_LAZY2 : LHMM_RPI_BUDGET_EXACT2);
     return 16 * words * 16 <= budget ? 16 : (8 * words * 16 <= budget ? 8 : 4);
+}
+
+// Whether word k of a row group takes the FP16 form of Fp16Sat (matches the
+// table encoding in build_table: h % 4 == 3 of full groups).
+template <class V>
+__host__ __device__ constexpr bool fp_word(int k, bool full) {
+    if constexpr (V::kTwoMode) {
+        return V::kFpEvery == 4 && full && k == 3;
+    } else {
+        return false;
+    }
 }
 
 // One chunk of RPI residue rows (fully unrolled).  Returns true when the
@@ -547,7 +561,11 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                     if (h >= H) continue;
                     const int sl = ((h - 1 - r) % H + H) % H;
                     const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
-                    g[sl] = V::template cell<LAZY>(in, cw[k], st);
+                    // (the condition folds away once the loops are unrolled)
+                    if (fp_word<V>(k, full))
+                        g[sl] = V::template cell<LAZY, true>(in, cw[k], st);
+                    else
+                        g[sl] = V::template cell<LAZY, false>(in, cw[k], st);
                 }
                 if constexpr (!V::kMsv || LAZY) {
                     // SSV (and saturated MSV): fold the new words into E

@@ -71,6 +71,7 @@ class Variant(enum.IntEnum):
     Fp16 = 2
     Swar8 = 3
     Fp16x = 4
+    Fp16xAlt = 5   # MSV only: FP16X with a quarter of the cost steps on the FP16 pipe
 
 
 @dataclass

@@ -20,7 +20,8 @@ sys.path.insert(0, os.path.join(ROOT, "paper_1707_09683_b200", "csrc"))
 import gen_instances  # noqa: E402
 
 ROWS = {P.Variant.Dpx16: gen_instances.ROWS["dpx16"], P.Variant.Fp16: gen_instances.ROWS["fp16"],
-        P.Variant.Swar8: gen_instances.ROWS["swar8"], P.Variant.Fp16x: gen_instances.ROWS["fp16x"]}
+        P.Variant.Swar8: gen_instances.ROWS["swar8"], P.Variant.Fp16x: gen_instances.ROWS["fp16x"],
+        P.Variant.Fp16xAlt: gen_instances.ROWS["fp16xalt"]}
 
 
 def main():
@@ -38,7 +39,7 @@ def main():
     s.set_database(db)
     res = db.total_residues()
     vmap = {"dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16, "swar8": P.Variant.Swar8,
-            "fp16x": P.Variant.Fp16x}
+            "fp16x": P.Variant.Fp16x, "fp16xalt": P.Variant.Fp16xAlt}
     for m in [int(x) for x in args.models.split(",")]:
         hmm = P.Rng(7000 + m).random_profile(m)
         costs = P.quantize_emissions(hmm, q)

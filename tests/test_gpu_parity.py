@@ -11,7 +11,7 @@ import paper_1707_09683_b200 as P
 
 pytestmark = pytest.mark.gpu
 
-VARIANTS = [P.Variant.Dpx16, P.Variant.Fp16, P.Variant.Swar8, P.Variant.Fp16x]
+VARIANTS = [P.Variant.Dpx16, P.Variant.Fp16, P.Variant.Swar8, P.Variant.Fp16x, P.Variant.Fp16xAlt]
 QUANTS = [P.QuantParams(), P.QuantParams(3.0, 120, 3, 20, 20), P.QuantParams(2.0, 240, 10, 1, 5),
           P.QuantParams(3.0, 0, 0, 0, 0)]
 
@@ -26,7 +26,8 @@ def rows_list(variant):
     sys.path.insert(0, os.path.join(os.path.dirname(P.__file__), "csrc"))
     import gen_instances
     return gen_instances.ROWS[{P.Variant.Swar8: "swar8", P.Variant.Dpx16: "dpx16",
-                               P.Variant.Fp16: "fp16", P.Variant.Fp16x: "fp16x"}[variant]]
+                               P.Variant.Fp16: "fp16", P.Variant.Fp16x: "fp16x",
+                               P.Variant.Fp16xAlt: "fp16xalt"}[variant]]
 
 
 def rows_for(variant, L, m):
@@ -282,8 +283,9 @@ def test_relaxed_variant_rescoring_is_exact(ora, alg):
             assert rep.stats["recomputed"] > 0
 
 
+@pytest.mark.parametrize("variant", [P.Variant.Fp16x, P.Variant.Fp16xAlt], ids=lambda v: v.name)
 @pytest.mark.parametrize("L", [1, 2, 4, 8, 16, 32])
-def test_two_mode_msv_switch(ora, L):
+def test_two_mode_msv_switch(ora, L, variant):
     """FP16X MSV switches a warp to the lazy-B form once all of its
     sequences reach E = 255.  Mix saturating (planted), slowly saturating and
     never-saturating sequences of varied lengths in the same warps, at
@@ -299,7 +301,7 @@ def test_two_mode_msv_switch(ora, L):
               P.QuantParams(3.0, 195, 3, 0, 0)):
         costs = P.quantize_emissions(hmm, q)
         want = ora.scan_flat(0, costs.bytes, db.residues, db.offsets, oq(q))
-        rep = scan(costs, q, db, hmm, alg=P.Algorithm.Msv, variant=P.Variant.Fp16x, lanes=L,
+        rep = scan(costs, q, db, hmm, alg=P.Algorithm.Msv, variant=variant, lanes=L,
                    rows=rows_for(P.Variant.Fp16x, L, m))
         np.testing.assert_array_equal(rep.raw, want, err_msg=f"L={L} q={q}")
 
