@@ -111,11 +111,19 @@ bool use_replica(int variant, uint32_t L, uint32_t H) {
     return L > 1 && L < 32 && lhmm::table_bytes_for(variant, L, H, true) <= kMaxTableBytes;
 }
 
+// measured rate of one (variant, alg, L, H), or -1 (indexed once: the policy
+// queries a few hundred points per scan)
 double calib_rate(int variant, int alg, uint32_t L, uint32_t H) {
-    for (const auto& c : kCalib)
-        if (c.variant == variant && c.alg == alg && uint32_t(c.lanes) == L && uint32_t(c.rows) == H)
-            return c.cell_gcups;
-    return -1.0;
+    static const std::map<uint64_t, double> index = [] {
+        std::map<uint64_t, double> m;
+        for (const auto& c : kCalib)
+            m[(uint64_t(c.variant) << 48) | (uint64_t(c.alg) << 40) | (uint64_t(c.lanes) << 20) |
+              uint64_t(c.rows)] = c.cell_gcups;
+        return m;
+    }();
+    const auto it = index.find((uint64_t(variant) << 48) | (uint64_t(alg) << 40) |
+                               (uint64_t(L) << 20) | uint64_t(H));
+    return it == index.end() ? -1.0 : it->second;
 }
 
 // Fallback cost model for points without a measurement: estimated
@@ -275,6 +283,9 @@ struct lhmm_context {
     DevBuf<uint32_t> d_flag_count;
 
     std::map<std::tuple<int, int, uint32_t, uint32_t, size_t>, int> occupancy;
+    // geometry policy results per (m, alg, variant, want_L, tiles, relaxed ok)
+    std::map<std::tuple<uint32_t, int, int, uint32_t, uint64_t, bool>, std::tuple<int, uint32_t, uint32_t>>
+        choices;
 
     // out-of-core mode: when the packed image exceeds db_budget the database
     // stays in pinned host memory and every scan streams it through two
@@ -408,8 +419,16 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (L != 0 && (L > 32 || (L & (L - 1))))
         return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,32]");
     if (H == 0) {
-        Choice ch = choose_geometry(pf.m, opt->alg, variant, L, v.n_tiles, c->sm_count,
-                                    !streamed_db);
+        Choice ch;
+        const auto ckey = std::make_tuple(pf.m, opt->alg, variant, L, v.n_tiles, !streamed_db);
+        const auto cit = c->choices.find(ckey);
+        if (cit != c->choices.end()) {
+            std::tie(ch.variant, ch.L, ch.H) = cit->second;
+        } else {
+            ch = choose_geometry(pf.m, opt->alg, variant, L, v.n_tiles, c->sm_count, !streamed_db);
+            if (c->choices.size() > 256) c->choices.clear();
+            c->choices.emplace(ckey, std::make_tuple(ch.variant, ch.L, ch.H));
+        }
         if (!ch.L)
             return set_error(LHMM_ERR_DATA,
                              "no instantiated geometry covers model length " + std::to_string(pf.m));
