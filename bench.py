@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 CELLS_PER_CLK_PER_SM = 64  # packed-integer-SIMD roofline
+L2_BYTES = 126 * 2**20     # B200 L2
 
 WORKLOADS = {
     # name: (description, alg, models, nseq per GPU, generator)
@@ -232,6 +233,9 @@ def main():
     ap.add_argument("--algs", default="", help="override algorithms: msv, ssv or both")
     ap.add_argument("--backend", default=os.environ.get("LHMM_DIST_BACKEND", "nccl"),
                     help="torch.distributed backend for N>1 (gloo lets ranks share one GPU)")
+    ap.add_argument("--db-budget", type=int, default=0,
+                    help="device bytes for the packed database (0 = resident); larger databases "
+                         "are streamed from pinned host memory on every scan")
     ap.add_argument("--lanes", type=int, default=0)
     ap.add_argument("--rows", type=int, default=0)
     args = ap.parse_args()
@@ -280,6 +284,10 @@ def main():
     stream = torch.cuda.current_stream()
     s = P.Scanner(local)
     s.set_stream(stream.cuda_stream)
+    if args.db_budget:
+        # out-of-core mode: the packed database stays in pinned host memory and
+        # every scan streams it through a two-slot device ring
+        s.set_db_budget(args.db_budget)
     t0 = time.perf_counter()
     n_local = s.set_database(db, rank, world)
     t_pack = time.perf_counter() - t0
@@ -333,21 +341,38 @@ def main():
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # inputs smaller than L2 (126 MB): flush L2 between timed steps by writing
+    # a 256 MB buffer outside the timed windows; larger inputs evict it anyway
+    flush = None
+    if dbstats["packed_bytes"] < L2_BYTES and not args.db_budget:
+        flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device="cuda")
     launches = 0
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            launches += step(True)
-            gather_results()
-        ev1.record(stream)
-        torch.cuda.synchronize()
+        if flush is None:
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            for _ in range(args.steps):
+                launches += step(True)
+                gather_results()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            ms = ev0.elapsed_time(ev1)
+        else:
+            ms = 0.0
+            for _ in range(args.steps):
+                flush.fill_(1)
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record(stream)
+                launches += step(True)
+                gather_results()
+                ev1.record(stream)
+                torch.cuda.synchronize()
+                ms += ev0.elapsed_time(ev1)
         if dist:
             dist.barrier()
-    ms = ev0.elapsed_time(ev1)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=comm_dev)
     cells_local = sum(dbstats["residues"] * m for _, m, _ in scans) * args.steps
     cells_t = torch.tensor([float(cells_local)], dtype=torch.float64, device=comm_dev)
@@ -444,9 +469,16 @@ def main():
                    "sequences": int(db.count), "residues": int(db.total_residues()),
                    "threshold": threshold, "quant": "QuantParams{3.0,195,3,3,3}",
                    "parallelism": f"shard{world} by residue count, raw+pass gathered to rank 0",
-                   "l2": "inputs larger than L2 (packed database "
-                         f"{dbstats['packed_bytes'] / 1e6:.0f} MB per GPU > 126 MB)",
-                   "early_exit": False},
+                   "l2": ("inputs larger than L2 (packed database "
+                          f"{dbstats['packed_bytes'] / 1e6:.0f} MB per GPU > 126 MB)"
+                          if flush is None else
+                          "L2 flushed between timed steps (256 MB write outside the timed "
+                          f"windows; packed database {dbstats['packed_bytes'] / 1e6:.1f} MB < "
+                          "126 MB)"),
+                   "early_exit": False,
+                   **({"out_of_core": f"database streamed from pinned host memory through a "
+                                      f"{args.db_budget / 2**20:.0f} MiB device ring per scan"}
+                      if args.db_budget else {})},
         "e2e": e2e,
         "gpu_launches": launches * world,
         "roofline": {"bound": "int-simd", "achieved": round(achieved, 1),
