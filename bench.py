@@ -286,7 +286,7 @@ def main():
     s.set_stream(stream.cuda_stream)
     if args.db_budget:
         # out-of-core mode: the packed database stays in pinned host memory and
-        # every scan streams it through a two-slot device ring
+        # every scan streams it through a ring of device slots
         s.set_db_budget(args.db_budget)
     t0 = time.perf_counter()
     n_local = s.set_database(db, rank, world)

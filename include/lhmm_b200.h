@@ -154,10 +154,11 @@ int lhmm_context_device_info(lhmm_context* ctx, int* sm_count, int* sm_clock_khz
 
 /* Out-of-core databases: cap the device bytes the packed residue data may
  * occupy (0 = unlimited, the default).  A database whose packed image is
- * larger stays in pinned host memory and every scan streams it through two
- * device slots of budget/2 bytes (the copy of one piece overlaps the scan of
- * the previous); results are identical to a resident scan.  Takes effect at
- * the next lhmm_set_database; the budget must hold two of the largest tile. */
+ * larger stays in pinned host memory and every scan streams it through a
+ * ring of 2..8 device slots of ~32 MB (the copy of one piece overlaps the
+ * scans of the previous ones); results are identical to a resident scan.
+ * Takes effect at the next lhmm_set_database; the budget must hold two of
+ * the largest tile. */
 int lhmm_context_set_db_budget(lhmm_context* ctx, uint64_t device_bytes);
 /* *on_device = 1 if the current database is resident in HBM, 0 if streamed. */
 int lhmm_database_resident(lhmm_context* ctx, int* on_device);

@@ -177,8 +177,10 @@ Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64
                               ? vs[vi] : variant;
             if (!find_dispatch(v, alg, 1)) continue;  // FP16X_ALT: MSV only
             const bool x = v == LHMM_VARIANT_FP16X || v == LHMM_VARIANT_FP16X_ALT;
-            if (variant == LHMM_VARIANT_AUTO && x &&
-                ((alg == LHMM_SSV && n_tiles > 0 && n_tiles < 4096) || !allow_relaxed))
+            // relaxed SSV needs a device-resident tile set (rescoring) and a
+            // database large enough to amortise its flag check
+            if (variant == LHMM_VARIANT_AUTO && x && alg == LHMM_SSV &&
+                ((n_tiles > 0 && n_tiles < 4096) || !allow_relaxed))
                 continue;
             const uint32_t cpw = lhmm::cells_per_word(v);
             int n;
@@ -292,9 +294,12 @@ struct lhmm_context {
     // device ring slots (copy of piece k+1 overlaps the scan of piece k)
     uint64_t db_budget = 0;        // device bytes for residue data; 0 = unlimited
     bool host_resident = false;
+    static constexpr int kMaxSlots = 8;
+    static constexpr uint64_t kSlotTarget = 32ull << 20;  // pipelining granularity
     uint64_t slot_bytes = 0;
+    int n_slots = 0;
     DevBuf<uint8_t> d_ring;
-    cudaEvent_t ring_copied[2] = {nullptr, nullptr}, ring_done[2] = {nullptr, nullptr};
+    cudaEvent_t ring_copied[kMaxSlots] = {}, ring_done[kMaxSlots] = {};
 
     // on-device pipeline scratch (survivor compaction)
     struct Pipe {
@@ -335,15 +340,23 @@ int upload_db(lhmm_context* c) {
             const uint64_t e = t + 1 < db.n_tiles ? db.tile_off[t + 1] : db.data_bytes;
             max_tile = std::max(max_tile, e - db.tile_off[t]);
         }
-        c->slot_bytes = c->db_budget / 2 / 512 * 512;
+        // 2..8 slots of ~32 MB (small pieces start the pipeline sooner), never
+        // smaller than the largest tile
+        c->n_slots = int(std::max<uint64_t>(
+            2, std::min<uint64_t>(lhmm_context::kMaxSlots, c->db_budget / lhmm_context::kSlotTarget)));
+        c->slot_bytes = c->db_budget / uint64_t(c->n_slots) / 512 * 512;
+        if (c->slot_bytes < max_tile && c->n_slots > 2) {
+            c->n_slots = 2;
+            c->slot_bytes = c->db_budget / 2 / 512 * 512;
+        }
         if (c->slot_bytes < max_tile)
             return set_error(LHMM_ERR_CONTRACT,
                              "device database budget " + std::to_string(c->db_budget) +
                                  " B is below two of the largest tile (" +
                                  std::to_string(max_tile) + " B)");
         c->d_db.release();
-        if (int rc = c->d_ring.reserve(2 * c->slot_bytes)) return rc;
-        for (int k = 0; k < 2; ++k)
+        if (int rc = c->d_ring.reserve(uint64_t(c->n_slots) * c->slot_bytes)) return rc;
+        for (int k = 0; k < c->n_slots; ++k)
             if (!c->ring_copied[k]) {
                 CUDA_TRY(cudaEventCreateWithFlags(&c->ring_copied[k], cudaEventDisableTiming));
                 CUDA_TRY(cudaEventCreateWithFlags(&c->ring_done[k], cudaEventDisableTiming));
@@ -568,10 +581,11 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         const uint64_t T = db.n_tiles;
         CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
         CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev0, 0));
-        for (int k = 0; k < 2; ++k) CUDA_TRY(cudaEventRecord(c->ring_done[k], c->stream));
+        for (int k = 0; k < c->n_slots; ++k)
+            CUDA_TRY(cudaEventRecord(c->ring_done[k], c->stream));
         uint64_t t0 = 0;
         for (int k = 0; t0 < T; ++k) {
-            const int sl = k & 1;
+            const int sl = k % c->n_slots;
             const uint64_t b0 = db.tile_off[t0];
             uint64_t t1 = t0 + 1;  // one tile always fits (checked at upload)
             while (t1 < T) {
@@ -988,7 +1002,7 @@ int lhmm_context_destroy(lhmm_context* c) {
     if (c->pinned) pinned_free(c->pinned);
     c->d_db.release();
     c->d_ring.release();
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < lhmm_context::kMaxSlots; ++k) {
         if (c->ring_copied[k]) cudaEventDestroy(c->ring_copied[k]);
         if (c->ring_done[k]) cudaEventDestroy(c->ring_done[k]);
     }

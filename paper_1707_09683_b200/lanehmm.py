@@ -294,7 +294,7 @@ class Scanner:
     def set_db_budget(self, device_bytes):
         """Out-of-core mode: databases whose packed image exceeds this many
         device bytes stay in pinned host memory and are streamed through a
-        two-slot device ring on every scan (0 = unlimited)."""
+        ring of device slots on every scan (0 = unlimited)."""
         _check(_native.lib().lhmm_context_set_db_budget(self._ctx, int(device_bytes)))
 
     def database_resident(self):

@@ -380,7 +380,7 @@ def test_two_row_top_group(ora, variant, alg):
 
 def test_out_of_core_database_streams_through_the_ring(ora):
     """lhmm_context_set_db_budget: a database larger than the device budget
-    stays in pinned host memory and is streamed through two ring slots per
+    stays in pinned host memory and is streamed through the device ring per
     scan; scores, pass bits and the pipeline equal the resident scan."""
     rng = P.Rng(0x00C)
     hmm = rng.random_profile(300)
