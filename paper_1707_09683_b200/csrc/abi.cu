@@ -158,7 +158,7 @@ struct Choice {
 // fraction of the persistent grid's warps the database's work items
 // (tiles * L) can occupy.  `want_L` pins the lane count when non-zero.
 Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64_t n_tiles,
-                       int sm_count, bool allow_relaxed = true) {
+                       int sm_count) {
     Choice best;
     // auto considers the measured variants only (calib_b200.inc); the
     // relaxed FP16X also needs a database large enough to amortise its
@@ -177,10 +177,10 @@ Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64
                               ? vs[vi] : variant;
             if (!find_dispatch(v, alg, 1)) continue;  // FP16X_ALT: MSV only
             const bool x = v == LHMM_VARIANT_FP16X || v == LHMM_VARIANT_FP16X_ALT;
-            // relaxed SSV needs a device-resident tile set (rescoring) and a
-            // database large enough to amortise its flag check
-            if (variant == LHMM_VARIANT_AUTO && x && alg == LHMM_SSV &&
-                ((n_tiles > 0 && n_tiles < 4096) || !allow_relaxed))
+            // relaxed SSV needs a database large enough to amortise its flag
+            // check and rescoring launch
+            if (variant == LHMM_VARIANT_AUTO && x && alg == LHMM_SSV && n_tiles > 0 &&
+                n_tiles < 4096)
                 continue;
             const uint32_t cpw = lhmm::cells_per_word(v);
             int n;
@@ -285,8 +285,8 @@ struct lhmm_context {
     DevBuf<uint32_t> d_flag_count;
 
     std::map<std::tuple<int, int, uint32_t, uint32_t, size_t>, int> occupancy;
-    // geometry policy results per (m, alg, variant, want_L, tiles, relaxed ok)
-    std::map<std::tuple<uint32_t, int, int, uint32_t, uint64_t, bool>, std::tuple<int, uint32_t, uint32_t>>
+    // geometry policy results per (m, alg, variant, want_L, tiles)
+    std::map<std::tuple<uint32_t, int, int, uint32_t, uint64_t>, std::tuple<int, uint32_t, uint32_t>>
         choices;
 
     // out-of-core mode: when the packed image exceeds db_budget the database
@@ -404,6 +404,8 @@ struct DbView {
 
 int compact(lhmm_context* c, lhmm_context::Pipe& P, const DbView& src, const uint8_t* sel,
             DbView* out, uint32_t* nsel_out);
+int compact_host(lhmm_context* c, lhmm_context::Pipe& P, const uint8_t* sel, DbView* out,
+                 uint32_t* nsel_out);
 
 int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8_t* d_pass,
             lhmm_scan_stats* st, int segments = 0, const DbView* view = nullptr) {
@@ -420,25 +422,23 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (opt->reorder_mode != 0 && opt->reorder_mode != 1)
         return set_error(LHMM_ERR_CONTRACT, "unknown reorder mode");
     ProfileSlot& pf = c->profiles[c->current];
-    // relaxed FP16X rescoring compacts from device-resident tiles; a
-    // host-resident (streamed) database uses the exact FP16 kernel instead
+    // a host-resident database is streamed through the device ring
     const bool streamed_db = view == nullptr && c->host_resident;
     int variant = opt->variant;
     if (variant == LHMM_VARIANT_FP16X_ALT && opt->alg == LHMM_SSV)
         variant = LHMM_VARIANT_FP16X;  // the ALT code form is MSV-only
-    if (streamed_db && opt->alg == LHMM_SSV && variant == LHMM_VARIANT_FP16X)
-        variant = LHMM_VARIANT_FP16;
+
     uint32_t L = opt->lanes, H = opt->rows;
     if (L != 0 && (L > 32 || (L & (L - 1))))
         return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,32]");
     if (H == 0) {
         Choice ch;
-        const auto ckey = std::make_tuple(pf.m, opt->alg, variant, L, v.n_tiles, !streamed_db);
+        const auto ckey = std::make_tuple(pf.m, opt->alg, variant, L, v.n_tiles);
         const auto cit = c->choices.find(ckey);
         if (cit != c->choices.end()) {
             std::tie(ch.variant, ch.L, ch.H) = cit->second;
         } else {
-            ch = choose_geometry(pf.m, opt->alg, variant, L, v.n_tiles, c->sm_count, !streamed_db);
+            ch = choose_geometry(pf.m, opt->alg, variant, L, v.n_tiles, c->sm_count);
             if (c->choices.size() > 256) c->choices.clear();
             c->choices.emplace(ckey, std::make_tuple(ch.variant, ch.L, ch.H));
         }
@@ -451,8 +451,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     } else {
         if (variant == LHMM_VARIANT_AUTO) variant = LHMM_VARIANT_FP16;
         if (L == 0) {
-            Choice ch = choose_geometry(pf.m, opt->alg, variant, 0, v.n_tiles, c->sm_count,
-                                        !streamed_db);
+            Choice ch = choose_geometry(pf.m, opt->alg, variant, 0, v.n_tiles, c->sm_count);
             L = ch.L ? ch.L : 1;
             if (ch.L) variant = ch.variant;
         } else if (variant == LHMM_VARIANT_FP16X && opt->alg == LHMM_MSV &&
@@ -692,7 +691,17 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         if (nflag) {
             DbView sub;
             uint32_t nsel = 0;
-            if (int rc = compact(c, c->resc, v, c->d_flag.ptr, &sub, &nsel)) return rc;
+            if (streamed_db) {
+                // host-resident database: gather the flagged sequences from
+                // the pinned image (the device only ever held ring slots)
+                std::vector<uint8_t> fl(std::max<uint64_t>(c->db.n_local, 1));
+                CUDA_TRY(cudaMemcpyAsync(fl.data(), c->d_flag.ptr, c->db.n_local,
+                                         cudaMemcpyDeviceToHost, c->stream));
+                CUDA_TRY(cudaStreamSynchronize(c->stream));
+                if (int rc = compact_host(c, c->resc, fl.data(), &sub, &nsel)) return rc;
+            } else if (int rc = compact(c, c->resc, v, c->d_flag.ptr, &sub, &nsel)) {
+                return rc;
+            }
             if (nsel) {
                 lhmm_scan_options ox = *opt;
                 ox.variant = LHMM_VARIANT_FP16;

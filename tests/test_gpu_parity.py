@@ -411,6 +411,19 @@ def test_out_of_core_database_streams_through_the_ring(ora):
         assert pa.msv_rescored == pb.msv_rescored > 0
         np.testing.assert_array_equal(pa.ssv_raw, pb.ssv_raw)
         np.testing.assert_array_equal(pa.msv_raw, pb.msv_raw)
+    # FP16X SSV rescoring on a streamed database (flags gathered on the host)
+    qd = P.QuantParams()
+    dbp = rng.random_records(6000, 100, 600, plant=(hmm, 0.5))
+    cd = P.quantize_emissions(hmm, qd)
+    with P.Scanner(0) as ooc:
+        ooc.set_db_budget(1 << 20)
+        ooc.set_profile(cd, qd, hmm.lambda_, hmm.tau)
+        ooc.set_database(dbp)
+        assert not ooc.database_resident()
+        rep = ooc.scan(P.ScanOptions(alg=P.Algorithm.Ssv, variant=P.Variant.Fp16x))
+        assert rep.stats["recomputed"] > 0
+        np.testing.assert_array_equal(
+            rep.raw, ora.scan_flat(1, cd.bytes, dbp.residues, dbp.offsets, oq(qd)))
     with P.Scanner(0) as tiny:
         tiny.set_db_budget(4096)
         tiny.set_profile(costs, q, hmm.lambda_, hmm.tau)
