@@ -89,7 +89,9 @@ typedef struct lhmm_quant {
 typedef struct lhmm_scan_options {
     int alg;            /* lhmm_alg */
     int variant;        /* lhmm_variant */
-    uint32_t lanes;     /* lanes cooperating on one sequence (1..32, pow2); 0 = auto */
+    uint32_t lanes;     /* lanes cooperating on one sequence (1..32, pow2; 64..512 =
+                           2..16 warps per sequence, the long-model kernel); 0 = auto
+                           (models beyond one warp's capacity go to the long kernel) */
     uint32_t rows;      /* striped rows H per lane; 0 = auto */
     double threshold;   /* pass iff pValue <= threshold || overflow; in [0,1] */
     int fault_injection;/* verification aid: corrupts one lane's E (ScanOptions.faultInjection) */

@@ -96,6 +96,39 @@ DispatchFn find_dispatch(int variant, int alg, uint32_t L) {
     return nullptr;
 }
 
+constexpr uint32_t kMaxLongK = 16;  // warps per sequence of the long-model kernel
+
+DispatchFn find_dispatch_long(int alg, uint32_t K) {
+    for (const auto& e : lhmm::kDispatchLong)
+        if (e.alg == alg && uint32_t(e.warps) == K) return e.fn;
+    return nullptr;
+}
+
+// Long-model geometry: the smallest capacity 2 * 32K * H >= m among the
+// compiled (K, H), fewer warps first at equal capacity.  `L` (in/out) may
+// pin the group width 32K.
+bool choose_long(uint32_t m, uint32_t& L, uint32_t& H) {
+    uint64_t best = ~0ull;
+    uint32_t bl = 0, bh = 0;
+    for (const auto& e : lhmm::kDispatchLong) {
+        if (e.alg != 0) continue;  // same (K, H) grid for both algorithms
+        const uint32_t lanes = 32u * uint32_t(e.warps);
+        if (L && lanes != L) continue;
+        for (int h : lhmm::kRowsLong) {
+            const uint64_t cap = 2ull * lanes * uint64_t(h);
+            if (cap >= m && (cap < best || (cap == best && lanes < bl))) {
+                best = cap;
+                bl = lanes;
+                bh = uint32_t(h);
+            }
+        }
+    }
+    if (!bl) return false;
+    L = bl;
+    H = bh;
+    return true;
+}
+
 bool rows_instantiated(int variant, uint32_t H) {
     int n;
     const int* r = rows_list(variant, &n);
@@ -105,6 +138,20 @@ bool rows_instantiated(int variant, uint32_t H) {
 }
 
 constexpr uint64_t kMaxTableBytes = 200 * 1024;  // leaves room for 1 CTA/SM + static smem
+
+// Largest model the one-warp kernels can hold (FP16 family, table in smem).
+uint32_t max_standard_capacity(int alg) {
+    (void)alg;
+    uint32_t best = 0;
+    int n;
+    const int* rows = rows_list(LHMM_VARIANT_FP16, &n);
+    for (uint32_t L = 1; L <= 32; L *= 2)
+        for (int i = 0; i < n; ++i)
+            if (lhmm::table_bytes_for(LHMM_VARIANT_FP16, L, uint32_t(rows[i]), true) <=
+                kMaxTableBytes)
+                best = std::max(best, 2u * L * uint32_t(rows[i]));
+    return best;
+}
 
 // Replicated (bank-conflict-free) tables when they fit, else one shared copy.
 bool use_replica(int variant, uint32_t L, uint32_t H) {
@@ -429,9 +476,19 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         variant = LHMM_VARIANT_FP16X;  // the ALT code form is MSV-only
 
     uint32_t L = opt->lanes, H = opt->rows;
-    if (L != 0 && (L > 32 || (L & (L - 1))))
-        return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,32]");
-    if (H == 0) {
+    if (L != 0 && (L > 32 * kMaxLongK || (L & (L - 1))))
+        return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,512]");
+    // models beyond one warp (or an explicit lanes > 32): K warps per sequence
+    bool long_model = L > 32;
+    if (!long_model && L == 0 && H == 0 && pf.m > max_standard_capacity(opt->alg))
+        long_model = true;
+    if (long_model) {
+        if (!choose_long(pf.m, L, H)) {
+            return set_error(LHMM_ERR_DATA, "no long-model geometry covers model length " +
+                                                std::to_string(pf.m));
+        }
+        variant = LHMM_VARIANT_FP16;
+    } else if (H == 0) {
         Choice ch;
         const auto ckey = std::make_tuple(pf.m, opt->alg, variant, L, v.n_tiles);
         const auto cit = c->choices.find(ckey);
@@ -460,26 +517,32 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             variant = LHMM_VARIANT_FP16X_ALT;  // the faster code form of this geometry
         }
     }
-    if (L < 1 || L > 32 || (L & (L - 1)))
+    if (!long_model && (L < 1 || L > 32 || (L & (L - 1))))
         return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,32]");
-    if (!rows_instantiated(variant, H))
+    if (!long_model && !rows_instantiated(variant, H))
         return set_error(LHMM_ERR_CONTRACT, "row count " + std::to_string(H) +
                                                 " has no compiled kernel for this variant");
     const uint64_t cap = uint64_t(lhmm::cells_per_word(variant)) * L * H;
     if (cap < pf.m)
         return set_error(LHMM_ERR_DATA, "geometry capacity " + std::to_string(cap) +
                                             " below model length " + std::to_string(pf.m));
-    DispatchFn fn = find_dispatch(variant, opt->alg, L);
+    DispatchFn fn = long_model ? find_dispatch_long(opt->alg, L / 32)
+                               : find_dispatch(variant, opt->alg, L);
     if (!fn) return set_error(LHMM_ERR_CONTRACT, "no kernel for this variant/alg/lanes");
+    // work items: (tile, sub-batch) pairs, or single slots for long models;
+    // the persistent grid holds `units_per_cta` of them per CTA at a time
+    const uint64_t items_per_tile = long_model ? 32 : L;
+    const uint64_t warps_per_cta =
+        long_model ? lhmm::kMaxThreads / 32 / (L / 32) : lhmm::kMaxThreads / 32;
 
     // profile table image (cached per profile and geometry)
-    const bool rep = use_replica(variant, L, H);
+    const bool rep = !long_model && use_replica(variant, L, H);
     auto tkey = std::make_tuple(variant, opt->alg, L, H, rep);
     auto tit = pf.tables.find(tkey);
     if (tit == pf.tables.end()) {
         lhmm::TableImage img;
         lhmm::build_table(pf.costs.data(), pf.m, variant, opt->alg, L, H, rep, pf.q.dbias, img);
-        if (img.words.size() * 4 > kMaxTableBytes + 16 * 1024)
+        if (!long_model && img.words.size() * 4 > kMaxTableBytes + 16 * 1024)
             return set_error(LHMM_ERR_DATA, "profile table does not fit in shared memory");
         ProfileSlot::DevTable t;
         if (int rc = t.buf.reserve(img.words.size())) return rc;
@@ -532,7 +595,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     p.raw_out = d_raw;
     p.pass_out = d_pass;
     p.counter = c->d_counter.ptr;
-    p.n_items = uint32_t(v.n_tiles * L);
+    p.n_items = uint32_t(v.n_tiles * items_per_tile);
     p.table_bytes = uint32_t(table_bytes);
     p.res_stride = tab.res_stride;
     p.copy_stride = tab.copy_stride;
@@ -556,7 +619,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
 
     lhmm::LaunchCfg cfg{};
     cfg.threads = lhmm::kMaxThreads;
-    cfg.smem = table_bytes;
+    cfg.smem = long_model ? 0 : table_bytes;  // long models read the table from global
     cfg.stream = c->stream;
     auto okey = std::make_tuple(variant, opt->alg, L, H, table_bytes);
     auto it = c->occupancy.find(okey);
@@ -568,7 +631,6 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     }
     const int bps = it->second;
     if (bps < 1) return set_error(LHMM_ERR_CUDA, "kernel cannot be resident (smem/registers)");
-    const uint64_t warps_per_cta = lhmm::kMaxThreads / 32;
     const uint64_t need = (uint64_t(p.n_items) + warps_per_cta - 1) / warps_per_cta;
     cfg.grid = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(c->sm_count) * bps, need)));
 
@@ -603,7 +665,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             ps.db = slot;
             ps.db_off = b0;
             ps.tile_base = uint32_t(t0);
-            ps.n_items = uint32_t((t1 - t0) * L);
+            ps.n_items = uint32_t((t1 - t0) * items_per_tile);
             lhmm::LaunchCfg cs = cfg;
             const uint64_t need_s = (uint64_t(ps.n_items) + warps_per_cta - 1) / warps_per_cta;
             cs.grid = int(std::max<uint64_t>(
@@ -663,7 +725,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             CUDA_TRY(cudaStreamWaitEvent(c->stream, c->seg_events[size_t(k)], 0));
             lhmm::KParams ps = p;
             ps.tile_base = uint32_t(t0);
-            ps.n_items = uint32_t((t1 - t0) * L);
+            ps.n_items = uint32_t((t1 - t0) * items_per_tile);
             lhmm::LaunchCfg cs = cfg;
             const uint64_t need_s = (uint64_t(ps.n_items) + warps_per_cta - 1) / warps_per_cta;
             cs.grid = int(std::max<uint64_t>(
@@ -730,7 +792,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         st->launches = launches;
         st->grid = uint32_t(cfg.grid);
         st->threads = uint32_t(cfg.threads);
-        st->smem_bytes = uint32_t(table_bytes);
+        st->smem_bytes = uint32_t(cfg.smem);
         st->recomputed = recomputed;
     }
     return LHMM_OK;

@@ -41,6 +41,7 @@ namespace lhmm {
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kResidueRows = 23;  // codes 0..20, 21 '@', 22 '#'
 constexpr int kPadCode = 22;
+constexpr uint32_t kNoOutIdx = 0xffffffffu;
 #ifndef LHMM_MAX_THREADS
 #define LHMM_MAX_THREADS 512
 #endif
@@ -715,6 +716,124 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// Long models (beyond one warp's register capacity, M > 4352): K warps per
+// sequence.  The group's 32K lanes hold the model striped exactly as one
+// 32K-lane warp would (node (2*l + k)*H + h + 1 for group lane l); the stripe
+// shift crosses warps through shared memory, and for MSV the row maximum is
+// combined across the K warps before B is updated -- one named barrier per
+// residue row.  The table (23 x M x 2 B, up to 2.9 MB) lives in global
+// memory (L2-resident), read with 128-bit read-only loads.  This is the
+// analogue of the reference's S=1 fallback (src/select.cpp:16-48), which has
+// no model-length bound.
+
+__device__ __forceinline__ void group_barrier(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+template <class V, int K, int H>
+__global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel_long(const KParams p) {
+    static_assert(K >= 2 && kMaxThreads / 32 % K == 0 && kMaxThreads / 32 / K <= 15,
+                  "K warps per group, at most 15 groups (named barriers 1..15)");
+    static_assert(H % 4 == 0, "rows are read four at a time");
+    static_assert(!V::kTwoMode && !V::kRelaxed, "exact policies only");
+    constexpr int NG = kMaxThreads / 32 / K;  // groups per CTA
+    constexpr uint32_t LG = 32u * K;          // lanes per group
+    __shared__ uint32_t s_top[NG][2][K], s_e[NG][2][K], s_item[NG];
+
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t grp = warp / K, wig = warp % K;
+    const uint32_t l = wig * 32u + lane;  // lane within the group
+    const uint32_t bar = 1u + grp;
+    const uint32_t P = p.res_stride;
+    const uint32_t* tab_lane = p.table + 4u * l;
+
+    for (;;) {
+        if (wig == 0 && lane == 0) s_item[grp] = atomicAdd(p.counter, 1u);
+        group_barrier(bar, LG);
+        const uint32_t item = s_item[grp];
+        group_barrier(bar, LG);  // s_item is rewritten by the next claim
+        if (item >= p.n_items) break;
+        const uint32_t tile = p.tile_base + item / 32u;
+        const uint32_t slot = item % 32u;
+        const uint32_t sidx = tile * 32u + slot;
+        const uint32_t oi = p.out_idx[sidx];
+        if (oi == kNoOutIdx) continue;
+        const uint32_t len = p.lens[sidx];
+        const uint8_t* src = p.db + (p.tile_off[tile] - p.db_off) + slot * 16u;
+
+        typename V::St st;
+        V::init(st, p.base_tab[len], p);
+        uint32_t g[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) g[h] = V::init_word(st);
+        uint32_t e0 = V::NEG, e1 = V::NEG;
+        uint32_t xin = V::template inject<false>(st);  // previous warp's top word
+        uint4 res4 = make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+        for (uint32_t r = 0; r < len; ++r) {
+            if ((r & 15u) == 0) res4 = ld_stream(src + (r >> 4) * 512u);
+            const uint32_t w4 = (r & 8u) ? ((r & 4u) ? res4.w : res4.z)
+                                         : ((r & 4u) ? res4.y : res4.x);
+            const uint32_t x = (w4 >> (8u * (r & 3u))) & 0xffu;
+            const uint32_t* tp = tab_lane + x * P;
+            const uint32_t top = g[H - 1];
+            uint32_t up = __shfl_sync(kFull, top, (lane + 31u) & 31u);
+            if (lane == 0) up = xin;
+#pragma unroll
+            for (int h4 = H / 4 - 1; h4 >= 0; --h4) {
+                const uint4 c = __ldg(reinterpret_cast<const uint4*>(tp + h4 * 4 * LG));
+                const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+                for (int k = 3; k >= 0; --k) {
+                    const int h = 4 * h4 + k;
+                    const uint32_t in = h == 0 ? V::shift(top, up) : g[h - 1];
+                    g[h] = V::template cell<false>(in, cw[k], st);
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < H; h += 4) {
+                e0 = V::acc2(e0, g[h], g[h + 1]);
+                e1 = V::acc2(e1, g[h + 2], g[h + 3]);
+            }
+            const uint32_t par = r & 1u;
+            if (lane == 31) s_top[grp][par][wig] = g[H - 1];
+            if constexpr (V::kMsv) {
+                const uint32_t ew = V::template group_reduce<32>(V::acc2(e0, e1, e1));
+                if (lane == 0) s_e[grp][par][wig] = ew;
+            }
+            group_barrier(bar, LG);
+            if constexpr (V::kMsv) {
+                uint32_t E = s_e[grp][par][0];
+#pragma unroll
+                for (int k = 1; k < K; ++k) E = V::acc2(E, s_e[grp][par][k], E);
+                V::update_B(st, E);
+                e0 = E;
+            }
+            xin = wig > 0 ? s_top[grp][par][wig - 1]
+                          : (p.wrap ? s_top[grp][par][K - 1] : V::template inject<false>(st));
+        }
+        uint32_t E = V::acc2(e0, e1, e1);
+        if constexpr (!V::kMsv) {
+            // SSV: the group maximum once, at the end
+            const uint32_t ew = V::template group_reduce<32>(E);
+            if (lane == 0) s_e[grp][0][wig] = ew;
+            group_barrier(bar, LG);
+            E = s_e[grp][0][0];
+#pragma unroll
+            for (int k = 1; k < K; ++k) E = V::acc2(E, s_e[grp][0][k], E);
+        }
+        if (wig == 0 && lane == 0) {
+            uint32_t raw = V::raw(E);
+            if (p.fault && raw < 255u) raw += 1u;  // verification aid
+            p.raw_out[oi] = uint8_t(raw);
+            p.pass_out[oi] = uint8_t(raw == 255u || raw >= p.rawmin_tab[len]);
+        }
+        group_barrier(bar, LG);  // s_e / s_top reuse by the next sequence
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host-side launch plumbing, instantiated per (variant, alg, L) translation
 // unit by gen_instances.py
 
@@ -743,6 +862,20 @@ int launch_one(int op, LaunchCfg* c, const KParams* p) {
         return 0;
     }
     k<<<c->grid, c->threads, c->smem, c->stream>>>(*p);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -2;
+}
+
+template <class V, int K, int H>
+int launch_long(int op, LaunchCfg* c, const KParams* p) {
+    auto* k = &scan_kernel_long<V, K, H>;
+    if (op == kOpQuery) {
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, c->threads, 0) != cudaSuccess)
+            return -2;
+        c->blocks_per_sm = n;
+        return 0;
+    }
+    k<<<c->grid, c->threads, 0, c->stream>>>(*p);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -2;
 }
 

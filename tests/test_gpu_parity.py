@@ -429,3 +429,45 @@ def test_out_of_core_database_streams_through_the_ring(ora):
         tiny.set_profile(costs, q, hmm.lambda_, hmm.tau)
         with pytest.raises(P.ContractError, match="largest tile"):
             tiny.set_database(db)
+
+
+@pytest.mark.parametrize("alg", [P.Algorithm.Msv, P.Algorithm.Ssv], ids=lambda a: a.name)
+def test_long_models_beyond_one_warp(ora, alg):
+    """Models above one warp's capacity (M > 4352) run K warps per sequence
+    (scan_kernel_long; the reference's S=1 path has no model-length bound,
+    src/select.cpp:16-48).  Auto geometry and pinned group widths, saturating
+    and non-saturating parameters, against the oracle."""
+    for m, lanes in ((4353, 0), (6001, 0), (9000, 0), (17000, 0), (40000, 0), (700, 64),
+                     (3000, 128), (5000, 256), (9000, 512)):
+        rng = P.Rng(40000 + m + lanes)
+        hmm = rng.random_profile(m)
+        db = rng.random_records(40 if m > 10000 else 70, 1, 300, plant=(hmm, 0.3))
+        for q in (P.QuantParams(), P.QuantParams(3.0, 120, 3, 20, 20)):
+            costs = P.quantize_emissions(hmm, q)
+            rep = scan(costs, q, db, hmm, alg=alg, lanes=lanes, threshold=0.1)
+            want = ora.scan_flat(int(alg), costs.bytes, db.residues, db.offsets, oq(q))
+            assert rep.lanes > 32 and rep.lanes * rep.rows * 2 >= m
+            np.testing.assert_array_equal(rep.raw, want, err_msg=f"m={m} lanes={rep.lanes}")
+            lens = db.lengths()
+            wp = np.array([ora.passes(int(r), int(n), hmm.lambda_, hmm.tau, oq(q), int(alg), 0.1)
+                           for r, n in zip(rep.raw, lens)])
+            np.testing.assert_array_equal(rep.passed, wp)
+
+
+def test_long_model_pipeline_and_dropin_limits(ora):
+    """The filter pipeline and the out-of-core ring also run long models."""
+    rng = P.Rng(777)
+    hmm = rng.random_profile(6000)
+    db = rng.random_records(1500, 1, 200, plant=(hmm, 0.3))
+    q = P.QuantParams()
+    costs = P.quantize_emissions(hmm, q)
+    with P.Scanner(0) as s:
+        s.set_db_budget(1 << 15)
+        s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        s.set_database(db)
+        assert not s.database_resident()
+        rep = s.filter_pipeline(0.05)
+        np.testing.assert_array_equal(
+            rep.ssv_raw, ora.scan_flat(1, costs.bytes, db.residues, db.offsets, oq(q)))
+        want_msv = ora.scan_flat(0, costs.bytes, db.residues, db.offsets, oq(q))
+        np.testing.assert_array_equal(rep.msv_raw[rep.passed], want_msv[rep.passed])
