@@ -183,9 +183,6 @@ struct Dpx16 {
     __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
         return __vimax3_u16x2(E, a, b);
     }
-    __device__ static __forceinline__ uint32_t acc1(uint32_t E, uint32_t a) {
-        return __vmaxu2(E, a);
-    }
     __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
         return __byte_perm(top, up, 0x1076);
     }
@@ -252,9 +249,6 @@ struct Fp16 {
     __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
         return __vimax3_u16x2(E, a, b);
     }
-    __device__ static __forceinline__ uint32_t acc1(uint32_t E, uint32_t a) {
-        return __vmaxu2(E, a);
-    }
     __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
         return __byte_perm(top, up, 0x1076);
     }
@@ -305,9 +299,6 @@ struct Swar8 {
     }
     __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
         return __vmaxu4(__vmaxu4(E, a), b);
-    }
-    __device__ static __forceinline__ uint32_t acc1(uint32_t E, uint32_t a) {
-        return __vmaxu4(E, a);
     }
     __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
         return __byte_perm(top, up, 0x2107);
