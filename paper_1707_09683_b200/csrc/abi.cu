@@ -1,10 +1,12 @@
 // abi.cu -- the C ABI (include/lhmm_b200.h): device context, profile and
 // database residency, geometry policy and the scan launch.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -97,6 +99,7 @@ DispatchFn find_dispatch(int variant, int alg, uint32_t L) {
 }
 
 constexpr uint32_t kMaxLongK = 16;  // warps per sequence of the long-model kernel
+constexpr uint32_t kMaxPieces = 64; // pieces of a streamed scan
 
 DispatchFn find_dispatch_long(int alg, uint32_t K) {
     for (const auto& e : lhmm::kDispatchLong)
@@ -310,6 +313,11 @@ struct lhmm_context {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t copy_stream = nullptr;   // H2D of streamed scans
+    bool stream_mem_ops = false;          // cuStreamWriteValue32 usable (single-launch streaming)
+    // the driver entry point, resolved at run time (no link-time libcuda)
+    CUresult (*write_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+    DevBuf<uint32_t> d_pieces;            // streamed scans: piece ends + ready flags
+    cudaEvent_t ev_side = nullptr;
     std::vector<cudaEvent_t> seg_events;
     int sm_count = 0, sm_clock_khz = 0, cc_major = 0, cc_minor = 0;
 
@@ -687,6 +695,67 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
                                                     cudaGetErrorString(cudaGetLastError()));
             launches = 1;
         }
+    } else if (c->stream_mem_ops) {
+        // single launch: the kernel starts as soon as the per-tile side arrays
+        // are on the device and waits per piece (wait_for_tile) for the
+        // residue bytes, which the copy stream uploads piece by piece, each
+        // followed by a stream memory write of its ready flag -- no per-piece
+        // launches, no per-piece grid tails
+        if (view) return set_error(LHMM_ERR_CONTRACT, "streamed scans need the resident database");
+        auto& db = c->db;
+        const uint64_t T = db.n_tiles;
+        if (int rc = c->d_db.reserve(db.data_bytes)) return rc;
+        if (int rc = c->d_pieces.reserve(2 * kMaxPieces)) return rc;
+        if (!c->ev_side) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
+        std::vector<uint32_t> ends;
+        for (int k = 0, t0 = 0; k < segments && uint64_t(t0) < T; ++k) {
+            const uint64_t goal = db.data_bytes * uint64_t(k + 1) / uint64_t(segments);
+            uint64_t t1 = k + 1 == segments ? T
+                                            : uint64_t(std::lower_bound(db.tile_off.begin(),
+                                                                        db.tile_off.end(), goal) -
+                                                       db.tile_off.begin());
+            t1 = std::max<uint64_t>(t1, uint64_t(t0) + 1);
+            ends.push_back(uint32_t(t1));
+            t0 = int(t1);
+        }
+        ends.back() = uint32_t(T);
+        CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+        CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev0, 0));
+        CUDA_TRY(cudaMemsetAsync(c->d_pieces.ptr + kMaxPieces, 0, kMaxPieces * 4, c->copy_stream));
+        CUDA_TRY(cudaMemcpyAsync(c->d_pieces.ptr, ends.data(), ends.size() * 4,
+                                 cudaMemcpyHostToDevice, c->copy_stream));
+        CUDA_TRY(cudaMemcpyAsync(c->d_tile_off.ptr, db.tile_off.data(), T * sizeof(uint64_t),
+                                 cudaMemcpyHostToDevice, c->copy_stream));
+        CUDA_TRY(cudaMemcpyAsync(c->d_lens.ptr, db.lens.data(), db.lens.size() * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, c->copy_stream));
+        CUDA_TRY(cudaMemcpyAsync(c->d_out_idx.ptr, db.out_idx.data(),
+                                 db.out_idx.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                 c->copy_stream));
+        CUDA_TRY(cudaEventRecord(c->ev_side, c->copy_stream));
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_side, 0));
+        lhmm::KParams ps = p;
+        ps.piece_end = c->d_pieces.ptr;
+        ps.piece_ready = c->d_pieces.ptr + kMaxPieces;
+        ps.n_pieces = uint32_t(ends.size());
+        CUDA_TRY(cudaMemsetAsync(c->d_counter.ptr, 0, sizeof(uint32_t), c->stream));
+        if (p.n_items > 0 && fn(lhmm::kOpLaunch, int(H), &cfg, &ps) != 0)
+            return set_error(LHMM_ERR_CUDA, std::string("kernel launch failed: ") +
+                                                cudaGetErrorString(cudaGetLastError()));
+        launches = p.n_items > 0 ? 1 : 0;
+        uint64_t t0 = 0;
+        for (size_t k = 0; k < ends.size(); ++k) {
+            const uint64_t b0 = db.tile_off[t0];
+            const uint64_t b1 = ends[k] < T ? db.tile_off[ends[k]] : db.data_bytes;
+            CUDA_TRY(cudaMemcpyAsync(c->d_db.ptr + b0, db.data + b0, b1 - b0,
+                                     cudaMemcpyHostToDevice, c->copy_stream));
+            const CUresult cr = c->write_value32(
+                reinterpret_cast<CUstream>(c->copy_stream),
+                reinterpret_cast<CUdeviceptr>(c->d_pieces.ptr + kMaxPieces + k), 1u,
+                CU_STREAM_WRITE_VALUE_DEFAULT);
+            if (cr != CUDA_SUCCESS)
+                return set_error(LHMM_ERR_CUDA, "cuStreamWriteValue32 failed");
+            t0 = ends[k];
+        }
     } else {
         if (view) return set_error(LHMM_ERR_CONTRACT, "streamed scans need the resident database");
         auto& db = c->db;
@@ -1060,6 +1129,26 @@ int lhmm_context_create(int device, lhmm_context** out) {
         return set_error(LHMM_ERR_CUDA, "stream/event creation failed");
     }
     c->stream = c->own_stream;
+    // single-launch streamed scans need stream memory operations; probe once
+    // (LHMM_STREAM_MEM_OPS=0 forces the per-piece launch path)
+    {
+        const char* env = std::getenv("LHMM_STREAM_MEM_OPS");
+        void* fp = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if ((!env || std::atoi(env) != 0) &&
+            cudaGetDriverEntryPoint("cuStreamWriteValue32", &fp, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess && fp) {
+            c->write_value32 = reinterpret_cast<decltype(c->write_value32)>(fp);
+            if (c->d_pieces.reserve(2 * kMaxPieces) == LHMM_OK &&
+                c->write_value32(reinterpret_cast<CUstream>(c->copy_stream),
+                                 reinterpret_cast<CUdeviceptr>(c->d_pieces.ptr), 0u,
+                                 CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS &&
+                cudaStreamSynchronize(c->copy_stream) == cudaSuccess)
+                c->stream_mem_ops = true;
+        }
+        cudaGetLastError();
+    }
     *out = c;
     return LHMM_OK;
 }
@@ -1072,6 +1161,8 @@ int lhmm_context_destroy(lhmm_context* c) {
     lhmm::free_packed(c->db, pinned_free);
     if (c->pinned) pinned_free(c->pinned);
     c->d_db.release();
+    c->d_pieces.release();
+    if (c->ev_side) cudaEventDestroy(c->ev_side);
     c->d_ring.release();
     for (int k = 0; k < lhmm_context::kMaxSlots; ++k) {
         if (c->ring_copied[k]) cudaEventDestroy(c->ring_copied[k]);
@@ -1256,12 +1347,14 @@ int lhmm_scan_streamed(lhmm_context* c, const lhmm_scan_options* opt, int segmen
                        uint8_t* raw, uint8_t* pass, lhmm_scan_stats* st) {
     if (!c) return set_error(LHMM_ERR_CONTRACT, "null context");
     if (!raw || !pass) return set_error(LHMM_ERR_CONTRACT, "null output");
-    if (segments < 1 || segments > 64)
+    if (segments < 1 || segments > int(kMaxPieces))
         return set_error(LHMM_ERR_CONTRACT, "segments must lie in [1,64]");
     DeviceGuard g(c->device);
     if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
-    // pieces of at least 16 MB: smaller ones only add launch/sync overhead
-    const uint64_t max_pieces = std::max<uint64_t>(1, c->db.data_bytes >> 24);
+    // pieces of at least 4 MB with the single-launch path (a piece costs one
+    // copy + one flag write), 16 MB with per-piece launches (each has a tail)
+    const uint64_t max_pieces =
+        std::max<uint64_t>(1, c->db.data_bytes >> (c->stream_mem_ops ? 22 : 24));
     segments = int(std::min<uint64_t>(uint64_t(segments), max_pieces));
     if (int rc = do_scan(c, opt, c->d_raw.ptr, c->d_pass.ptr, st, segments)) return rc;
     const uint64_t n = c->db.n_local;

@@ -61,6 +61,12 @@ struct KParams {
     uint32_t n_items;           // tiles * L
     uint32_t tile_base;         // first tile of this launch (streamed scans)
     uint64_t db_off;            // byte offset of db[0] in the packed image (ring slots)
+    // single-launch streamed scans: the database lands in pieces while the
+    // kernel runs; piece k covers tiles [piece_end[k-1], piece_end[k]) and is
+    // usable once the copy stream has set piece_ready[k] (stream memory op)
+    const uint32_t* piece_end;
+    const uint32_t* piece_ready;
+    uint32_t n_pieces;          // 0: the database is fully resident
     uint32_t table_bytes;       // multiple of 16
     uint32_t res_stride;        // words per residue row (P)
     uint32_t copy_stride;       // words between per-group replicas (0: shared)
@@ -112,6 +118,24 @@ __device__ __forceinline__ void stage_table(uint32_t* smem, const uint32_t* gsrc
             : "r"(b)
             : "memory");
     }
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Streamed scans: block until the piece holding `tile` has landed.  Work is
+// claimed in increasing tile order and pieces land in order, so each warp
+// keeps the tile bound below which everything is known to be resident.
+__device__ __forceinline__ void wait_for_tile(const KParams& p, uint32_t tile,
+                                              uint32_t& ready_below) {
+    if (tile < ready_below) return;
+    uint32_t k = 0;
+    while (k + 1 < p.n_pieces && p.piece_end[k] <= tile) ++k;
+    while (ld_acquire(p.piece_ready + k) == 0) __nanosleep(200);
+    ready_below = p.piece_end[k];
 }
 
 __device__ __forceinline__ uint4 ld_stream(const uint8_t* p) {
@@ -628,6 +652,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
     // gets -inf (normative) or, in the paper's wrap mode, the last lane's top
     const uint32_t shift_src = (lane & ~uint32_t(L - 1)) | ((lane + L - 1) & uint32_t(L - 1));
     const bool inject_here = oig == 0 && !p.wrap;
+    uint32_t ready_below = 0;
 
     for (;;) {
         uint32_t item = 0;
@@ -635,6 +660,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
         item = __shfl_sync(kFull, item, 0);
         if (item >= p.n_items) break;
         const uint32_t tile = p.tile_base + item / L;
+        if (p.n_pieces) wait_for_tile(p, tile, ready_below);  // warp-uniform
         const uint32_t sub = item % L;
         const uint32_t slot = sub * G + grp;
         const uint32_t sidx = tile * 32u + slot;
@@ -739,8 +765,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel_long(const KParams
     const uint32_t P = p.res_stride;
     const uint32_t* tab_lane = p.table + 4u * l;
 
+    uint32_t ready_below = 0;
     for (;;) {
-        if (wig == 0 && lane == 0) s_item[grp] = atomicAdd(p.counter, 1u);
+        if (wig == 0 && lane == 0) {
+            const uint32_t it = atomicAdd(p.counter, 1u);
+            if (p.n_pieces && it < p.n_items) wait_for_tile(p, p.tile_base + it / 32u, ready_below);
+            s_item[grp] = it;
+        }
         group_barrier(bar, LG);
         const uint32_t item = s_item[grp];
         group_barrier(bar, LG);  // s_item is rewritten by the next claim

@@ -199,12 +199,16 @@ def test_multiple_resident_profiles(ora):
             np.testing.assert_array_equal(rep.raw, want)
 
 
-def test_streamed_scan_matches_resident_scan(ora):
-    """lhmm_scan_streamed (H2D in pieces overlapped with per-piece launches)
-    returns exactly the resident scan's scores and pass bits."""
+@pytest.mark.parametrize("mem_ops", ["1", "0"], ids=["single_launch", "per_piece"])
+def test_streamed_scan_matches_resident_scan(ora, mem_ops, monkeypatch):
+    """lhmm_scan_streamed (H2D in pieces overlapped with the scan: one launch
+    waiting on stream-written piece flags, or per-piece launches) returns
+    exactly the resident scan's scores and pass bits, for every variant and
+    the long-model kernel."""
+    monkeypatch.setenv("LHMM_STREAM_MEM_OPS", mem_ops)
     rng = P.Rng(21)
     hmm = rng.random_profile(333)
-    db = rng.lognormal_records(150000, 290, 0.65, 2)  # ~55 MB packed: 3 pieces
+    db = rng.lognormal_records(150000, 290, 0.65, 2)  # ~55 MB packed
     q = P.QuantParams(3.0, 120, 3, 20, 20)
     costs = P.quantize_emissions(hmm, q)
     want = ora.scan_flat(0, costs.bytes, db.residues, db.offsets, oq(q))
@@ -212,12 +216,18 @@ def test_streamed_scan_matches_resident_scan(ora):
         s.set_profile(costs, q, hmm.lambda_, hmm.tau)
         s.set_database(db)
         for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
-            base = s.scan(P.ScanOptions(alg=alg, threshold=0.3))
-            for seg in (1, 3, 8, 64):
-                st = s.scan_streamed(P.ScanOptions(alg=alg, threshold=0.3), seg)
-                np.testing.assert_array_equal(st.raw, base.raw)
-                np.testing.assert_array_equal(st.passed, base.passed)
-                assert 1 <= st.stats["launches"] <= seg
+            for variant, lanes in ((P.Variant.Auto, 0), (P.Variant.Fp16x, 0),
+                                   (P.Variant.Dpx16, 0), (P.Variant.Fp16, 64)):
+                o = P.ScanOptions(alg=alg, threshold=0.3, variant=variant, lanes=lanes)
+                base = s.scan(o)
+                for seg in (1, 3, 8, 64):
+                    st = s.scan_streamed(o, seg)
+                    np.testing.assert_array_equal(st.raw, base.raw)
+                    np.testing.assert_array_equal(st.passed, base.passed)
+                    if mem_ops == "1":
+                        assert st.stats["launches"] == 1
+                    else:
+                        assert 1 <= st.stats["launches"] <= seg
         np.testing.assert_array_equal(s.scan(P.ScanOptions(alg=P.Algorithm.Msv)).raw, want)
 
 
