@@ -488,6 +488,9 @@ def main():
                      "kernel": f"{dom_a} M={dom_m}", "kernel_share_of_step": share,
                      "peak_basis": f"{n_sm} SMs x {sm_max:.0f} MHz x 64 cells/clk/SM "
                                    "(64 INT32 lane-ops/clk/SM x 4 packed u8 cells / 4 ops per cell)",
+                     "binding_resource": "the same 64 cells/clk/SM is the shared-memory bound of "
+                                         "the FP16 kernels (one 128-B table wavefront per 64 cells; "
+                                         "ncu: 95% of peak wavefronts on the C2 dominant kernel)",
                      "hbm": {"bound": "hbm", "achieved": round(hbm_achieved, 1),
                              "peak": hbm_gbs, "unit": "GB/s",
                              "frac": round(hbm_achieved / hbm_gbs, 4)}},
