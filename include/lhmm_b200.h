@@ -205,6 +205,26 @@ int lhmm_scan(lhmm_context* ctx, const lhmm_scan_options* opt, uint8_t* raw_out,
 int lhmm_scan_device(lhmm_context* ctx, const lhmm_scan_options* opt, uint8_t* d_raw,
                      uint8_t* d_pass, lhmm_scan_stats* stats);
 
+/* ---- fused gather (multi-GPU) ----------------------------------
+ * Instead of scanning into local buffers and gathering, every rank's scan
+ * kernel writes its results straight into rank 0's full-length buffers,
+ * addressed by GLOBAL sequence index: rank 0 creates a peer buffer and
+ * exports its CUDA IPC handle (64 bytes), the other ranks map it (NVLink peer
+ * memory on one box), and each calls lhmm_scan_device_global with the mapped
+ * pointers.  After every rank's stream is synchronised and a barrier, rank 0
+ * holds all raw bytes / pass bits.  d_raw_all / d_pass_all span all sequences
+ * of the database given to lhmm_set_database. */
+int lhmm_scan_device_global(lhmm_context* ctx, const lhmm_scan_options* opt, uint8_t* d_raw_all,
+                            uint8_t* d_pass_all, lhmm_scan_stats* stats);
+int lhmm_peer_buffer_create(lhmm_context* ctx, uint64_t bytes, void* ipc_handle /* 64 B out */,
+                            void** dptr);
+int lhmm_peer_buffer_open(lhmm_context* ctx, const void* ipc_handle /* 64 B */, void** dptr);
+/* Unmaps opened and frees created peer buffers (also done by destroy). */
+int lhmm_peer_buffers_release(lhmm_context* ctx);
+/* Small device-memory helpers for callers without a CUDA binding. */
+int lhmm_device_fill(lhmm_context* ctx, void* dptr, uint8_t value, uint64_t bytes);
+int lhmm_device_to_host(lhmm_context* ctx, const void* dptr, void* host, uint64_t bytes);
+
 /* End-to-end scan from the packed HOST image: the database bytes are copied
  * host->device in `segments` byte-balanced pieces on a copy stream while each
  * piece is scanned as soon as it lands (H2D overlapped with the kernels);

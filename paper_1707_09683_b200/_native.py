@@ -84,6 +84,13 @@ SIGNATURES = {
     "lhmm_scan": (C.c_int, [vp, C.POINTER(ScanOptionsC), u8p, u8p, C.POINTER(ScanStatsC)]),
     "lhmm_scan_device": (C.c_int, [vp, C.POINTER(ScanOptionsC), vp, vp,
                                    C.POINTER(ScanStatsC)]),
+    "lhmm_scan_device_global": (C.c_int, [vp, C.POINTER(ScanOptionsC), vp, vp,
+                                          C.POINTER(ScanStatsC)]),
+    "lhmm_peer_buffer_create": (C.c_int, [vp, C.c_uint64, vp, C.POINTER(vp)]),
+    "lhmm_peer_buffer_open": (C.c_int, [vp, vp, C.POINTER(vp)]),
+    "lhmm_peer_buffers_release": (C.c_int, [vp]),
+    "lhmm_device_fill": (C.c_int, [vp, vp, C.c_uint8, C.c_uint64]),
+    "lhmm_device_to_host": (C.c_int, [vp, vp, vp, C.c_uint64]),
     "lhmm_scan_streamed": (C.c_int, [vp, C.POINTER(ScanOptionsC), C.c_int, u8p, u8p,
                                      C.POINTER(ScanStatsC)]),
     "lhmm_filter_pipeline": (C.c_int, [vp, C.c_double, C.c_int, u8p, u8p, u8p, u64p,

@@ -336,6 +336,9 @@ struct lhmm_context {
     DevBuf<uint32_t> d_lens, d_out_idx;
     DevBuf<uint32_t> d_counter;
     DevBuf<uint8_t> d_raw, d_pass;
+    DevBuf<uint32_t> d_out_gidx;   // slot -> GLOBAL sequence index (fused peer gather)
+    uint64_t n_global = 0;         // sequences of the whole (unsharded) database
+    std::vector<void*> peer_own, peer_open;  // exported / mapped peer output buffers
     DevBuf<uint8_t> d_flag;        // FP16X: per-sequence "rescore exactly"
     DevBuf<uint32_t> d_flag_count;
 
@@ -438,6 +441,13 @@ int upload_db(lhmm_context* c) {
         CUDA_TRY(cudaMemcpyAsync(c->d_out_idx.ptr, db.out_idx.data(),
                                  db.out_idx.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
                                  c->stream));
+        // the same slots addressed by global sequence index (fused gather)
+        std::vector<uint32_t> g(db.out_idx.size(), lhmm::kNoOutput);
+        for (size_t i = 0; i < g.size(); ++i)
+            if (db.out_idx[i] != lhmm::kNoOutput) g[i] = uint32_t(db.global_idx[db.out_idx[i]]);
+        if (int rc = c->d_out_gidx.reserve(g.size())) return rc;
+        CUDA_TRY(cudaMemcpyAsync(c->d_out_gidx.ptr, g.data(), g.size() * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, c->stream));
     }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     return LHMM_OK;
@@ -460,14 +470,21 @@ struct DbView {
 int compact(lhmm_context* c, lhmm_context::Pipe& P, const DbView& src, const uint8_t* sel,
             DbView* out, uint32_t* nsel_out);
 int compact_host(lhmm_context* c, lhmm_context::Pipe& P, const uint8_t* sel, DbView* out,
-                 uint32_t* nsel_out);
+                 uint32_t* nsel_out, bool global_out = false);
 
+// global_out: outputs (and FP16X flags) are addressed by GLOBAL sequence
+// index -- d_raw / d_pass span the whole database, typically rank 0's
+// buffers mapped through CUDA IPC (the fused gather).
 int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8_t* d_pass,
-            lhmm_scan_stats* st, int segments = 0, const DbView* view = nullptr) {
+            lhmm_scan_stats* st, int segments = 0, const DbView* view = nullptr,
+            bool global_out = false) {
     if (!c || !opt) return set_error(LHMM_ERR_CONTRACT, "null argument");
     const DbView v = view ? *view
-                          : DbView{c->d_db.ptr, c->d_tile_off.ptr, c->d_lens.ptr, c->d_out_idx.ptr,
+                          : DbView{c->d_db.ptr, c->d_tile_off.ptr, c->d_lens.ptr,
+                                   global_out ? c->d_out_gidx.ptr : c->d_out_idx.ptr,
                                    c->db.n_tiles, c->db.residues, c->db.n_local};
+    if (global_out && segments > 0)
+        return set_error(LHMM_ERR_CONTRACT, "streamed scans write local outputs");
     if (c->current < 0) return set_error(LHMM_ERR_CONTRACT, "no profile set");
     if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
     if (opt->alg != LHMM_MSV && opt->alg != LHMM_SSV)
@@ -613,7 +630,9 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     p.wrap = opt->reorder_mode == 1 ? 1u : 0u;
     const bool relaxed = variant == LHMM_VARIANT_FP16X && opt->alg == LHMM_SSV;
     if (relaxed) {
-        if (int rc = c->d_flag.reserve(std::max<uint64_t>(c->db.n_local, 1))) return rc;
+        if (int rc = c->d_flag.reserve(
+                std::max<uint64_t>(global_out ? c->n_global : c->db.n_local, 1)))
+            return rc;
         if (int rc = c->d_flag_count.reserve(1)) return rc;
         if (!c->evr0) {
             CUDA_TRY(cudaEventCreate(&c->evr0));
@@ -825,11 +844,13 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             if (streamed_db) {
                 // host-resident database: gather the flagged sequences from
                 // the pinned image (the device only ever held ring slots)
-                std::vector<uint8_t> fl(std::max<uint64_t>(c->db.n_local, 1));
-                CUDA_TRY(cudaMemcpyAsync(fl.data(), c->d_flag.ptr, c->db.n_local,
-                                         cudaMemcpyDeviceToHost, c->stream));
+                const uint64_t nf = global_out ? c->n_global : c->db.n_local;
+                std::vector<uint8_t> fl(std::max<uint64_t>(nf, 1));
+                CUDA_TRY(cudaMemcpyAsync(fl.data(), c->d_flag.ptr, nf, cudaMemcpyDeviceToHost,
+                                         c->stream));
                 CUDA_TRY(cudaStreamSynchronize(c->stream));
-                if (int rc = compact_host(c, c->resc, fl.data(), &sub, &nsel)) return rc;
+                if (int rc = compact_host(c, c->resc, fl.data(), &sub, &nsel, global_out))
+                    return rc;
             } else if (int rc = compact(c, c->resc, v, c->d_flag.ptr, &sub, &nsel)) {
                 return rc;
             }
@@ -990,11 +1011,12 @@ int compact(lhmm_context* c, lhmm_context::Pipe& P, const DbView& src, const uin
 // sequences (sel[local index] != 0, already copied to the host) are re-tiled
 // from the pinned image in their sorted order and uploaded into `P`.
 int compact_host(lhmm_context* c, lhmm_context::Pipe& P, const uint8_t* sel, DbView* out,
-                 uint32_t* nsel_out) {
+                 uint32_t* nsel_out, bool global_out) {
     const auto& db = c->db;
+    auto key = [&](uint32_t o) -> uint64_t { return global_out ? db.global_idx[o] : o; };
     std::vector<uint32_t> src;
     for (uint64_t i = 0; i < db.n_tiles * 32; ++i)
-        if (db.out_idx[i] != lhmm::kNoOutput && sel[db.out_idx[i]]) src.push_back(uint32_t(i));
+        if (db.out_idx[i] != lhmm::kNoOutput && sel[key(db.out_idx[i])]) src.push_back(uint32_t(i));
     const uint32_t nsel = uint32_t(src.size());
     *nsel_out = nsel;
     *out = DbView{nullptr, nullptr, nullptr, nullptr, 0, 0, 0};
@@ -1005,7 +1027,7 @@ int compact_host(lhmm_context* c, lhmm_context::Pipe& P, const uint8_t* sel, DbV
     uint64_t residues = 0;
     for (uint32_t j = 0; j < nsel; ++j) {
         lens[j] = db.lens[src[j]];
-        outi[j] = db.out_idx[src[j]];
+        outi[j] = uint32_t(key(db.out_idx[src[j]]));
         residues += lens[j];
     }
     for (uint32_t t = 0; t < ntiles; ++t)
@@ -1160,6 +1182,8 @@ int lhmm_context_destroy(lhmm_context* c) {
     c->db.data = nullptr;  // owned by the pinned cache
     lhmm::free_packed(c->db, pinned_free);
     if (c->pinned) pinned_free(c->pinned);
+    lhmm_peer_buffers_release(c);
+    c->d_out_gidx.release();
     c->d_db.release();
     c->d_pieces.release();
     if (c->ev_side) cudaEventDestroy(c->ev_side);
@@ -1283,6 +1307,9 @@ int lhmm_set_database(lhmm_context* c, const uint8_t* residues, const uint64_t* 
     if (int rc = lhmm::pack_database(residues ? residues : &empty, offsets, nseq, rank, world,
                                      c->db, alloc))
         return rc;
+    if (nseq >= lhmm::kNoOutput)
+        return set_error(LHMM_ERR_DATA, "more than 2^32-1 sequences in one database");
+    c->n_global = nseq;
     if (int rc = upload_db(c)) return rc;
     c->have_db = true;
     ++c->db_gen;
@@ -1325,6 +1352,72 @@ int lhmm_scan_device(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_r
     if (!d_raw || !d_pass) return set_error(LHMM_ERR_CONTRACT, "null output");
     DeviceGuard g(c->device);
     return do_scan(c, opt, d_raw, d_pass, st);
+}
+
+int lhmm_scan_device_global(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw_all,
+                            uint8_t* d_pass_all, lhmm_scan_stats* st) {
+    if (!c) return set_error(LHMM_ERR_CONTRACT, "null context");
+    if (!d_raw_all || !d_pass_all) return set_error(LHMM_ERR_CONTRACT, "null output");
+    DeviceGuard g(c->device);
+    return do_scan(c, opt, d_raw_all, d_pass_all, st, 0, nullptr, true);
+}
+
+int lhmm_peer_buffer_create(lhmm_context* c, uint64_t bytes, void* ipc_handle, void** dptr) {
+    if (!c || !ipc_handle || !dptr) return set_error(LHMM_ERR_CONTRACT, "null argument");
+    DeviceGuard g(c->device);
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<uint64_t>(bytes, 16)) != cudaSuccess)
+        return set_error(LHMM_ERR_NOMEM, "cudaMalloc failed for a peer buffer");
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
+        cudaFree(p);
+        return set_error(LHMM_ERR_CUDA, "cudaIpcGetMemHandle failed");
+    }
+    std::memcpy(ipc_handle, &h, sizeof h);
+    c->peer_own.push_back(p);
+    *dptr = p;
+    return LHMM_OK;
+}
+
+int lhmm_peer_buffer_open(lhmm_context* c, const void* ipc_handle, void** dptr) {
+    if (!c || !ipc_handle || !dptr) return set_error(LHMM_ERR_CONTRACT, "null argument");
+    DeviceGuard g(c->device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handle, sizeof h);
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+        return set_error(LHMM_ERR_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    c->peer_open.push_back(p);
+    *dptr = p;
+    return LHMM_OK;
+}
+
+int lhmm_peer_buffers_release(lhmm_context* c) {
+    if (!c) return set_error(LHMM_ERR_CONTRACT, "null context");
+    DeviceGuard g(c->device);
+    cudaDeviceSynchronize();
+    for (void* p : c->peer_open) cudaIpcCloseMemHandle(p);
+    for (void* p : c->peer_own) cudaFree(p);
+    c->peer_open.clear();
+    c->peer_own.clear();
+    return LHMM_OK;
+}
+
+int lhmm_device_fill(lhmm_context* c, void* dptr, uint8_t value, uint64_t bytes) {
+    if (!c || (!dptr && bytes)) return set_error(LHMM_ERR_CONTRACT, "null argument");
+    DeviceGuard g(c->device);
+    CUDA_TRY(cudaMemsetAsync(dptr, value, bytes, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return LHMM_OK;
+}
+
+int lhmm_device_to_host(lhmm_context* c, const void* dptr, void* host, uint64_t bytes) {
+    if (!c || ((!dptr || !host) && bytes)) return set_error(LHMM_ERR_CONTRACT, "null argument");
+    DeviceGuard g(c->device);
+    CUDA_TRY(cudaMemcpyAsync(host, dptr, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return LHMM_OK;
 }
 
 int lhmm_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* raw, uint8_t* pass,

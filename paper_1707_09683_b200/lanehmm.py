@@ -399,6 +399,42 @@ class Scanner:
                               s2.device_ms * 1e-3, np.flatnonzero(passed[:k]), ssv[:k],
                               passed[:k].astype(bool), msv[:k], s1.as_dict(), s2.as_dict())
 
+    def scan_device_global(self, opt: ScanOptions, raw_ptr: int, pass_ptr: int):
+        """Outputs addressed by GLOBAL sequence index into full-length device
+        buffers -- typically rank 0's, mapped through CUDA IPC (the fused
+        gather, shard.PeerOutputs)."""
+        st = _native.ScanStatsC()
+        oc = opt.c()
+        _check(_native.lib().lhmm_scan_device_global(self._ctx, C.byref(oc), C.c_void_p(raw_ptr),
+                                                     C.c_void_p(pass_ptr), C.byref(st)))
+        return st.as_dict()
+
+    def peer_buffer_create(self, nbytes):
+        """A device buffer whose CUDA IPC handle other processes can map;
+        returns (device pointer, 64-byte handle)."""
+        h = (C.c_uint8 * 64)()
+        ptr = C.c_void_p()
+        _check(_native.lib().lhmm_peer_buffer_create(self._ctx, int(nbytes), h, C.byref(ptr)))
+        return ptr.value, bytes(h)
+
+    def peer_buffer_open(self, handle: bytes):
+        h = (C.c_uint8 * 64).from_buffer_copy(handle)
+        ptr = C.c_void_p()
+        _check(_native.lib().lhmm_peer_buffer_open(self._ctx, h, C.byref(ptr)))
+        return ptr.value
+
+    def peer_buffers_release(self):
+        _check(_native.lib().lhmm_peer_buffers_release(self._ctx))
+
+    def device_fill(self, ptr, value, nbytes):
+        _check(_native.lib().lhmm_device_fill(self._ctx, C.c_void_p(ptr), value, int(nbytes)))
+
+    def device_to_host(self, ptr, nbytes):
+        out = np.zeros(max(int(nbytes), 1), np.uint8)
+        _check(_native.lib().lhmm_device_to_host(self._ctx, C.c_void_p(ptr),
+                                                 out.ctypes.data_as(C.c_void_p), int(nbytes)))
+        return out[:int(nbytes)]
+
     def scan_device(self, opt: ScanOptions, raw_ptr: int, pass_ptr: int):
         """Outputs stay on the device (e.g. torch.uint8 tensors' data_ptr())."""
         st = _native.ScanStatsC()

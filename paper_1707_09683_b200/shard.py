@@ -3,8 +3,13 @@ count (lhmm_set_database's LPT tile plan), per-sequence raw scores and pass
 bits gathered to rank 0.  The path has no reduction -- only this gather
 (BASELINE.json north_star).
 
-Works with any torch.distributed backend: NCCL over NVLink/NVSwitch on the
-GPU box, gloo on CPU for the tests.
+Two gathers:
+* PeerOutputs -- the fused one: rank 0's full-length result buffers are
+  mapped into every rank through CUDA IPC and each rank's scan kernel stores
+  its results there directly (NVLink peer stores), addressed by global
+  sequence index (lhmm_scan_device_global).  No separate collective runs.
+* gather_to_rank0 -- a torch.distributed gather of (index, raw | pass << 8);
+  any backend (NCCL on the box, gloo on CPU for the tests).
 """
 from __future__ import annotations
 
@@ -69,3 +74,46 @@ def shard_plan(offsets, rank, world):
     _check(_native.lib().lhmm_shard_plan(off.ctypes.data_as(_native.u64p), n, rank, world,
                                          out.ctypes.data_as(_native.u64p), C.byref(cnt)))
     return out[:cnt.value]
+
+
+class PeerOutputs:
+    """Rank 0's result buffers for `n_scans` scans of `n_total` sequences,
+    mapped into every rank of `dist` through CUDA IPC (handles exchanged with
+    broadcast_object_list).  raw(k) / passed(k) are device pointers valid on
+    the calling rank; rank 0 reads the results with results(k) after every
+    rank's scans are synchronised and a barrier."""
+
+    def __init__(self, dist, scanner, n_total, n_scans=1):
+        self.dist, self.s, self.n, self.k = dist, scanner, int(n_total), int(n_scans)
+        nbytes = 2 * self.n * self.k
+        if dist.get_rank() == 0:
+            self.base, handle = scanner.peer_buffer_create(nbytes)
+            obj = [handle]
+        else:
+            obj = [None]
+        dist.broadcast_object_list(obj, src=0)
+        if dist.get_rank() != 0:
+            self.base = scanner.peer_buffer_open(obj[0])
+
+    def raw(self, k):
+        return self.base + 2 * self.n * k
+
+    def passed(self, k):
+        return self.base + 2 * self.n * k + self.n
+
+    def mark_unwritten(self):
+        """Rank 0: pass bytes to 2 (scans write 0/1) so coverage is checkable."""
+        if self.dist.get_rank() == 0:
+            self.s.device_fill(self.base, 2, 2 * self.n * self.k)
+
+    def results(self, k):
+        """Rank 0: (raw uint8[n], pass bool[n]) of scan k; raises if some
+        sequence was not written by any rank."""
+        buf = self.s.device_to_host(self.raw(k), 2 * self.n)
+        raw, ps = buf[:self.n], buf[self.n:]
+        if (ps > 1).any():
+            raise RuntimeError("fused gather: %d sequences not written" % int((ps > 1).sum()))
+        return raw, ps.astype(bool)
+
+    def close(self):
+        self.s.peer_buffers_release()
