@@ -233,6 +233,8 @@ def main():
     ap.add_argument("--algs", default="", help="override algorithms: msv, ssv or both")
     ap.add_argument("--backend", default=os.environ.get("LHMM_DIST_BACKEND", "nccl"),
                     help="torch.distributed backend for N>1 (gloo lets ranks share one GPU)")
+    ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1: fused peer-store gather (default) or a torch.distributed gather")
     ap.add_argument("--db-budget", type=int, default=0,
                     help="device bytes for the packed database (0 = resident); larger databases "
                          "are streamed from pinned host memory on every scan")
@@ -308,11 +310,28 @@ def main():
     per_launch = {k: [] for k in range(len(scans))}
     geo = {}
 
+    # N>1: the fused gather -- every rank's scan kernel stores its results in
+    # rank 0's buffers (CUDA IPC / NVLink peer memory) by global index; the
+    # NCCL gather below is the fallback if the mapping is unavailable
+    peer = None
+    if world > 1 and args.gather == "p2p":
+        try:
+            from paper_1707_09683_b200.shard import PeerOutputs
+            peer = PeerOutputs(dist, s, db.count, n_scans=len(scans))
+            peer.mark_unwritten()
+        except Exception as e:  # noqa: BLE001
+            log(f"[bench] fused peer gather unavailable ({e}); using the NCCL gather")
+            peer = None
+    gather_mode = "fused peer stores (CUDA IPC)" if peer else "torch.distributed gather"
+
     def step(record):
         launches = 0
         for k, (pid, m, a) in enumerate(scans):
             s.select_profile(pid)
-            st = s.scan_device(opt_for(a), outs[k][0].data_ptr(), outs[k][1].data_ptr())
+            if peer is not None:
+                st = s.scan_device_global(opt_for(a), peer.raw(k), peer.passed(k))
+            else:
+                st = s.scan_device(opt_for(a), outs[k][0].data_ptr(), outs[k][1].data_ptr())
             launches += st["launches"]
             geo[k] = (st["lanes"], st["rows"], st["variant"], st["grid"], st["smem_bytes"],
                       st["recomputed"])
@@ -324,8 +343,19 @@ def main():
 
     def gather_results():
         """Per-sequence raw + pass bytes of every scan to rank 0 (one gather per
-        scan; NCCL over NVLink on the box, gloo when ranks share a GPU)."""
+        scan; NCCL over NVLink on the box, gloo when ranks share a GPU).  With
+        the fused gather the scans already wrote them; the first call checks
+        that every sequence of every scan arrived."""
         if world == 1:
+            return
+        if peer is not None:
+            if not gathered["validated"]:
+                torch.cuda.synchronize()
+                dist.barrier()
+                if rank == 0:
+                    for k in range(len(scans)):
+                        peer.results(k)  # raises on an unwritten sequence
+                gathered["validated"] = True
             return
         from paper_1707_09683_b200.shard import gather_to_rank0
         gi = gidx.to(comm_dev)
@@ -469,7 +499,8 @@ def main():
         "config": {"workload": desc, "models": list(models_m), "algorithms": algs,
                    "sequences": int(db.count), "residues": int(db.total_residues()),
                    "threshold": threshold, "quant": "QuantParams{3.0,195,3,3,3}",
-                   "parallelism": f"shard{world} by residue count, raw+pass gathered to rank 0",
+                   "parallelism": f"shard{world} by residue count, raw+pass gathered to rank 0"
+                                  + (f" ({gather_mode})" if world > 1 else ""),
                    "l2": ("inputs larger than L2 (packed database "
                           f"{dbstats['packed_bytes'] / 1e6:.0f} MB per GPU > 126 MB)"
                           if flush is None else
