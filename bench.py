@@ -317,7 +317,7 @@ def main():
     if world > 1 and args.gather == "p2p":
         try:
             from paper_1707_09683_b200.shard import PeerOutputs
-            peer = PeerOutputs(dist, s, db.count, n_scans=len(scans))
+            peer = PeerOutputs(dist, s, db.count, n_scans=len(scans), comm_device=comm_dev)
             peer.mark_unwritten()
         except Exception as e:  # noqa: BLE001
             log(f"[bench] fused peer gather unavailable ({e}); using the NCCL gather")

@@ -83,17 +83,35 @@ class PeerOutputs:
     the calling rank; rank 0 reads the results with results(k) after every
     rank's scans are synchronised and a barrier."""
 
-    def __init__(self, dist, scanner, n_total, n_scans=1):
+    def __init__(self, dist, scanner, n_total, n_scans=1, comm_device=None):
+        """Collective over `dist`: either every rank maps the buffers or every
+        rank raises (no rank is left half-configured)."""
+        import torch
         self.dist, self.s, self.n, self.k = dist, scanner, int(n_total), int(n_scans)
         nbytes = 2 * self.n * self.k
+        self.base, err = None, None
+        obj = [None]
         if dist.get_rank() == 0:
-            self.base, handle = scanner.peer_buffer_create(nbytes)
-            obj = [handle]
-        else:
-            obj = [None]
+            try:
+                self.base, handle = scanner.peer_buffer_create(nbytes)
+                obj = [handle]
+            except Exception as e:  # noqa: BLE001
+                err = e
         dist.broadcast_object_list(obj, src=0)
         if dist.get_rank() != 0:
-            self.base = scanner.peer_buffer_open(obj[0])
+            if obj[0] is None:
+                err = RuntimeError("rank 0 could not export its result buffers")
+            else:
+                try:
+                    self.base = scanner.peer_buffer_open(obj[0])
+                except Exception as e:  # noqa: BLE001
+                    err = e
+        dev = comm_device if comm_device is not None else torch.device("cpu")
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            scanner.peer_buffers_release()
+            raise RuntimeError(f"fused gather unavailable on some rank ({err or 'peer failure'})")
 
     def raw(self, k):
         return self.base + 2 * self.n * k

@@ -41,7 +41,7 @@ def _worker(rank, world, port, result_path):
         with P.Scanner(0) as s:
             s.set_profile(costs, q, hmm.lambda_, hmm.tau)
             s.set_database(db, rank, world)
-            out = PeerOutputs(dist, s, db.count, n_scans=2)
+            out = PeerOutputs(dist, s, db.count, n_scans=2)  # gloo: CPU agreement
             out.mark_unwritten()
             dist.barrier()
             for k, (alg, var) in enumerate(((P.Algorithm.Msv, P.Variant.Auto),
