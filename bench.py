@@ -181,8 +181,26 @@ def cpu_reference_gcups(P, db, models, algs, q, sample_n, reps=1):
             f"{'+'.join(algs)}; lanehmm::scan_database with reference geometry, "
             f"{cores} threads, host CPU '{cpu_model()}'" if kind == "reference" else
             f"fixed-stride sample of {sample.count} sequences, C oracle port on {cores} threads")
+    # the other two CPU figures SURVEY §8(d) lists: the scalar oracle
+    # (oracle/oracle.c, the restatement of scalar_msv / scalar_ssv) on all
+    # host threads and on one core, on smaller samples
+    also = {}
+    ora = oracle.Oracle()
+    for label, n_s, thr in (("scalar_oracle_all_threads", 2000, cores),
+                            ("scalar_oracle_1_core", 200, 1)):
+        sub = db.subset(np.arange(0, db.count, max(1, db.count // n_s))[:n_s])
+        cells, secs = 0, 0.0
+        for hmm, costs in models:
+            for a in algs:
+                t0 = time.perf_counter()
+                ora.scan_flat(0 if a == "msv" else 1, costs.bytes, sub.residues, sub.offsets, oq,
+                              thr)
+                secs += time.perf_counter() - t0
+                cells += sub.total_residues() * hmm.length
+        also[label] = {"value": round(cells / secs / 1e9, 3), "threads": thr,
+                       "sample_sequences": int(sub.count)}
     return {"value": round(best, 3), "unit": "GCUPS", "cores": cores, "kind": kind,
-            "sample": desc}
+            "sample": desc, "also": also}
 
 
 def run_reference(args, wl):
