@@ -338,7 +338,8 @@ def wrap_model(alg, costs, m, seq, q, base):
     return E
 
 
-@pytest.mark.parametrize("variant", [P.Variant.Fp16, P.Variant.Dpx16, P.Variant.Swar8],
+@pytest.mark.parametrize("variant", [P.Variant.Fp16, P.Variant.Dpx16, P.Variant.Swar8,
+                                     P.Variant.Fp16x, P.Variant.Fp16xAlt],
                          ids=lambda v: v.name)
 @pytest.mark.parametrize("alg", [P.Algorithm.Msv, P.Algorithm.Ssv], ids=lambda a: a.name)
 def test_paper_wrap_mode(ora, variant, alg):
