@@ -514,12 +514,24 @@ __host__ __device__ constexpr bool fp_word(int k, bool full) {
 // One chunk of RPI residue rows (fully unrolled).  Returns true when the
 // sub-batch's rows ended inside the chunk.  LAZY (two-mode MSV only): the
 // cells hold max(v, B) and B is constant -- see Fp16Sat.
-template <class V, int L, int H, int RPI, bool LAZY>
+__device__ __forceinline__ void group_barrier(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Long models (K > 1, see scan_kernel_long): the K warps of a group hold
+// one sequence (TL = 32K table lanes); lane 0 of each warp takes its stripe
+// shift input from *xin (the previous warp's top word, exchanged through
+// shared memory `xch` = [2 parities][2: top, row max][K] after every row,
+// with one named barrier), and MSV combines the row max across the warps.
+template <class V, int L, int H, int RPI, bool LAZY, int K = 1, int TL = L>
 __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32_t& e1,
                                           uint32_t& e2, uint32_t& e3, typename V::St& st,
                                           const KParams& p, const uint8_t* src, uint32_t r0,
                                           uint32_t rows, const uint32_t* tab_lane, uint32_t P,
-                                          int part_off, uint32_t shift_src, bool inject_here) {
+                                          int part_off, uint32_t shift_src, bool inject_here,
+                                          uint32_t* xch = nullptr, uint32_t wig = 0,
+                                          uint32_t bar = 0, uint32_t* xin = nullptr) {
+    static_assert(K == 1 || (L == 32 && !LAZY), "multi-warp groups use whole warps, exact mode");
     uint32_t wds[RPI / 4];
     const uint8_t* chunk = src + (r0 >> 4) * 512u;
     if constexpr (RPI == 16) {
@@ -546,7 +558,10 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
             // the register holding cell H-1 becomes cell 0 (stripe shift)
             const int stop = ((H - 1 - r) % H + H) % H;
             uint32_t up;
-            if constexpr (L > 1) {
+            if constexpr (K > 1) {
+                up = __shfl_sync(kFull, g[stop], shift_src);
+                if ((threadIdx.x & 31u) == 0) up = *xin;
+            } else if constexpr (L > 1) {
                 up = __shfl_sync(kFull, g[stop], shift_src);
                 if (inject_here) up = V::template inject<LAZY>(st);
             } else {
@@ -559,14 +574,14 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                 const bool full = 4 * h4 + 4 <= H;  // compile-time after unrolling
                 uint32_t cw[4];
                 if (full) {
-                    const uint4 c = *reinterpret_cast<const uint4*>(tp + h4 * 4 * L);
+                    const uint4 c = *reinterpret_cast<const uint4*>(tp + h4 * 4 * TL);
                     cw[0] = c.x;
                     cw[1] = c.y;
                     cw[2] = c.z;
                     cw[3] = c.w;
                 } else {
                     // two-row top group: densely packed pairs (build_table)
-                    const uint2 c = *reinterpret_cast<const uint2*>(tp + part_off + h4 * 4 * L);
+                    const uint2 c = *reinterpret_cast<const uint2*>(tp + part_off + h4 * 4 * TL);
                     cw[0] = c.x;
                     cw[1] = c.y;
                     cw[2] = cw[3] = 0u;
@@ -611,7 +626,30 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                     if (h + 6 < H) e3 = V::acc2(e3, g[h + 6], g[h + 7]);
                 }
             }
-            if constexpr (V::kMsv && !LAZY) {
+            if constexpr (K > 1) {
+                // cross-warp exchange: this row's top word (cell H-1, the
+                // next row's shift input) and, for MSV, the warp's row max
+                const uint32_t lane = threadIdx.x & 31u;
+                const uint32_t par = (r0 + uint32_t(r)) & 1u;
+                uint32_t* xt = xch + par * 2u * K;
+                const int stop_next = ((H - 2 - r) % H + H) % H;
+                if (lane == 31u) xt[wig] = g[stop_next];
+                if constexpr (V::kMsv) {
+                    const uint32_t ew =
+                        V::template group_reduce<32>(V::acc2(V::acc2(e0, e1, e2), e3, e3));
+                    if (lane == 0u) xt[K + wig] = ew;
+                }
+                group_barrier(bar, 32u * K);
+                if constexpr (V::kMsv) {
+                    uint32_t E = xt[K];
+#pragma unroll
+                    for (int k = 1; k < K; ++k) E = V::acc2(E, xt[K + k], E);
+                    e0 = E;
+                    V::update_B(st, E);
+                }
+                *xin = wig > 0 ? xt[wig - 1]
+                               : (p.wrap ? xt[K - 1] : V::template inject<false>(st));
+            } else if constexpr (V::kMsv && !LAZY) {
                 const uint32_t E =
                     V::template group_reduce<L>(V::acc2(V::acc2(e0, e1, e2), e3, e3));
                 e0 = E;
@@ -743,10 +781,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
 // analogue of the reference's S=1 fallback (src/select.cpp:16-48), which has
 // no model-length bound.
 
-__device__ __forceinline__ void group_barrier(uint32_t id, uint32_t threads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
 template <class V, int K, int H>
 __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel_long(const KParams p) {
     static_assert(K >= 2 && kMaxThreads / 32 % K == 0 && kMaxThreads / 32 / K <= 15,
@@ -755,7 +789,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel_long(const KParams
     static_assert(!V::kTwoMode && !V::kRelaxed, "exact policies only");
     constexpr int NG = kMaxThreads / 32 / K;  // groups per CTA
     constexpr uint32_t LG = 32u * K;          // lanes per group
-    __shared__ uint32_t s_top[NG][2][K], s_e[NG][2][K], s_item[NG];
+    __shared__ uint32_t s_x[NG][2 * 2 * K], s_e[NG][2][K], s_item[NG];
 
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
@@ -764,6 +798,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel_long(const KParams
     const uint32_t bar = 1u + grp;
     const uint32_t P = p.res_stride;
     const uint32_t* tab_lane = p.table + 4u * l;
+    const uint32_t shift_src = (lane + 31u) & 31u;
 
     uint32_t ready_below = 0;
     for (;;) {
@@ -789,52 +824,19 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel_long(const KParams
         uint32_t g[H];
 #pragma unroll
         for (int h = 0; h < H; ++h) g[h] = V::init_word(st);
-        uint32_t e0 = V::NEG, e1 = V::NEG;
-        uint32_t xin = V::template inject<false>(st);  // previous warp's top word
-        uint4 res4 = make_uint4(0, 0, 0, 0);
+        uint32_t e0 = V::NEG, e1 = V::NEG, e2 = V::NEG, e3 = V::NEG;
+        // lane 0's shift input for the first row: -inf (or, wrapping, the
+        // last warp's top word, which is -inf as well before any row)
+        uint32_t xin = V::template inject<false>(st);
+        constexpr int RPI = rows_per_iter<V, H>();
+        bool done = false;
 #pragma unroll 1
-        for (uint32_t r = 0; r < len; ++r) {
-            if ((r & 15u) == 0) res4 = ld_stream(src + (r >> 4) * 512u);
-            const uint32_t w4 = (r & 8u) ? ((r & 4u) ? res4.w : res4.z)
-                                         : ((r & 4u) ? res4.y : res4.x);
-            const uint32_t x = (w4 >> (8u * (r & 3u))) & 0xffu;
-            const uint32_t* tp = tab_lane + x * P;
-            const uint32_t top = g[H - 1];
-            uint32_t up = __shfl_sync(kFull, top, (lane + 31u) & 31u);
-            if (lane == 0) up = xin;
-#pragma unroll
-            for (int h4 = H / 4 - 1; h4 >= 0; --h4) {
-                const uint4 c = __ldg(reinterpret_cast<const uint4*>(tp + h4 * 4 * LG));
-                const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-                for (int k = 3; k >= 0; --k) {
-                    const int h = 4 * h4 + k;
-                    const uint32_t in = h == 0 ? V::shift(top, up) : g[h - 1];
-                    g[h] = V::template cell<false>(in, cw[k], st);
-                }
-            }
-#pragma unroll
-            for (int h = 0; h < H; h += 4) {
-                e0 = V::acc2(e0, g[h], g[h + 1]);
-                e1 = V::acc2(e1, g[h + 2], g[h + 3]);
-            }
-            const uint32_t par = r & 1u;
-            if (lane == 31) s_top[grp][par][wig] = g[H - 1];
-            if constexpr (V::kMsv) {
-                const uint32_t ew = V::template group_reduce<32>(V::acc2(e0, e1, e1));
-                if (lane == 0) s_e[grp][par][wig] = ew;
-            }
-            group_barrier(bar, LG);
-            if constexpr (V::kMsv) {
-                uint32_t E = s_e[grp][par][0];
-#pragma unroll
-                for (int k = 1; k < K; ++k) E = V::acc2(E, s_e[grp][par][k], E);
-                V::update_B(st, E);
-                e0 = E;
-            }
-            xin = wig > 0 ? s_top[grp][par][wig - 1]
-                          : (p.wrap ? s_top[grp][par][K - 1] : V::template inject<false>(st));
-        }
+        for (uint32_t r0 = 0; r0 < len && !done; r0 += RPI)
+            done = run_chunk<V, 32, H, RPI, false, K, 32 * K>(
+                g, e0, e1, e2, e3, st, p, src, r0, len, tab_lane, P, 0, shift_src, false,
+                &s_x[grp][0], wig, bar, &xin);
+        e0 = V::acc2(e0, e1, e2);
+        e1 = e3;
         uint32_t E = V::acc2(e0, e1, e1);
         if constexpr (!V::kMsv) {
             // SSV: the group maximum once, at the end
@@ -851,7 +853,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel_long(const KParams
             p.raw_out[oi] = uint8_t(raw);
             p.pass_out[oi] = uint8_t(raw == 255u || raw >= p.rawmin_tab[len]);
         }
-        group_barrier(bar, LG);  // s_e / s_top reuse by the next sequence
+        group_barrier(bar, LG);  // s_e / s_x reuse by the next sequence
     }
 }
 
