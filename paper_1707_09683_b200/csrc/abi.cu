@@ -208,7 +208,7 @@ struct Choice {
 // fraction of the persistent grid's warps the database's work items
 // (tiles * L) can occupy.  `want_L` pins the lane count when non-zero.
 Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64_t n_tiles,
-                       int sm_count) {
+                       int sm_count, bool two_mode_ok = true) {
     Choice best;
     // auto considers the measured variants only (calib_b200.inc); the
     // relaxed FP16X also needs a database large enough to amortise its
@@ -232,6 +232,8 @@ Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64
             if (variant == LHMM_VARIANT_AUTO && x && alg == LHMM_SSV && n_tiles > 0 &&
                 n_tiles < 4096)
                 continue;
+            // MSV: the two-mode kernel's table rates assume saturating scores
+            if (variant == LHMM_VARIANT_AUTO && x && alg == LHMM_MSV && !two_mode_ok) continue;
             const uint32_t cpw = lhmm::cells_per_word(v);
             int n;
             const int* rows = rows_list(v, &n);
@@ -296,6 +298,11 @@ struct ProfileSlot {
         DevBuf<uint8_t> base, rawmin;
     };
     std::map<std::tuple<int, double, uint64_t>, LenTables> lens;
+    // MSV saturation feedback for the geometry policy: the fraction of this
+    // profile's scores that saturated on database generation sat_gen (the
+    // two-mode FP16X kernel only pays off when most warps saturate)
+    double sat_frac = -1.0;
+    uint64_t sat_gen = 0;
     void release() {
         for (auto& kv : tables) kv.second.buf.release();
         for (auto& kv : lens) {
@@ -335,6 +342,7 @@ struct lhmm_context {
     DevBuf<uint64_t> d_tile_off;
     DevBuf<uint32_t> d_lens, d_out_idx;
     DevBuf<uint32_t> d_counter;
+    DevBuf<uint32_t> d_sat;        // MSV saturated-score count of the last scan
     DevBuf<uint8_t> d_raw, d_pass;
     DevBuf<uint32_t> d_out_gidx;   // slot -> GLOBAL sequence index (fused peer gather)
     uint64_t n_global = 0;         // sequences of the whole (unsharded) database
@@ -515,12 +523,18 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         variant = LHMM_VARIANT_FP16;
     } else if (H == 0) {
         Choice ch;
-        const auto ckey = std::make_tuple(pf.m, opt->alg, variant, L, v.n_tiles);
+        // after one MSV scan of this profile over this database we know
+        // whether its scores saturate; mostly non-saturating inputs keep the
+        // exact-mode code, where the one-body FP16 kernel is faster
+        const bool two_mode_ok = !(view == nullptr && pf.sat_gen == c->db_gen &&
+                                   pf.sat_frac >= 0.0 && pf.sat_frac < 0.5);
+        const auto ckey =
+            std::make_tuple(pf.m, opt->alg, variant, L, v.n_tiles + (two_mode_ok ? 0 : (1ull << 62)));
         const auto cit = c->choices.find(ckey);
         if (cit != c->choices.end()) {
             std::tie(ch.variant, ch.L, ch.H) = cit->second;
         } else {
-            ch = choose_geometry(pf.m, opt->alg, variant, L, v.n_tiles, c->sm_count);
+            ch = choose_geometry(pf.m, opt->alg, variant, L, v.n_tiles, c->sm_count, two_mode_ok);
             if (c->choices.size() > 256) c->choices.clear();
             c->choices.emplace(ckey, std::make_tuple(ch.variant, ch.L, ch.H));
         }
@@ -627,6 +641,12 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     p.dbias = pf.q.dbias;
     p.tecjb = uint32_t(pf.q.tec) + uint32_t(pf.q.tjb);
     p.fault = opt->fault_injection ? 1u : 0u;
+    const bool track_sat = opt->alg == LHMM_MSV && view == nullptr;
+    if (track_sat) {
+        if (int rc = c->d_sat.reserve(1)) return rc;
+        CUDA_TRY(cudaMemsetAsync(c->d_sat.ptr, 0, 4, c->stream));
+        p.sat_count = c->d_sat.ptr;
+    }
     p.wrap = opt->reorder_mode == 1 ? 1u : 0u;
     const bool relaxed = variant == LHMM_VARIANT_FP16X && opt->alg == LHMM_SSV;
     if (relaxed) {
@@ -830,6 +850,12 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     CUDA_TRY(cudaEventSynchronize(c->ev1));
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    if (track_sat && v.sequences > 0) {
+        uint32_t nsat = 0;
+        CUDA_TRY(cudaMemcpy(&nsat, c->d_sat.ptr, 4, cudaMemcpyDeviceToHost));
+        pf.sat_frac = double(nsat) / double(v.sequences);
+        pf.sat_gen = c->db_gen;
+    }
     uint32_t recomputed = 0;
     if (relaxed) {
         // rescore the flagged sequences with the exact kernel; the reported
@@ -1203,6 +1229,7 @@ int lhmm_context_destroy(lhmm_context* c) {
     if (c->evr0) cudaEventDestroy(c->evr0);
     if (c->evr1) cudaEventDestroy(c->evr1);
     c->d_counter.release();
+    c->d_sat.release();
     c->d_raw.release();
     c->d_pass.release();
     cudaEventDestroy(c->ev0);

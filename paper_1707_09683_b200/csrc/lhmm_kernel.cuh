@@ -76,6 +76,7 @@ struct KParams {
     uint32_t wrap;              // paper-literal stripe wrap instead of -inf injection
     uint8_t* flag_out;          // relaxed variants: 1 = rescore exactly
     uint32_t* flag_count;       // relaxed variants: number of flagged sequences
+    uint32_t* sat_count;        // MSV: sequences whose score saturated (policy feedback)
 };
 
 // ---------------------------------------------------------------------------
@@ -762,6 +763,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
         if (oig == 0 && oi != 0xffffffffu) {
             p.raw_out[oi] = uint8_t(raw);
             p.pass_out[oi] = uint8_t(raw == 255u || raw >= p.rawmin_tab[len]);
+            if (V::kMsv && p.sat_count && raw == 255u) atomicAdd(p.sat_count, 1u);
             if constexpr (V::kRelaxed) {
                 p.flag_out[oi] = exact_needed ? 1u : 0u;
                 if (exact_needed) atomicAdd(p.flag_count, 1u);
@@ -852,6 +854,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel_long(const KParams
             if (p.fault && raw < 255u) raw += 1u;  // verification aid
             p.raw_out[oi] = uint8_t(raw);
             p.pass_out[oi] = uint8_t(raw == 255u || raw >= p.rawmin_tab[len]);
+            if (V::kMsv && p.sat_count && raw == 255u) atomicAdd(p.sat_count, 1u);
         }
         group_barrier(bar, LG);  // s_e / s_x reuse by the next sequence
     }
