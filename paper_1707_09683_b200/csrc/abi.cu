@@ -232,8 +232,9 @@ Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64
             if (variant == LHMM_VARIANT_AUTO && x && alg == LHMM_SSV && n_tiles > 0 &&
                 n_tiles < 4096)
                 continue;
-            // MSV: the two-mode kernel's table rates assume saturating scores
-            if (variant == LHMM_VARIANT_AUTO && x && alg == LHMM_MSV && !two_mode_ok) continue;
+            // MSV: the two-mode kernel's table rates assume saturating scores;
+            // SSV: the relaxed kernel's, that few sequences need rescoring
+            if (variant == LHMM_VARIANT_AUTO && x && !two_mode_ok) continue;
             const uint32_t cpw = lhmm::cells_per_word(v);
             int n;
             const int* rows = rows_list(v, &n);
@@ -303,6 +304,9 @@ struct ProfileSlot {
     // two-mode FP16X kernel only pays off when most warps saturate)
     double sat_frac = -1.0;
     uint64_t sat_gen = 0;
+    // SSV: fraction of sequences the relaxed FP16X kernel had to rescore
+    double flag_frac = -1.0;
+    uint64_t flag_gen = 0;
     void release() {
         for (auto& kv : tables) kv.second.buf.release();
         for (auto& kv : lens) {
@@ -526,8 +530,11 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         // after one MSV scan of this profile over this database we know
         // whether its scores saturate; mostly non-saturating inputs keep the
         // exact-mode code, where the one-body FP16 kernel is faster
-        const bool two_mode_ok = !(view == nullptr && pf.sat_gen == c->db_gen &&
-                                   pf.sat_frac >= 0.0 && pf.sat_frac < 0.5);
+        const bool two_mode_ok =
+            opt->alg == LHMM_MSV
+                ? !(view == nullptr && pf.sat_gen == c->db_gen && pf.sat_frac >= 0.0 &&
+                    pf.sat_frac < 0.5)
+                : !(view == nullptr && pf.flag_gen == c->db_gen && pf.flag_frac > 0.2);
         const auto ckey =
             std::make_tuple(pf.m, opt->alg, variant, L, v.n_tiles + (two_mode_ok ? 0 : (1ull << 62)));
         const auto cit = c->choices.find(ckey);
@@ -890,6 +897,10 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
                 launches += sx.launches;
             }
             recomputed = nsel;
+        }
+        if (view == nullptr && v.sequences > 0) {
+            pf.flag_frac = double(nflag) / double(v.sequences);
+            pf.flag_gen = c->db_gen;
         }
         CUDA_TRY(cudaEventRecord(c->evr1, c->stream));
         CUDA_TRY(cudaEventSynchronize(c->evr1));
