@@ -482,3 +482,34 @@ def test_long_model_pipeline_and_dropin_limits(ora):
             rep.ssv_raw, ora.scan_flat(1, costs.bytes, db.residues, db.offsets, oq(q)))
         want_msv = ora.scan_flat(0, costs.bytes, db.residues, db.offsets, oq(q))
         np.testing.assert_array_equal(rep.msv_raw[rep.passed], want_msv[rep.passed])
+
+
+def test_policy_feedback_from_saturation_and_rescoring(ora):
+    """The auto policy learns from the first scan of a profile/database pair:
+    MSV keeps the one-body FP16 kernel when scores mostly do not saturate,
+    SSV drops the relaxed FP16X kernel when it had to rescore > 20%; results
+    stay exact either way."""
+    rng = P.Rng(0xFEED)
+    hmm = rng.random_profile(400)
+    db = rng.lognormal_records(150000, 290, 0.65, 2)
+    for q, msv_two_mode in ((P.QuantParams(), True), (P.QuantParams(3.0, 120, 3, 20, 20), False)):
+        costs = P.quantize_emissions(hmm, q)
+        with P.Scanner(0) as s:
+            s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+            s.set_database(db)
+            first = s.scan(P.ScanOptions(alg=P.Algorithm.Msv))
+            second = s.scan(P.ScanOptions(alg=P.Algorithm.Msv))
+            np.testing.assert_array_equal(first.raw, second.raw)
+            two_mode = second.variant in (int(P.Variant.Fp16x), int(P.Variant.Fp16xAlt))
+            assert two_mode == msv_two_mode, (q, second.variant)
+    planted = rng.lognormal_records(150000, 290, 0.65, 2, plant=(hmm, 0.9))
+    q = P.QuantParams()
+    costs = P.quantize_emissions(hmm, q)
+    with P.Scanner(0) as s:
+        s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        s.set_database(planted)
+        first = s.scan(P.ScanOptions(alg=P.Algorithm.Ssv))
+        second = s.scan(P.ScanOptions(alg=P.Algorithm.Ssv))
+        np.testing.assert_array_equal(first.raw, second.raw)
+        if first.variant == int(P.Variant.Fp16x) and first.stats["recomputed"] > 0.2 * planted.count:
+            assert second.variant == int(P.Variant.Fp16)
