@@ -7,11 +7,12 @@
 // node = stripe*H + h + 1 (src/profile.cpp:176-181).  Every residue row:
 //
 //   1. the stripe shift (vwarp::reorder, src/vwarp.cpp:27-64): word H-1 moves
-//      one stripe up -- a __byte_perm inside the lane plus one __shfl_up_sync
-//      inside the group, with -inf injected at stripe 0;
-//   2. H cell updates in registers, in place from h = H-1 down to 0, with the
+//      one stripe up -- a __byte_perm inside the lane plus one __shfl_sync
+//      inside the group, with -inf injected at stripe 0 (or, in the paper's
+//      wrap mode, the top stripe's value);
+//   2. H cell updates in registers (slot-rotated, in place), with the
 //      emission costs for (residue, h) read from the shared-memory profile
-//      (one LDS per word, immediate offsets);
+//      (one LDS.128 per four words, immediate offsets);
 //   3. the running E max; for MSV the group max is reduced every row with
 //      xor shuffles (vwarp::max_reduce, src/vwarp.cpp:66-89) and B updated
 //      with the exact J-free form  B = max(base, subs(E, tec+tjb))
@@ -20,21 +21,31 @@
 // Scores are saturated bytes (the device-side bit-exact contract of
 // SURVEY.md §8(a)); the arithmetic "variant" policy decides how the bytes
 // are packed in a 32-bit register:
-//   Dpx16  : two u16 cells, native DPX VIADDMNMX / VIMNMX / VIMNMX3 (ALU pipe)
-//   Fp16   : two f16 cells in a fixed-point byte domain, saturating HADD2 on
-//            the FMA pipe (exact: every value is a multiple of 2^-8 or 2^-7)
-//   Swar8  : four u8 cells, __vaddus4 / __vsubus4 / __vmaxu4 (paper tier 5)
+//   Dpx16       : two u16 cells, native DPX VIADDMNMX / VIMNMX / VIMNMX3 (ALU)
+//   Fp16        : two f16 cells in a fixed-point byte domain, saturating HADD2
+//                 on the FP16 pipe (exact: every value a multiple of 2^-8/2^-7)
+//   Fp16Relaxed : FP16X SSV -- one HADD2.SAT per word without the 255 cap;
+//                 sequences that could have capped are flagged and rescored
+//   Fp16Sat     : FP16X MSV -- two-mode: exact in the linear f16 binade, then
+//                 (once a warp's sequences saturate) max(x, B) folded into the
+//                 floor clamp; FPE = 4 is the FP16X_ALT code form
+//   Swar8       : four u8 cells, __vaddus4 / __vsubus4 / __vmaxu4 (paper tier 5)
+//
+// Models beyond one warp's capacity run K warps per sequence
+// (scan_kernel_long) on the same chunk body with a per-row cross-warp
+// exchange through shared memory.
 //
 // Sequences are length-binned into 32-sequence tiles (host packer); a
 // persistent grid of warps pulls (tile, sub-batch) work items from a global
 // counter, longest tiles first.  Residues stream from HBM as 16-byte chunks
 // (one 128-bit load per lane per 16 rows, coalesced per warp).  The profile
 // table is staged once per CTA with one cp.async.bulk (TMA engine) copy.
+// Streamed scans start before the database has landed and wait per piece on
+// flags the copy stream writes (wait_for_tile).
 #pragma once
 
 #include <cuda_fp16.h>
 #include <stdint.h>
-
 
 namespace lhmm {
 
