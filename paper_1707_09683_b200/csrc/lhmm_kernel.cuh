@@ -530,6 +530,34 @@ __device__ __forceinline__ void group_barrier(uint32_t id, uint32_t threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+// The residue codes of one chunk (RPI rows; bytes 4q..4q+3 of word q are
+// rows r0+4q..r0+4q+3), loaded one chunk ahead so the HBM latency of the
+// residue stream hides behind a chunk of DP work.
+template <int RPI>
+struct ResChunk {
+    uint32_t w[RPI / 4];
+};
+
+template <int RPI>
+__device__ __forceinline__ ResChunk<RPI> load_res(const uint8_t* src, uint32_t r0) {
+    ResChunk<RPI> c;
+    const uint8_t* chunk = src + (r0 >> 4) * 512u;
+    if constexpr (RPI == 16) {
+        const uint4 v = ld_stream(chunk);
+        c.w[0] = v.x;
+        c.w[1] = v.y;
+        c.w[2] = v.z;
+        c.w[3] = v.w;
+    } else if constexpr (RPI == 8) {
+        const uint2 v = __ldcs(reinterpret_cast<const uint2*>(chunk + (r0 & 8u)));
+        c.w[0] = v.x;
+        c.w[1] = v.y;
+    } else {
+        c.w[0] = __ldcs(reinterpret_cast<const unsigned int*>(chunk + (r0 & 12u)));
+    }
+    return c;
+}
+
 // Long models (K > 1, see scan_kernel_long): the K warps of a group hold
 // one sequence (TL = 32K table lanes); lane 0 of each warp takes its stripe
 // shift input from *xin (the previous warp's top word, exchanged through
@@ -539,26 +567,15 @@ template <class V, int L, int H, int RPI, bool LAZY, int K = 1, int TL = L>
 __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32_t& e1,
                                           uint32_t& e2, uint32_t& e3, typename V::St& st,
                                           const KParams& p, const uint8_t* src, uint32_t r0,
-                                          uint32_t rows, const uint32_t* tab_lane, uint32_t P,
+                                          uint32_t rows, ResChunk<RPI>& pre,
+                                          const uint32_t* tab_lane, uint32_t P,
                                           int part_off, uint32_t shift_src, bool inject_here,
                                           uint32_t* xch = nullptr, uint32_t wig = 0,
                                           uint32_t bar = 0, uint32_t* xin = nullptr) {
     static_assert(K == 1 || (L == 32 && !LAZY), "multi-warp groups use whole warps, exact mode");
-    uint32_t wds[RPI / 4];
-    const uint8_t* chunk = src + (r0 >> 4) * 512u;
-    if constexpr (RPI == 16) {
-        const uint4 v = ld_stream(chunk);
-        wds[0] = v.x;
-        wds[1] = v.y;
-        wds[2] = v.z;
-        wds[3] = v.w;
-    } else if constexpr (RPI == 8) {
-        const uint2 v = __ldcs(reinterpret_cast<const uint2*>(chunk + (r0 & 8u)));
-        wds[0] = v.x;
-        wds[1] = v.y;
-    } else {
-        wds[0] = __ldcs(reinterpret_cast<const unsigned int*>(chunk + (r0 & 12u)));
-    }
+    const ResChunk<RPI> cur = pre;  // this chunk's residues, loaded one chunk ago
+    if (r0 + RPI < rows) pre = load_res<RPI>(src, r0 + RPI);
+    const uint32_t* wds = cur.w;
 #pragma unroll
     for (int q = 0; q < RPI / 4; ++q) {
         if (r0 + 4u * q >= rows) return true;  // warp-uniform
@@ -737,9 +754,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
         constexpr int RPI = rows_per_iter<V, H>();
         uint32_t r0 = 0;
         bool done = false;
+        ResChunk<RPI> pre{};
+        if (rows > 0) pre = load_res<RPI>(src, 0);
 #pragma unroll 1
         for (; r0 < rows && !done; r0 += RPI) {
-            done = run_chunk<V, L, H, RPI, false>(g, e0, e1, e2, e3, st, p, src, r0, rows,
+            done = run_chunk<V, L, H, RPI, false>(g, e0, e1, e2, e3, st, p, src, r0, rows, pre,
                                                   tab_lane, P, part_off, shift_src, inject_here);
             if constexpr (V::kTwoMode) {
                 // every sequence of the warp saturated (E = 255): B is constant
@@ -755,10 +774,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
         }
         if constexpr (V::kTwoMode) {
             constexpr int RPI_L = rows_per_iter<V, H, true>();
+            ResChunk<RPI_L> preL{};
+            if (r0 < rows && !done) preL = load_res<RPI_L>(src, r0);
 #pragma unroll 1
             for (; r0 < rows && !done; r0 += RPI_L)
                 done = run_chunk<V, L, H, RPI_L, true>(g, e0, e1, e2, e3, st, p, src, r0, rows,
-                                                       tab_lane, P, part_off, shift_src,
+                                                       preL, tab_lane, P, part_off, shift_src,
                                                        inject_here);
         }
         uint32_t E = V::acc2(V::acc2(e0, e1, e2), e3, e3);
@@ -843,10 +864,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel_long(const KParams
         uint32_t xin = V::template inject<false>(st);
         constexpr int RPI = rows_per_iter<V, H>();
         bool done = false;
+        ResChunk<RPI> pre{};
+        if (len > 0) pre = load_res<RPI>(src, 0);
 #pragma unroll 1
         for (uint32_t r0 = 0; r0 < len && !done; r0 += RPI)
             done = run_chunk<V, 32, H, RPI, false, K, 32 * K>(
-                g, e0, e1, e2, e3, st, p, src, r0, len, tab_lane, P, 0, shift_src, false,
+                g, e0, e1, e2, e3, st, p, src, r0, len, pre, tab_lane, P, 0, shift_src, false,
                 &s_x[grp][0], wig, bar, &xin);
         e0 = V::acc2(e0, e1, e2);
         e1 = e3;
