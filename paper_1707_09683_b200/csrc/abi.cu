@@ -557,11 +557,9 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             Choice ch = choose_geometry(pf.m, opt->alg, variant, 0, v.n_tiles, c->sm_count);
             L = ch.L ? ch.L : 1;
             if (ch.L) variant = ch.variant;
-        } else if (variant == LHMM_VARIANT_FP16X && opt->alg == LHMM_MSV &&
-                   calib_rate(LHMM_VARIANT_FP16X_ALT, LHMM_MSV, L, H) >
-                       calib_rate(LHMM_VARIANT_FP16X, LHMM_MSV, L, H)) {
-            variant = LHMM_VARIANT_FP16X_ALT;  // the faster code form of this geometry
         }
+        // an explicit (variant, L, H) runs exactly that code form -- the
+        // calibration sweep depends on it
     }
     if (!long_model && (L < 1 || L > 32 || (L & (L - 1))))
         return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,32]");
