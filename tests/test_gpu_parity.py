@@ -513,3 +513,38 @@ def test_policy_feedback_from_saturation_and_rescoring(ora):
         np.testing.assert_array_equal(first.raw, second.raw)
         if first.variant == int(P.Variant.Fp16x) and first.stats["recomputed"] > 0.2 * planted.count:
             assert second.variant == int(P.Variant.Fp16)
+
+
+def test_global_outputs_two_shards_one_process(ora):
+    """lhmm_scan_device_global from two shard contexts into one full-length
+    buffer (what the fused gather does across processes), over the long-model
+    kernel, an out-of-core shard and FP16X SSV rescoring."""
+    rng = P.Rng(0x6B0)
+    for m, budget, alg, variant in ((6000, 0, P.Algorithm.Msv, P.Variant.Auto),
+                                    (700, 1 << 20, P.Algorithm.Msv, P.Variant.Auto),
+                                    (300, 0, P.Algorithm.Ssv, P.Variant.Fp16x),
+                                    (300, 1 << 20, P.Algorithm.Ssv, P.Variant.Fp16x)):
+        hmm = rng.random_profile(m)
+        db = rng.lognormal_records(8000 if m < 1000 else 1500, 250, 0.6, 2, plant=(hmm, 0.4))
+        q = P.QuantParams()
+        costs = P.quantize_emissions(hmm, q)
+        a, b = P.Scanner(0), P.Scanner(0)
+        try:
+            base, _ = a.peer_buffer_create(2 * db.count)
+            for rank, s in enumerate((a, b)):
+                if budget:
+                    s.set_db_budget(budget)
+                s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+                s.set_database(db, rank, 2)
+            a.device_fill(base, 2, 2 * db.count)
+            for s in (a, b):
+                s.scan_device_global(P.ScanOptions(alg=alg, variant=variant, threshold=0.05),
+                                     base, base + db.count)
+            buf = a.device_to_host(base, 2 * db.count)
+            raw, ps = buf[:db.count], buf[db.count:]
+            assert (ps <= 1).all()
+            want = ora.scan_flat(int(alg), costs.bytes, db.residues, db.offsets, oq(q))
+            np.testing.assert_array_equal(raw, want, err_msg=f"m={m} budget={budget}")
+        finally:
+            b.close()
+            a.close()
