@@ -87,7 +87,27 @@ def build(verbose=False, jobs=None, defines=(), tag=""):
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    if not tag:
+        build_examples()
     return LIB
+
+
+def build_examples():
+    """Plain-C programs against the C ABI only (examples/*.c -> examples/bin/)."""
+    src_dir = os.path.join(ROOT, "examples")
+    out_dir = os.path.join(src_dir, "bin")
+    os.makedirs(out_dir, exist_ok=True)
+    for src in sorted(glob.glob(os.path.join(src_dir, "*.c"))):
+        exe = os.path.join(out_dir, os.path.splitext(os.path.basename(src))[0])
+        if os.path.exists(exe) and os.path.getmtime(exe) > max(os.path.getmtime(src),
+                                                              os.path.getmtime(LIB)):
+            continue
+        cmd = ["gcc", "-O2", "-Wall", "-std=c11", "-I" + os.path.join(ROOT, "include"), src,
+               "-o", exe, "-L" + LIBDIR, "-llhmm_b200",
+               "-Wl,-rpath,$ORIGIN/../../paper_1707_09683_b200/_lib"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"example build failed: {' '.join(cmd)}\n{r.stderr}")
 
 
 if __name__ == "__main__":
