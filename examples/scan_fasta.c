@@ -6,8 +6,8 @@
  *
  *   scan_fasta PROFILE.txt DB.fa|DB.lhmm [threshold]
  *
- * Built by oracle/Makefile (`make -C oracle examples`) against
- * paper_1707_09683_b200/_lib/liblhmm_b200.so; tests/test_examples.py runs
+ * Built by __graft_entry__.build() (paper_1707_09683_b200/build.py) into
+ * examples/bin/ against paper_1707_09683_b200/_lib/liblhmm_b200.so; tests/test_examples.py runs
  * it on a B200 and compares with the oracle.
  */
 #include <stdint.h>
