@@ -414,8 +414,9 @@ struct Fp16Relaxed {
 //               255 - tec - tjb) never changes again, so the cells can hold
 //               w = max(v, B) and the next row's max(x, B) folds into this
 //               row's floor clamp: w' = VIADDMNMX.S16(HADD2.SAT(w, dbias),
-//               -cost, B) -- one FP16 + one ALU op per word, no row
-//               reduction, no B update (both exact no-ops from there on).
+//               -cost, B) -- one FP16 + one ALU op per word, no E
+//               accumulation, row reduction or B update (all exact no-ops
+//               from there on: E is 255 and stays 255).
 // The switch happens at a chunk boundary (run_chunk<.., LAZY>).  Every cell
 // of every row is still computed exactly in both modes.
 template <int ALG, int FPE = 0>
@@ -505,7 +506,7 @@ struct Fp16Sat {
 #endif
 template <class V, int H, bool LAZY = false>
 __host__ __device__ constexpr int rows_per_iter() {
-    constexpr int per_row = LAZY ? H * 11 / 4 + 12 : H * (V::kMsv ? 15 : 11) / 4 + 20;
+    constexpr int per_row = LAZY ? H * 9 / 4 + 12 : H * (V::kMsv ? 15 : 11) / 4 + 20;
     constexpr int words = V::CPW == 4 ? per_row * 3 : per_row;  // SWAR8 ops are emulated
     constexpr int budget = !V::kTwoMode ? LHMM_RPI_BUDGET
                                         : (LAZY ? LHMM_RPI_BUDGET_LAZY2 : LHMM_RPI_BUDGET_EXACT2);
@@ -627,10 +628,11 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                     else
                         g[sl] = V::template cell<LAZY, false>(in, cw[k], st);
                 }
-                if constexpr (!V::kMsv || LAZY) {
-                    // SSV (and saturated MSV): fold the new words into E
-                    // right away so the ALU work interleaves with the FP16
-                    // cell updates (+4% at M=200/400)
+                if constexpr (!V::kMsv) {
+                    // SSV: fold the new words into E right away so the ALU
+                    // work interleaves with the FP16 cell updates (+4% at
+                    // M=200/400).  Lazy MSV needs no E at all: every E of
+                    // the warp is already 255, the maximum
                     const int s0 = ((4 * h4 - 1 - r) % H + H) % H;
                     const int s1 = ((4 * h4 - r) % H + H) % H;
                     const int s2 = ((4 * h4 + 1 - r) % H + H) % H;
@@ -781,6 +783,14 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
                 done = run_chunk<V, L, H, RPI_L, true>(g, e0, e1, e2, e3, st, p, src, r0, rows,
                                                        preL, tab_lane, P, part_off, shift_src,
                                                        inject_here);
+        }
+        if constexpr (V::kTwoMode) {
+            // lazy rows accumulate no E (it is already 255); folding the last
+            // row into E keeps every lazily computed cell live -- the scan
+            // computes all cells of all rows, never a saturation early exit
+            // (SURVEY 8(d)); H/2 ops per sequence
+#pragma unroll
+            for (int h = 0; h + 1 < H; h += 2) e1 = V::acc2(e1, g[h], g[h + 1]);
         }
         uint32_t E = V::acc2(V::acc2(e0, e1, e2), e3, e3);
         if constexpr (!V::kMsv) E = V::template group_reduce<L>(E);
