@@ -1,0 +1,79 @@
+#!/usr/bin/env python
+"""Small workload touching every device code path, sized to run under
+compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
+every variant and algorithm at a few lane counts, the K-warp long-model
+kernel, the relaxed-SSV rescoring, the device filter pipeline, the
+single-launch streamed scan and the out-of-core ring.  Checks results
+against the oracle as it goes (test infrastructure: scripts/ + oracle/).
+
+    compute-sanitizer --tool memcheck python scripts/sanitize_driver.py
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
+import paper_1707_09683_b200 as P  # noqa: E402
+
+
+def main():
+    ora = oracle.Oracle()
+    rng = P.Rng(0x5A17)
+    checked = 0
+
+    def check(rep, costs, q, db, alg):
+        nonlocal checked
+        want = ora.scan_flat(int(alg), costs.bytes, db.residues, db.offsets,
+                             oracle.QuantParams(q.scale, q.base, q.dbias, q.tec, q.tjb))
+        assert (rep.raw == want).all(), "mismatch"
+        checked += 1
+
+    q = P.QuantParams()
+    hmm = rng.random_profile(120)
+    db = rng.random_records(96, 1, 120, plant=(hmm, 0.3))
+    costs = P.quantize_emissions(hmm, q)
+    with P.Scanner(0) as s:
+        s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        s.set_database(db)
+        for v in (P.Variant.Fp16, P.Variant.Fp16x, P.Variant.Fp16xAlt, P.Variant.Dpx16,
+                  P.Variant.Swar8):
+            for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
+                if v == P.Variant.Fp16xAlt and alg == P.Algorithm.Ssv:
+                    continue
+                for L in (1, 4, 32):
+                    rep = s.scan(P.ScanOptions(alg=alg, variant=v, lanes=L, threshold=0.2))
+                    check(rep, costs, q, db, alg)
+        # paper wrap mode
+        rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv, variant=P.Variant.Fp16, lanes=8,
+                                   threshold=0.2, paper_wrap=True))
+        # device pipeline
+        s.filter_pipeline(0.3)
+        # streamed (single launch, stream-written flags)
+        for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
+            rep = s.scan_streamed(P.ScanOptions(alg=alg, threshold=0.2), 4)
+            check(rep, costs, q, db, alg)
+    # long model (K warps per sequence)
+    hl = rng.random_profile(5000)
+    dl = rng.random_records(12, 1, 40)
+    cl = P.quantize_emissions(hl, q)
+    with P.Scanner(0) as s:
+        s.set_profile(cl, q, hl.lambda_, hl.tau)
+        s.set_database(dl)
+        for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
+            check(s.scan(P.ScanOptions(alg=alg, threshold=0.2)), cl, q, dl, alg)
+    # out-of-core ring
+    big = rng.random_records(3000, 20, 400)
+    with P.Scanner(0) as s:
+        s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        s.set_db_budget(1 << 20)
+        s.set_database(big)
+        for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
+            check(s.scan(P.ScanOptions(alg=alg, threshold=0.2)), costs, q, big, alg)
+    print(f"sanitize driver ok: {checked} scans bit-exact")
+
+
+if __name__ == "__main__":
+    main()
