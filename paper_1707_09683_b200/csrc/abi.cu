@@ -45,6 +45,24 @@ void* pinned_alloc(size_t n) {
 }
 void pinned_free(void* p) { cudaFreeHost(p); }
 
+// A growable pinned host buffer (staging for async copies).
+struct PinnedBuf {
+    uint8_t* ptr = nullptr;
+    size_t cap = 0;
+    bool reserve(size_t n) {
+        if (n <= cap) return true;
+        release();
+        ptr = static_cast<uint8_t*>(pinned_alloc(n));
+        cap = ptr ? n : 0;
+        return ptr != nullptr;
+    }
+    void release() {
+        if (ptr) pinned_free(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+};
+
 template <class T>
 struct DevBuf {
     T* ptr = nullptr;
@@ -328,6 +346,10 @@ struct lhmm_context {
     // the driver entry point, resolved at run time (no link-time libcuda)
     CUresult (*write_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
     DevBuf<uint32_t> d_pieces;            // streamed scans: piece ends + ready flags
+    // pinned mirrors: the per-tile side arrays [tile_off | lens | out_idx]
+    // (streamed scans upload them piece by piece, asynchronously) and the
+    // staging area of host outputs (raw | pass)
+    PinnedBuf side_host, out_host;
     cudaEvent_t ev_side = nullptr;
     std::vector<cudaEvent_t> seg_events;
     int sm_count = 0, sm_clock_khz = 0, cc_major = 0, cc_minor = 0;
@@ -462,6 +484,74 @@ int upload_db(lhmm_context* c) {
                                  cudaMemcpyHostToDevice, c->stream));
     }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+    // pinned copy of the side arrays for streamed scans
+    const size_t T = db.tile_off.size();
+    if (T && c->side_host.reserve(T * sizeof(uint64_t) + 2 * T * 32 * sizeof(uint32_t))) {
+        std::memcpy(c->side_host.ptr, db.tile_off.data(), T * sizeof(uint64_t));
+        std::memcpy(c->side_host.ptr + T * 8, db.lens.data(), T * 32 * sizeof(uint32_t));
+        std::memcpy(c->side_host.ptr + T * 8 + T * 128, db.out_idx.data(),
+                    T * 32 * sizeof(uint32_t));
+    }
+    return LHMM_OK;
+}
+
+// Side arrays of tiles [t0, t1) on `s` (from the pinned mirror when there is
+// one, so the copies are asynchronous and overlap the scan).
+int upload_side(lhmm_context* c, uint64_t t0, uint64_t t1, cudaStream_t s) {
+    auto& db = c->db;
+    const uint64_t T = db.n_tiles;
+    if (t1 <= t0) return LHMM_OK;
+    const bool pin = c->side_host.cap >= T * 8 + T * 256;
+    const uint8_t* tile_off = pin ? c->side_host.ptr : reinterpret_cast<const uint8_t*>(db.tile_off.data());
+    const uint8_t* lens = pin ? c->side_host.ptr + T * 8 : reinterpret_cast<const uint8_t*>(db.lens.data());
+    const uint8_t* oidx = pin ? c->side_host.ptr + T * 8 + T * 128
+                              : reinterpret_cast<const uint8_t*>(db.out_idx.data());
+    CUDA_TRY(cudaMemcpyAsync(c->d_tile_off.ptr + t0, tile_off + t0 * 8, (t1 - t0) * 8,
+                             cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(c->d_lens.ptr + t0 * 32, lens + t0 * 128, (t1 - t0) * 128,
+                             cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(c->d_out_idx.ptr + t0 * 32, oidx + t0 * 128, (t1 - t0) * 128,
+                             cudaMemcpyHostToDevice, s));
+    return LHMM_OK;
+}
+
+// Raw + pass bytes of the last scan to caller-owned host buffers: one async
+// copy into the pinned staging area, then a parallel host copy (pageable
+// device-to-host copies run at a fraction of the link rate).
+bool page_locked(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+int outputs_to_host(lhmm_context* c, uint8_t* raw, uint8_t* pass, uint64_t n) {
+    if (!n) return LHMM_OK;
+    if ((page_locked(raw) && page_locked(pass)) || !c->out_host.reserve(2 * n)) {
+        // caller's buffers are page-locked (direct DMA), or no staging area
+        CUDA_TRY(cudaMemcpyAsync(raw, c->d_raw.ptr, n, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaMemcpyAsync(pass, c->d_pass.ptr, n, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        return LHMM_OK;
+    }
+    uint8_t* h = c->out_host.ptr;
+    CUDA_TRY(cudaMemcpyAsync(h, c->d_raw.ptr, n, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(h + n, c->d_pass.ptr, n, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    constexpr uint64_t kChunk = 1 << 18;
+    const int64_t chunks = int64_t((2 * n + kChunk - 1) / kChunk);
+#pragma omp parallel for schedule(static) if (chunks > 1)
+    for (int64_t k = 0; k < chunks; ++k) {
+        const uint64_t a = uint64_t(k) * kChunk, b = std::min<uint64_t>(2 * n, a + kChunk);
+        // [a, b) of raw|pass, split at the boundary
+        if (a < n) std::memcpy(raw + a, h + a, std::min(b, n) - a);
+        if (b > n) {
+            const uint64_t a2 = std::max(a, n);
+            std::memcpy(pass + (a2 - n), h + a2, b - a2);
+        }
+    }
     return LHMM_OK;
 }
 
@@ -768,13 +858,8 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         CUDA_TRY(cudaMemsetAsync(c->d_pieces.ptr + kMaxPieces, 0, kMaxPieces * 4, c->copy_stream));
         CUDA_TRY(cudaMemcpyAsync(c->d_pieces.ptr, ends.data(), ends.size() * 4,
                                  cudaMemcpyHostToDevice, c->copy_stream));
-        CUDA_TRY(cudaMemcpyAsync(c->d_tile_off.ptr, db.tile_off.data(), T * sizeof(uint64_t),
-                                 cudaMemcpyHostToDevice, c->copy_stream));
-        CUDA_TRY(cudaMemcpyAsync(c->d_lens.ptr, db.lens.data(), db.lens.size() * sizeof(uint32_t),
-                                 cudaMemcpyHostToDevice, c->copy_stream));
-        CUDA_TRY(cudaMemcpyAsync(c->d_out_idx.ptr, db.out_idx.data(),
-                                 db.out_idx.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                                 c->copy_stream));
+        // the per-tile side arrays travel with their piece (wait_for_tile
+        // precedes every side-array read; its acquire invalidates L1)
         CUDA_TRY(cudaEventRecord(c->ev_side, c->copy_stream));
         CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_side, 0));
         lhmm::KParams ps = p;
@@ -790,6 +875,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         for (size_t k = 0; k < ends.size(); ++k) {
             const uint64_t b0 = db.tile_off[t0];
             const uint64_t b1 = ends[k] < T ? db.tile_off[ends[k]] : db.data_bytes;
+            if (int rc = upload_side(c, t0, ends[k], c->copy_stream)) return rc;
             CUDA_TRY(cudaMemcpyAsync(c->d_db.ptr + b0, db.data + b0, b1 - b0,
                                      cudaMemcpyHostToDevice, c->copy_stream));
             const CUresult cr = c->write_value32(
@@ -813,14 +899,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         }
         CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
         CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev0, 0));
-        // per-tile side arrays first (small), then the residue bytes piecewise
-        CUDA_TRY(cudaMemcpyAsync(c->d_tile_off.ptr, db.tile_off.data(), T * sizeof(uint64_t),
-                                 cudaMemcpyHostToDevice, c->copy_stream));
-        CUDA_TRY(cudaMemcpyAsync(c->d_lens.ptr, db.lens.data(), db.lens.size() * sizeof(uint32_t),
-                                 cudaMemcpyHostToDevice, c->copy_stream));
-        CUDA_TRY(cudaMemcpyAsync(c->d_out_idx.ptr, db.out_idx.data(),
-                                 db.out_idx.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                                 c->copy_stream));
+        // each piece: its tiles' side arrays, then their residue bytes
         uint64_t t0 = 0;
         for (int k = 0; k < segments && t0 < T; ++k) {
             // byte-balanced boundary: first tile whose offset reaches the k+1-th share
@@ -832,6 +911,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             t1 = std::max(t1, t0 + 1);
             const uint64_t b0 = db.tile_off[t0];
             const uint64_t b1 = t1 < T ? db.tile_off[t1] : db.data_bytes;
+            if (int rc = upload_side(c, t0, t1, c->copy_stream)) return rc;
             CUDA_TRY(cudaMemcpyAsync(c->d_db.ptr + b0, db.data + b0, b1 - b0,
                                      cudaMemcpyHostToDevice, c->copy_stream));
             CUDA_TRY(cudaEventRecord(c->seg_events[size_t(k)], c->copy_stream));
@@ -1217,6 +1297,8 @@ int lhmm_context_destroy(lhmm_context* c) {
     c->db.data = nullptr;  // owned by the pinned cache
     lhmm::free_packed(c->db, pinned_free);
     if (c->pinned) pinned_free(c->pinned);
+    c->side_host.release();
+    c->out_host.release();
     lhmm_peer_buffers_release(c);
     c->d_out_gidx.release();
     c->d_db.release();
@@ -1463,13 +1545,7 @@ int lhmm_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* raw, uint8
     DeviceGuard g(c->device);
     if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
     if (int rc = do_scan(c, opt, c->d_raw.ptr, c->d_pass.ptr, st)) return rc;
-    const uint64_t n = c->db.n_local;
-    if (n) {
-        CUDA_TRY(cudaMemcpyAsync(raw, c->d_raw.ptr, n, cudaMemcpyDeviceToHost, c->stream));
-        CUDA_TRY(cudaMemcpyAsync(pass, c->d_pass.ptr, n, cudaMemcpyDeviceToHost, c->stream));
-        CUDA_TRY(cudaStreamSynchronize(c->stream));
-    }
-    return LHMM_OK;
+    return outputs_to_host(c, raw, pass, c->db.n_local);
 }
 
 int lhmm_scan_streamed(lhmm_context* c, const lhmm_scan_options* opt, int segments,
@@ -1486,13 +1562,7 @@ int lhmm_scan_streamed(lhmm_context* c, const lhmm_scan_options* opt, int segmen
         std::max<uint64_t>(1, c->db.data_bytes >> (c->stream_mem_ops ? 22 : 24));
     segments = int(std::min<uint64_t>(uint64_t(segments), max_pieces));
     if (int rc = do_scan(c, opt, c->d_raw.ptr, c->d_pass.ptr, st, segments)) return rc;
-    const uint64_t n = c->db.n_local;
-    if (n) {
-        CUDA_TRY(cudaMemcpyAsync(raw, c->d_raw.ptr, n, cudaMemcpyDeviceToHost, c->stream));
-        CUDA_TRY(cudaMemcpyAsync(pass, c->d_pass.ptr, n, cudaMemcpyDeviceToHost, c->stream));
-        CUDA_TRY(cudaStreamSynchronize(c->stream));
-    }
-    return LHMM_OK;
+    return outputs_to_host(c, raw, pass, c->db.n_local);
 }
 
 int lhmm_filter_pipeline(lhmm_context* c, double threshold, int variant, uint8_t* ssv_raw,

@@ -353,23 +353,34 @@ class Scanner:
     def upload_database(self):
         _check(_native.lib().lhmm_upload_database(self._ctx))
 
-    def scan(self, opt: ScanOptions):
-        raw = np.zeros(max(self.n_local, 1), dtype=np.uint8)
-        passed = np.zeros(max(self.n_local, 1), dtype=np.uint8)
+    def _outputs(self, out):
+        """Caller-provided (raw, passed) uint8 arrays of >= n_local bytes
+        (reused across scans; page-locked ones are copied into directly),
+        or fresh ones."""
+        n = max(self.n_local, 1)
+        if out is None:
+            return np.empty(n, dtype=np.uint8), np.empty(n, dtype=np.uint8)
+        raw, passed = out
+        for a in (raw, passed):
+            if a.dtype != np.uint8 or a.size < self.n_local or not a.flags.c_contiguous:
+                raise ContractError("outputs must be contiguous uint8 arrays of n_local bytes")
+        return raw, passed
+
+    def scan(self, opt: ScanOptions, out=None):
+        raw, passed = self._outputs(out)
         st = _native.ScanStatsC()
         oc = opt.c()
         _check(_native.lib().lhmm_scan(self._ctx, C.byref(oc), raw.ctypes.data_as(_native.u8p),
                                        passed.ctypes.data_as(_native.u8p), C.byref(st)))
         n = self.n_local
         return ScanReport(opt.alg, st.lanes, st.rows, st.variant, st.sequences, st.residues,
-                          st.device_ms * 1e-3, st.gcups, raw[:n], passed[:n].astype(bool),
+                          st.device_ms * 1e-3, st.gcups, raw[:n], passed[:n].view(bool),
                           st.as_dict())
 
-    def scan_streamed(self, opt: ScanOptions, segments=8):
+    def scan_streamed(self, opt: ScanOptions, segments=8, out=None):
         """End-to-end scan from the packed host image with the H2D copy
         overlapped with the kernels (lhmm_scan_streamed)."""
-        raw = np.zeros(max(self.n_local, 1), dtype=np.uint8)
-        passed = np.zeros(max(self.n_local, 1), dtype=np.uint8)
+        raw, passed = self._outputs(out)
         st = _native.ScanStatsC()
         oc = opt.c()
         _check(_native.lib().lhmm_scan_streamed(self._ctx, C.byref(oc), segments,
@@ -377,7 +388,7 @@ class Scanner:
                                                 passed.ctypes.data_as(_native.u8p), C.byref(st)))
         n = self.n_local
         return ScanReport(opt.alg, st.lanes, st.rows, st.variant, st.sequences, st.residues,
-                          st.device_ms * 1e-3, st.gcups, raw[:n], passed[:n].astype(bool),
+                          st.device_ms * 1e-3, st.gcups, raw[:n], passed[:n].view(bool),
                           st.as_dict())
 
     def filter_pipeline(self, threshold, variant=Variant.Auto):
