@@ -349,7 +349,7 @@ struct lhmm_context {
     // pinned mirrors: the per-tile side arrays [tile_off | lens | out_idx]
     // (streamed scans upload them piece by piece, asynchronously) and the
     // staging area of host outputs (raw | pass)
-    PinnedBuf side_host, out_host;
+    PinnedBuf side_host, out_host, counts_host;
     cudaEvent_t ev_side = nullptr;
     std::vector<cudaEvent_t> seg_events;
     int sm_count = 0, sm_clock_khz = 0, cc_major = 0, cc_minor = 0;
@@ -931,13 +931,27 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             t0 = t1;
         }
     }
+    // the saturation / flag counters come back with the same synchronisation
+    // as the end event (pinned words, no extra round trip)
+    uint32_t* counts = c->counts_host.reserve(8) ? reinterpret_cast<uint32_t*>(c->counts_host.ptr)
+                                                 : nullptr;
+    if (counts) {
+        if (track_sat)
+            CUDA_TRY(cudaMemcpyAsync(counts, c->d_sat.ptr, 4, cudaMemcpyDeviceToHost, c->stream));
+        if (relaxed)
+            CUDA_TRY(cudaMemcpyAsync(counts + 1, c->d_flag_count.ptr, 4, cudaMemcpyDeviceToHost,
+                                     c->stream));
+    }
     CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
     CUDA_TRY(cudaEventSynchronize(c->ev1));
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
     if (track_sat && v.sequences > 0) {
         uint32_t nsat = 0;
-        CUDA_TRY(cudaMemcpy(&nsat, c->d_sat.ptr, 4, cudaMemcpyDeviceToHost));
+        if (counts)
+            nsat = counts[0];
+        else
+            CUDA_TRY(cudaMemcpy(&nsat, c->d_sat.ptr, 4, cudaMemcpyDeviceToHost));
         pf.sat_frac = double(nsat) / double(v.sequences);
         pf.sat_gen = c->db_gen;
     }
@@ -946,9 +960,13 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         // rescore the flagged sequences with the exact kernel; the reported
         // time spans the relaxed kernel, the flag check and the rescoring
         uint32_t nflag = 0;
-        CUDA_TRY(cudaMemcpyAsync(&nflag, c->d_flag_count.ptr, 4, cudaMemcpyDeviceToHost,
-                                 c->stream));
-        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        if (counts) {
+            nflag = counts[1];
+        } else {
+            CUDA_TRY(cudaMemcpyAsync(&nflag, c->d_flag_count.ptr, 4, cudaMemcpyDeviceToHost,
+                                     c->stream));
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+        }
         if (nflag) {
             DbView sub;
             uint32_t nsel = 0;
@@ -1299,6 +1317,7 @@ int lhmm_context_destroy(lhmm_context* c) {
     if (c->pinned) pinned_free(c->pinned);
     c->side_host.release();
     c->out_host.release();
+    c->counts_host.release();
     lhmm_peer_buffers_release(c);
     c->d_out_gidx.release();
     c->d_db.release();
