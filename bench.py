@@ -242,7 +242,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--variant", default="auto", choices=["auto", "dpx16", "fp16", "swar8", "fp16x",
-                                                       "fp16xalt"])
+                                                       "fp16xalt", "fp16xm"])
     ap.add_argument("--nseq", type=int, default=0, help="override sequences per GPU")
     ap.add_argument("--ref-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -291,7 +291,7 @@ def main():
     desc, wl_alg, models_m, nseq, gen = WORKLOADS[args.workload]
     variant = {"auto": P.Variant.Auto, "dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16,
                "swar8": P.Variant.Swar8, "fp16x": P.Variant.Fp16x,
-               "fp16xalt": P.Variant.Fp16xAlt}[args.variant]
+               "fp16xalt": P.Variant.Fp16xAlt, "fp16xm": P.Variant.Fp16xMixed}[args.variant]
     q = P.QuantParams()
     algs = algs_of(wl_alg)
     threshold = 0.022
@@ -499,6 +499,11 @@ def main():
     hbm_gbs = float(peaks.get("hbm_gbs", 6545.9))
     hbm_achieved = (dbstats["packed_bytes"] + 9 * n_local) / (dom_ms * 1e-3) / 1e9
     share = sum(per_launch[dom]) / ms_max if ms_max else None
+    # binding resource of the dominant kernel: the shared-memory table gather
+    # (128 B/clk/SM); table bytes per cell of its code form
+    dom_form = ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm"][geo[dom][2]]
+    table_bpc = {"fp16xm": 1.6, "swar8": 1.0}.get(dom_form, 2.0)
+    smem_peak = n_sm * sm_max * 1e6 * (128 / table_bpc) / 1e9
     clocks = clk.summary()
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -512,7 +517,7 @@ def main():
         L, H, v, grid, smem, recomputed = geo[k]
         per_scan.append({"alg": a, "M": m, "ms": round(t, 4),
                          "gcups": round(dbstats["residues"] * m / (t * 1e-3) / 1e9, 1),
-                         "lanes": L, "rows": H, "variant": ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt"][v],
+                         "lanes": L, "rows": H, "variant": ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm"][v],
                          "grid": grid, "smem_bytes": smem, "rescored_exactly": recomputed})
     line = {
         "metric": "MSV/SSV GCUPS (device-timed) vs model length",
@@ -537,15 +542,21 @@ def main():
                       if args.db_budget else {})},
         "e2e": e2e,
         "gpu_launches": launches * world,
-        "roofline": {"bound": "int-simd", "achieved": round(achieved, 1),
-                     "peak": round(peak_gcups, 1), "unit": "GCUPS",
-                     "frac": round(achieved / peak_gcups, 4), "traffic": traffic,
-                     "kernel": f"{dom_a} M={dom_m}", "kernel_share_of_step": share,
-                     "peak_basis": f"{n_sm} SMs x {sm_max:.0f} MHz x 64 cells/clk/SM "
-                                   "(64 INT32 lane-ops/clk/SM x 4 packed u8 cells / 4 ops per cell)",
-                     "binding_resource": "the same 64 cells/clk/SM is the shared-memory bound of "
-                                         "the FP16 kernels (one 128-B table wavefront per 64 cells; "
-                                         "ncu: 95% of peak wavefronts on the C2 dominant kernel)",
+        "roofline": {"bound": "smem", "achieved": round(achieved, 1),
+                     "peak": round(smem_peak, 1), "unit": "GCUPS",
+                     "frac": round(achieved / smem_peak, 4), "traffic": traffic,
+                     "kernel": f"{dom_a} M={dom_m} ({dom_form})", "kernel_share_of_step": share,
+                     "peak_basis": f"{n_sm} SMs x {sm_max:.0f} MHz x 128 B/clk/SM shared-memory "
+                                   f"bandwidth / {table_bpc} emission-table bytes per cell "
+                                   f"({dom_form}) = {128 / table_bpc:.0f} cells/clk/SM: every "
+                                   "cell gathers its cost from the shared-memory table",
+                     "int_simd": {"peak": round(peak_gcups, 1), "unit": "GCUPS",
+                                  "frac": round(achieved / peak_gcups, 4),
+                                  "basis": "BASELINE north-star packed-integer-SIMD roofline: "
+                                           "64 INT32 lane-ops/clk/SM x 4 packed u8 cells / 4 ops "
+                                           "per cell = 64 cells/clk/SM; the FP16X forms split "
+                                           "each cell update over the FP16 and ALU pipes, so "
+                                           "they can pass it (FP16XM)"},
                      "hbm": {"bound": "hbm", "achieved": round(hbm_achieved, 1),
                              "peak": hbm_gbs, "unit": "GB/s",
                              "frac": round(hbm_achieved / hbm_gbs, 4)}},

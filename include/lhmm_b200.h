@@ -70,10 +70,15 @@ enum lhmm_variant {
     LHMM_VARIANT_FP16X = 4, /* SSV: relaxed f16 without the 255 cap, flagged sequences
                                rescored by the exact FP16 kernel; MSV: two-mode (exact
                                linear-f16, then lazy B once a warp's sequences saturate) */
-    LHMM_VARIANT_FP16X_ALT = 5 /* MSV: FP16X with every 4th word's cost step on the FP16
+    LHMM_VARIANT_FP16X_ALT = 5, /* MSV: FP16X with every 4th word's cost step on the FP16
                                   pipe instead of the ALU (same results; a code-generation
                                   alternative picked per geometry from the calibration);
                                   SSV: same as FP16X */
+    LHMM_VARIANT_FP16XM = 6 /* SSV: FP16X in the f16 subnormal domain with a mixed table --
+                               3 of every 5 words f16 (HADD2.SAT), 2 as signed bytes
+                               (PRMT + VIADDMNMX.S16): 1.6 table bytes per cell instead of
+                               2; flagged sequences rescored like FP16X; MSV: same as
+                               FP16X */
 };
 
 /* Byte-space constants; mirror of lanehmm::QuantParams

@@ -102,6 +102,9 @@ const int* rows_list(int variant, int* n) {
     case LHMM_VARIANT_FP16X_ALT:
         *n = int(sizeof(lhmm::kRows_fp16xalt) / sizeof(int));
         return lhmm::kRows_fp16xalt;
+    case LHMM_VARIANT_FP16XM:
+        *n = int(sizeof(lhmm::kRows_fp16xm) / sizeof(int));
+        return lhmm::kRows_fp16xm;
     default:
         *n = int(sizeof(lhmm::kRows_swar8) / sizeof(int));
         return lhmm::kRows_swar8;
@@ -201,7 +204,7 @@ double model_rate(int variant, int alg, uint32_t L, uint32_t H) {
     if (variant == LHMM_VARIANT_SWAR8)
         w = alg == LHMM_MSV ? 30.0 : 26.0;
     else if (variant == LHMM_VARIANT_FP16 || variant == LHMM_VARIANT_FP16X ||
-             variant == LHMM_VARIANT_FP16X_ALT)
+             variant == LHMM_VARIANT_FP16X_ALT || variant == LHMM_VARIANT_FP16XM)
         w = alg == LHMM_MSV ? 4.5 : 3.0;
     else
         w = alg == LHMM_MSV ? 4.5 : 3.5;
@@ -233,18 +236,19 @@ Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64
     // rescoring check.  Without any measurement the cost model decides.
     // FP16X stands for both of its code forms (FP16X, FP16X_ALT): the
     // measured table picks the faster one per geometry
-    const int vs_auto[4] = {LHMM_VARIANT_FP16, LHMM_VARIANT_DPX16, LHMM_VARIANT_FP16X,
-                            LHMM_VARIANT_FP16X_ALT};
-    const int vs_x[2] = {LHMM_VARIANT_FP16X, LHMM_VARIANT_FP16X_ALT};
+    const int vs_auto[5] = {LHMM_VARIANT_FP16, LHMM_VARIANT_DPX16, LHMM_VARIANT_FP16X,
+                            LHMM_VARIANT_FP16X_ALT, LHMM_VARIANT_FP16XM};
+    const int vs_x[3] = {LHMM_VARIANT_FP16X, LHMM_VARIANT_FP16X_ALT, LHMM_VARIANT_FP16XM};
     const int* vs = variant == LHMM_VARIANT_AUTO ? vs_auto : vs_x;
-    const int nv = variant == LHMM_VARIANT_AUTO ? 4 : (variant == LHMM_VARIANT_FP16X ? 2 : 1);
+    const int nv = variant == LHMM_VARIANT_AUTO ? 5 : (variant == LHMM_VARIANT_FP16X ? 3 : 1);
     for (int pass = 0; pass < 2 && best.L == 0; ++pass) {
         const bool measured_only = variant == LHMM_VARIANT_AUTO && pass == 0;
         for (int vi = 0; vi < nv; ++vi) {
             const int v = (variant == LHMM_VARIANT_AUTO || variant == LHMM_VARIANT_FP16X)
                               ? vs[vi] : variant;
-            if (!find_dispatch(v, alg, 1)) continue;  // FP16X_ALT: MSV only
-            const bool x = v == LHMM_VARIANT_FP16X || v == LHMM_VARIANT_FP16X_ALT;
+            if (!find_dispatch(v, alg, 1)) continue;  // FP16X_ALT: MSV, FP16XM: SSV only
+            const bool x = v == LHMM_VARIANT_FP16X || v == LHMM_VARIANT_FP16X_ALT ||
+                           v == LHMM_VARIANT_FP16XM;
             // relaxed SSV needs a database large enough to amortise its flag
             // check and rescoring launch
             if (variant == LHMM_VARIANT_AUTO && x && alg == LHMM_SSV && n_tiles > 0 &&
@@ -591,7 +595,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
     if (opt->alg != LHMM_MSV && opt->alg != LHMM_SSV)
         return set_error(LHMM_ERR_CONTRACT, "unknown algorithm");
-    if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_FP16X_ALT)
+    if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_FP16XM)
         return set_error(LHMM_ERR_CONTRACT, "unknown kernel variant");
     if (opt->reorder_mode != 0 && opt->reorder_mode != 1)
         return set_error(LHMM_ERR_CONTRACT, "unknown reorder mode");
@@ -601,6 +605,8 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     int variant = opt->variant;
     if (variant == LHMM_VARIANT_FP16X_ALT && opt->alg == LHMM_SSV)
         variant = LHMM_VARIANT_FP16X;  // the ALT code form is MSV-only
+    if (variant == LHMM_VARIANT_FP16XM && opt->alg == LHMM_MSV)
+        variant = LHMM_VARIANT_FP16X;  // the mixed-table form is SSV-only
 
     uint32_t L = opt->lanes, H = opt->rows;
     if (L != 0 && (L > 32 * kMaxLongK || (L & (L - 1))))
@@ -743,7 +749,8 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         p.sat_count = c->d_sat.ptr;
     }
     p.wrap = opt->reorder_mode == 1 ? 1u : 0u;
-    const bool relaxed = variant == LHMM_VARIANT_FP16X && opt->alg == LHMM_SSV;
+    const bool relaxed = (variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16XM) &&
+                         opt->alg == LHMM_SSV;
     if (relaxed) {
         if (int rc = c->d_flag.reserve(
                 std::max<uint64_t>(global_out ? c->n_global : c->db.n_local, 1)))

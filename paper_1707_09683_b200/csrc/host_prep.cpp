@@ -279,11 +279,16 @@ static void strides_for(uint32_t L, uint32_t H, uint32_t& P, uint32_t& copies,
     }
 }
 
+// Table rows ("register rows" of the 16-byte-per-lane slots): the mixed
+// SSV table packs five rows per slot (lhmm_kernel.cuh Fp16Mixed).
+static uint32_t slot_rows(int variant, uint32_t H) {
+    return variant == LHMM_VARIANT_FP16XM ? (H + 4u) / 5u * 4u : H;
+}
+
 uint64_t table_bytes_for(int variant, uint32_t L, uint32_t H, bool replicate) {
-    (void)variant;
     (void)replicate;
     uint32_t P, copies, cs;
-    strides_for(L, H, P, copies, cs);
+    strides_for(L, slot_rows(variant, H), P, copies, cs);
     uint64_t words = copies > 1 ? uint64_t(copies - 1) * cs + 23ull * P : 23ull * P;
     return (words * 4 + 15) / 16 * 16;
 }
@@ -320,10 +325,42 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
                  bool replicate, uint32_t dbias, TableImage& out) {
     const uint32_t cpw = cells_per_word(variant);
     uint32_t P, copies, cs;
-    strides_for(L, H, P, copies, cs);
+    strides_for(L, slot_rows(variant, H), P, copies, cs);
     out.res_stride = P;
     out.copy_stride = copies > 1 ? cs : 0;
     out.words.assign(table_bytes_for(variant, L, H, replicate) / 4, 0);
+    if (variant == LHMM_VARIANT_FP16XM) {
+        // SSV, subnormal f16 domain (units of 2^-24): per lane and five-row
+        // group one 16-byte slot = rows 5g..5g+2 as f16x2 words of the signed
+        // subnormal dbias - cost, then rows 5g+3, 5g+4 as four signed bytes
+        // (dbias - cost clamped to [-128, 127]; see Fp16Mixed)
+        for (uint32_t x = 0; x < 23; ++x)
+            for (uint32_t hg = 0; hg < (H + 4) / 5; ++hg)
+                for (uint32_t oig = 0; oig < L; ++oig) {
+                    uint32_t slot[4] = {0, 0, 0, 0};
+                    for (uint32_t k = 0; k < 5; ++k) {
+                        const uint32_t h = 5 * hg + k;
+                        for (uint32_t c = 0; c < 2; ++c) {
+                            const uint64_t node = uint64_t(2 * oig + c) * H + h + 1;
+                            const int cost = (h >= H || node > m || x > kUnknown)
+                                                 ? 0xff
+                                                 : costs[(node - 1) * 21 + x];
+                            const int t = int(dbias) - cost;
+                            if (k < 3) {
+                                const uint32_t f = t >= 0 ? uint32_t(t) : 0x8000u | uint32_t(-t);
+                                slot[k] |= f << (16 * c);
+                            } else {
+                                const int b = t < -128 ? -128 : (t > 127 ? 127 : t);
+                                slot[3] |= (uint32_t(b) & 0xffu) << (8 * (2 * (k - 3) + c));
+                            }
+                        }
+                    }
+                    const size_t at = size_t(x) * P + size_t(hg) * 4 * L + 4 * oig;
+                    for (uint32_t g = 0; g < copies; ++g)
+                        for (uint32_t w = 0; w < 4; ++w) out.words[size_t(g) * cs + at + w] = slot[w];
+                }
+        return;
+    }
     for (uint32_t x = 0; x < 23; ++x)
         for (uint32_t h = 0; h < H; ++h)
             for (uint32_t oig = 0; oig < L; ++oig) {

@@ -404,6 +404,73 @@ struct Fp16Relaxed {
     }
 };
 
+// FP16XM, SSV ("mixed table"): the relaxed FP16X recurrence in the f16
+// SUBNORMAL domain, where a pattern is its own value in units of 2^-24: byte
+// v lives as v - 128, so f16 adds and s16 integer adds on the patterns are the
+// same byte arithmetic (exact below 2048 units; a sequence is flagged and
+// rescored long before, at raw >= 256 - dbias).  Row groups are five words
+// held in one 16-byte table slot per lane: three f16x2 words (table entry
+// dbias - cost as a signed subnormal; cell = HADD2.SAT, clamp at +0 = byte
+// 128, FP16 pipe) and two words packed as signed bytes (dbias - cost clamped
+// to [-128, 127]; exact for unflagged sequences, whose cells stay below 128 -
+// dbias, so a cost step below -128 lands on the floor either way), expanded
+// by PRMT sign extension and applied with VIADDMNMX.S16 (ALU pipe).  Table
+// traffic falls from 2 to 1.6 bytes per cell and the two pipes share the work.
+template <int ALG>
+struct Fp16Mixed {
+    static_assert(ALG == 1, "the mixed-table form is an SSV form of FP16X");
+    static constexpr int CPW = 2;
+    static constexpr int kGroup = 5;  // words per 16-byte table slot
+    static constexpr bool kMsv = false;
+    static constexpr bool kRelaxed = true;
+    static constexpr bool kTwoMode = false;
+    static constexpr int kFpEvery = 0;
+    static constexpr uint32_t NEG = 0u;
+    struct St {
+        uint32_t cap;
+    };
+    __device__ static __forceinline__ void init(St& s, uint32_t, const KParams& p) {
+        s.cap = 256u - p.dbias;
+    }
+    __device__ static __forceinline__ uint32_t init_word(const St&) { return 0u; }
+    template <bool LAZY = false>
+    __device__ static __forceinline__ uint32_t inject(const St&) { return 0u; }
+    // FORM 3: integer (byte-table) word
+    template <bool LAZY = false, bool FPW = false, int FORM = 0>
+    __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St&) {
+        if constexpr (FORM == 3) {
+            return __viaddmax_s16x2(x, c, 0u);
+        } else {
+            return as_u32(__hadd2_sat(as_h2(x), as_h2(c)));
+        }
+    }
+    // the two byte-table words of a slot: bytes (0,1) and (2,3), sign-extended
+    __device__ static __forceinline__ uint32_t unpack(uint32_t w, int which) {
+        uint32_t r;
+        if (which == 0)
+            asm("prmt.b32 %0, %1, 0, 0x9180;" : "=r"(r) : "r"(w));
+        else
+            asm("prmt.b32 %0, %1, 0, 0xB3A2;" : "=r"(r) : "r"(w));
+        return r;
+    }
+    __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
+        return __vimax3_u16x2(E, a, b);
+    }
+    __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
+        return __byte_perm(top, up, 0x1076);
+    }
+    template <int L>
+    __device__ static __forceinline__ uint32_t group_reduce(uint32_t E) {
+        const uint32_t e = __vmaxu2(E, __byte_perm(E, E, 0x1032));
+        return group_max<L>(e);
+    }
+    __device__ static __forceinline__ void update_B(St&, uint32_t) {}
+    __device__ static __forceinline__ uint32_t raw(uint32_t e) { return 128u + (e & 0xffffu); }
+    __device__ static __forceinline__ bool needs_exact(uint32_t raw, const St& s) {
+        return raw >= s.cap;
+    }
+};
+
 // FP16X, MSV ("two-mode", exact throughout, no rescoring).  Byte v lives in
 // the linear f16 binade p = 1 + (v-255)/2048: bit pattern 0x3B01 + v, so
 // integer ops on the patterns are byte arithmetic and HADD2.SAT's 1.0 cap is
@@ -513,6 +580,16 @@ __host__ __device__ constexpr int rows_per_iter() {
     return 16 * words * 16 <= budget ? 16 : (8 * words * 16 <= budget ? 8 : 4);
 }
 
+// Words per row group (one 16-byte table slot per lane): 4, or V::kGroup.
+template <class V, class = void>
+struct group_width {
+    static constexpr int value = 4;
+};
+template <class V>
+struct group_width<V, decltype(void(V::kGroup))> {
+    static constexpr int value = V::kGroup;
+};
+
 // Whether word k of a row group takes the FP16 form of Fp16Sat (matches the
 // table encoding in build_table: h % 4 == 3 of full groups).
 template <class V>
@@ -597,6 +674,47 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
             } else {
                 up = inject_here ? V::template inject<LAZY>(st) : g[stop];
             }
+            constexpr int GW = group_width<V>::value;
+            if constexpr (GW == 5) {
+                // mixed-table SSV (Fp16Mixed): five words per 16-byte slot,
+                // three f16x2 words and one word of four signed bytes
+                static_assert(H % 5 == 0, "mixed-table groups are five rows");
+#pragma unroll
+                for (int hg = H / 5 - 1; hg >= 0; --hg) {
+                    const uint4 c = *reinterpret_cast<const uint4*>(tp + hg * 4 * TL);
+                    const uint32_t cw[5] = {c.x, c.y, c.z, V::unpack(c.w, 0), V::unpack(c.w, 1)};
+#pragma unroll
+                    for (int k = 4; k >= 0; --k) {
+                        const int h = 5 * hg + k;
+                        const int sl = ((h - 1 - r) % H + H) % H;
+                        const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
+                        if (k >= 3)
+                            g[sl] = V::template cell<LAZY, false, 3>(in, cw[k], st);
+                        else
+                            g[sl] = V::template cell<LAZY, false, 0>(in, cw[k], st);
+                    }
+                    // E: two folds per group, spread over the four maxima;
+                    // the fifth words of two groups share a third fold (the
+                    // upper group's word keeps its value for the rest of
+                    // the row)
+                    const int s0 = ((5 * hg - 1 - r) % H + H) % H;
+                    const int s1 = ((5 * hg - r) % H + H) % H;
+                    const int s2 = ((5 * hg + 1 - r) % H + H) % H;
+                    const int s3 = ((5 * hg + 2 - r) % H + H) % H;
+                    const int s4 = ((5 * hg + 3 - r) % H + H) % H;
+                    uint32_t* acc[4] = {&e0, &e1, &e2, &e3};
+                    *acc[(2 * hg) % 4] = V::acc2(*acc[(2 * hg) % 4], g[s0], g[s1]);
+                    *acc[(2 * hg + 1) % 4] = V::acc2(*acc[(2 * hg + 1) % 4], g[s2], g[s3]);
+                    constexpr int NG = H / 5;
+                    if ((NG - 1 - hg) % 2 == 1) {
+                        // pair with the fifth word of group hg + 1
+                        const int s4u = ((5 * hg + 8 - r) % H + H) % H;
+                        *acc[(hg + 2) % 4] = V::acc2(*acc[(hg + 2) % 4], g[s4], g[s4u]);
+                    } else if (hg == 0) {
+                        *acc[2] = V::acc2(*acc[2], g[s4], g[s4]);  // odd group count
+                    }
+                }
+            } else {
             // rows go in groups of four (one LDS.128 per lane); with
             // H = 2 (mod 4) the top group holds two rows (LDS.64)
 #pragma unroll
@@ -647,6 +765,7 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                         e3 = V::acc2(e3, g[s1], g[s0]);
                     }
                 }
+            }
             }
             if constexpr (V::kMsv && !LAZY) {
 #pragma unroll
@@ -705,7 +824,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
     __shared__ __align__(8) uint64_t bar;
     stage_table(smem, p.table, p.table_bytes, &bar);
 
-    static_assert(H % 2 == 0, "rows are read four (or, in the top group, two) at a time");
+    static_assert(H % 2 == 0 || group_width<V>::value == 5,
+                  "rows are read four (or, in the top group, two) at a time");
     constexpr int G = 32 / L;                    // sequences per warp
     constexpr int COPIES = L < 8 ? 8 / L : 1;    // table replicas (one per quarter-warp group)
     const uint32_t lane = threadIdx.x & 31u;

@@ -72,6 +72,7 @@ class Variant(enum.IntEnum):
     Swar8 = 3
     Fp16x = 4
     Fp16xAlt = 5   # MSV only: FP16X with a quarter of the cost steps on the FP16 pipe
+    Fp16xMixed = 6  # SSV only: FP16X with a mixed f16 / signed-byte table (1.6 B per cell)
 
 
 @dataclass

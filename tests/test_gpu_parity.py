@@ -27,7 +27,8 @@ def rows_list(variant):
     import gen_instances
     return gen_instances.ROWS[{P.Variant.Swar8: "swar8", P.Variant.Dpx16: "dpx16",
                                P.Variant.Fp16: "fp16", P.Variant.Fp16x: "fp16x",
-                               P.Variant.Fp16xAlt: "fp16xalt"}[variant]]
+                               P.Variant.Fp16xAlt: "fp16xalt",
+                               P.Variant.Fp16xMixed: "fp16xm"}[variant]]
 
 
 def rows_for(variant, L, m):
@@ -293,6 +294,33 @@ def test_relaxed_variant_rescoring_is_exact(ora, alg):
             assert rep.stats["recomputed"] == 0
         elif prof is hmm and q == P.QuantParams():
             assert rep.stats["recomputed"] > 0
+
+
+@pytest.mark.parametrize("L", [1, 2, 4, 8, 16, 32])
+def test_mixed_table_ssv(ora, L):
+    """FP16XM (SSV): subnormal-domain f16 words and signed-byte words in one
+    16-byte slot per five rows; flagged sequences rescored exactly.  Every
+    lane count, the four QuantParams sets (incl. dbias 10 and 0), planted
+    motifs that force flags, a flat profile, full and partial top groups."""
+    rng = P.Rng(0x3157 + L)
+    for t, q in enumerate(QUANTS):
+        for m in (10 * L * 7 - int(rng.next() % (2 * L)), 2 * L * 5, 37):
+            m = max(1, min(m, 2 * L * 70))
+            hmm = rng.random_profile(m)
+            db = rng.random_records(300, 1, 300, plant=(hmm, 0.3))
+            costs = P.quantize_emissions(hmm, q)
+            H = next(h for h in rows_list(P.Variant.Fp16xMixed) if 2 * L * h >= m)
+            rep = scan(costs, q, db, hmm, alg=P.Algorithm.Ssv, variant=P.Variant.Fp16xMixed,
+                       lanes=L, rows=H, threshold=0.2)
+            assert rep.variant == int(P.Variant.Fp16xMixed) and rep.rows == H
+            want = ora.scan_flat(1, costs.bytes, db.residues, db.offsets, oq(q))
+            np.testing.assert_array_equal(rep.raw, want, err_msg=f"L={L} m={m} q={q}")
+    flat = P.ProfileHMM("flat", 2 * L * 5, np.zeros((2 * L * 5, 20)), 0.7, 2.0)
+    costs = P.quantize_emissions(flat, P.QuantParams())
+    rep = scan(costs, P.QuantParams(), db, flat, alg=P.Algorithm.Ssv,
+               variant=P.Variant.Fp16xMixed, lanes=L, rows=5, threshold=0.2)
+    want = ora.scan_flat(1, costs.bytes, db.residues, db.offsets, oq(P.QuantParams()))
+    np.testing.assert_array_equal(rep.raw, want)
 
 
 @pytest.mark.parametrize("variant", [P.Variant.Fp16x, P.Variant.Fp16xAlt], ids=lambda v: v.name)
