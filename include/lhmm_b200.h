@@ -74,11 +74,11 @@ enum lhmm_variant {
                                   pipe instead of the ALU (same results; a code-generation
                                   alternative picked per geometry from the calibration);
                                   SSV: same as FP16X */
-    LHMM_VARIANT_FP16XM = 6 /* SSV: FP16X in the f16 subnormal domain with a mixed table --
-                               3 of every 5 words f16 (HADD2.SAT), 2 as signed bytes
-                               (PRMT + VIADDMNMX.S16): 1.6 table bytes per cell instead of
-                               2; flagged sequences rescored like FP16X; MSV: same as
-                               FP16X */
+    LHMM_VARIANT_FP16XM = 6 /* FP16X in the f16 subnormal domain with a mixed table: per
+                               five rows one 16-byte slot (three 16-bit-pair words, four
+                               bytes expanded by PRMT), 1.6 table bytes per cell instead
+                               of 2.  SSV: relaxed, flagged sequences rescored like FP16X;
+                               MSV: two-mode on negated cells (n = 255 - v) */
 };
 
 /* Byte-space constants; mirror of lanehmm::QuantParams

@@ -246,7 +246,7 @@ Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64
         for (int vi = 0; vi < nv; ++vi) {
             const int v = (variant == LHMM_VARIANT_AUTO || variant == LHMM_VARIANT_FP16X)
                               ? vs[vi] : variant;
-            if (!find_dispatch(v, alg, 1)) continue;  // FP16X_ALT: MSV, FP16XM: SSV only
+            if (!find_dispatch(v, alg, 1)) continue;  // FP16X_ALT: MSV only
             const bool x = v == LHMM_VARIANT_FP16X || v == LHMM_VARIANT_FP16X_ALT ||
                            v == LHMM_VARIANT_FP16XM;
             // relaxed SSV needs a database large enough to amortise its flag
@@ -605,8 +605,6 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     int variant = opt->variant;
     if (variant == LHMM_VARIANT_FP16X_ALT && opt->alg == LHMM_SSV)
         variant = LHMM_VARIANT_FP16X;  // the ALT code form is MSV-only
-    if (variant == LHMM_VARIANT_FP16XM && opt->alg == LHMM_MSV)
-        variant = LHMM_VARIANT_FP16X;  // the mixed-table form is SSV-only
 
     uint32_t L = opt->lanes, H = opt->rows;
     if (L != 0 && (L > 32 * kMaxLongK || (L & (L - 1))))

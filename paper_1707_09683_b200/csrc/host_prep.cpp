@@ -330,10 +330,11 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
     out.copy_stride = copies > 1 ? cs : 0;
     out.words.assign(table_bytes_for(variant, L, H, replicate) / 4, 0);
     if (variant == LHMM_VARIANT_FP16XM) {
-        // SSV, subnormal f16 domain (units of 2^-24): per lane and five-row
-        // group one 16-byte slot = rows 5g..5g+2 as f16x2 words of the signed
-        // subnormal dbias - cost, then rows 5g+3, 5g+4 as four signed bytes
-        // (dbias - cost clamped to [-128, 127]; see Fp16Mixed)
+        // f16 subnormal domain (units of 2^-24): per lane and five-row group
+        // one 16-byte slot = rows 5g..5g+2 as 16-bit pairs, then rows 5g+3,
+        // 5g+4 as four bytes.  SSV (Fp16Mixed): signed subnormal dbias - cost,
+        // bytes dbias - cost clamped to [-128, 127].  MSV (Fp16SatMixed, cells
+        // negated): the cost itself, in both forms
         for (uint32_t x = 0; x < 23; ++x)
             for (uint32_t hg = 0; hg < (H + 4) / 5; ++hg)
                 for (uint32_t oig = 0; oig < L; ++oig) {
@@ -345,6 +346,13 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
                             const int cost = (h >= H || node > m || x > kUnknown)
                                                  ? 0xff
                                                  : costs[(node - 1) * 21 + x];
+                            if (alg == LHMM_MSV) {
+                                if (k < 3)
+                                    slot[k] |= uint32_t(cost) << (16 * c);
+                                else
+                                    slot[3] |= uint32_t(cost) << (8 * (2 * (k - 3) + c));
+                                continue;
+                            }
                             const int t = int(dbias) - cost;
                             if (k < 3) {
                                 const uint32_t f = t >= 0 ? uint32_t(t) : 0x8000u | uint32_t(-t);

@@ -169,6 +169,17 @@ __device__ __forceinline__ uint32_t group_max(uint32_t v) {
     }
 }
 
+template <int L>
+__device__ __forceinline__ uint32_t group_min(uint32_t v) {
+    if constexpr (L == 32) {
+        return __reduce_min_sync(kFull, v);
+    } else {
+#pragma unroll
+        for (int off = 1; off < L; off <<= 1) v = min(v, __shfl_xor_sync(kFull, v, off));
+        return v;
+    }
+}
+
 __device__ __forceinline__ __half2 as_h2(uint32_t u) {
     return *reinterpret_cast<__half2*>(&u);
 }
@@ -471,6 +482,72 @@ struct Fp16Mixed {
     }
 };
 
+// FP16XM, MSV (two-mode like Fp16Sat, mixed table like Fp16Mixed).  The
+// cells live NEGATED in the f16 subnormal domain: pattern n = 255 - v (units
+// of 2^-24), so the byte cap v <= 255 is HADD2.SAT's clamp at +0, the floor
+// v >= 0 is n <= 255, every cost step is a plain ADD of the cost (no sign, so
+// costs pack as unsigned bytes without clamping) and max/min swap:
+//   exact: n' = VIADDMNMX.MIN(HADD2.SAT(min(n, nB), -dbias), cost, 255)
+//   lazy:  n' = VIADDMNMX.MIN(HADD2.SAT(n, -dbias), cost, nB)   (n holds min(n, nB))
+// E (max v) is the min of n; B = max(base, E - tec - tjb) is
+// nB = min(nbase, nE + tec + tjb).  Table: per five-row group one 16-byte slot,
+// three u16x2 words and four cost bytes (zero-extended by PRMT).
+template <int ALG>
+struct Fp16SatMixed {
+    static_assert(ALG == 0, "the negated two-mode form is MSV");
+    static constexpr int CPW = 2;
+    static constexpr int kGroup = 5;
+    static constexpr bool kMsv = true;
+    static constexpr bool kRelaxed = false;
+    static constexpr bool kTwoMode = true;
+    static constexpr int kFpEvery = 0;
+    static constexpr uint32_t NEG = 0x00FF00FFu;  // byte 0 in both halves
+    struct St {
+        uint32_t B, nbase2, nd, tj2;  // B holds nB = 255 - B
+    };
+    __device__ static __forceinline__ void init(St& s, uint32_t base, const KParams& p) {
+        s.nbase2 = (255u - base) * 0x00010001u;
+        s.B = s.nbase2;
+        s.nd = (0x8000u | p.dbias) * 0x00010001u;  // -dbias as a subnormal f16
+        s.tj2 = p.tecjb * 0x00010001u;
+    }
+    __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
+    template <bool LAZY = false>
+    __device__ static __forceinline__ uint32_t inject(const St& s) { return LAZY ? s.B : NEG; }
+    template <bool LAZY = false, bool FPW = false, int FORM = 0>
+    __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
+        const uint32_t m = LAZY ? x : __vminu2(x, s.B);
+        const uint32_t pp = as_u32(__hadd2_sat(as_h2(m), as_h2(s.nd)));
+        return __viaddmin_s16x2(pp, c, LAZY ? s.B : NEG);
+    }
+    // the byte words of a slot: cost bytes (0,1) and (2,3), zero-extended
+    __device__ static __forceinline__ uint32_t unpack(uint32_t w, int which) {
+        return __byte_perm(w, 0u, which == 0 ? 0x4140 : 0x4342);
+    }
+    __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
+        return __vimin3_u16x2(E, a, b);
+    }
+    __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
+        return __byte_perm(top, up, 0x1076);
+    }
+    template <int L>
+    __device__ static __forceinline__ uint32_t group_reduce(uint32_t E) {
+        const uint32_t e = __vminu2(E, __byte_perm(E, E, 0x1032));
+        return group_min<L>(e);
+    }
+    __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
+        s.B = __viaddmin_s16x2(e, s.tj2, s.nbase2);  // nB = min(nbase, nE + tec + tjb)
+    }
+    __device__ static __forceinline__ bool saturated(uint32_t e) { return (e & 0xffffu) == 0u; }
+    template <int H>
+    __device__ static __forceinline__ void enter_lazy(uint32_t (&g)[H], const St& s) {
+#pragma unroll
+        for (int h = 0; h < H; ++h) g[h] = __vminu2(g[h], s.B);
+    }
+    __device__ static __forceinline__ uint32_t raw(uint32_t e) { return 255u - (e & 0xffffu); }
+    __device__ static __forceinline__ bool needs_exact(uint32_t, const St&) { return false; }
+};
+
 // FP16X, MSV ("two-mode", exact throughout, no rescoring).  Byte v lives in
 // the linear f16 binade p = 1 + (v-255)/2048: bit pattern 0x3B01 + v, so
 // integer ops on the patterns are byte arithmetic and HADD2.SAT's 1.0 cap is
@@ -676,8 +753,9 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
             }
             constexpr int GW = group_width<V>::value;
             if constexpr (GW == 5) {
-                // mixed-table SSV (Fp16Mixed): five words per 16-byte slot,
-                // three f16x2 words and one word of four signed bytes
+                // mixed tables (Fp16Mixed, Fp16SatMixed): five words per
+                // 16-byte slot, three 16-bit-pair words and one word of four
+                // bytes
                 static_assert(H % 5 == 0, "mixed-table groups are five rows");
 #pragma unroll
                 for (int hg = H / 5 - 1; hg >= 0; --hg) {
@@ -693,6 +771,7 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                         else
                             g[sl] = V::template cell<LAZY, false, 0>(in, cw[k], st);
                     }
+                    if constexpr (!V::kMsv) {
                     // E: two folds per group, spread over the four maxima;
                     // the fifth words of two groups share a third fold (the
                     // upper group's word keeps its value for the rest of
@@ -712,6 +791,7 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                         *acc[(hg + 2) % 4] = V::acc2(*acc[(hg + 2) % 4], g[s4], g[s4u]);
                     } else if (hg == 0) {
                         *acc[2] = V::acc2(*acc[2], g[s4], g[s4]);  // odd group count
+                    }
                     }
                 }
             } else {
@@ -770,10 +850,11 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
             if constexpr (V::kMsv && !LAZY) {
 #pragma unroll
                 for (int h = 0; h < H; h += 8) {
-                    e0 = V::acc2(e0, g[h], g[h + 1]);
-                    if (h + 2 < H) e1 = V::acc2(e1, g[h + 2], g[h + 3]);
-                    if (h + 4 < H) e2 = V::acc2(e2, g[h + 4], g[h + 5]);
-                    if (h + 6 < H) e3 = V::acc2(e3, g[h + 6], g[h + 7]);
+                    // (odd H: the last word pairs with itself)
+                    e0 = V::acc2(e0, g[h], g[h + 1 < H ? h + 1 : H - 1]);
+                    if (h + 2 < H) e1 = V::acc2(e1, g[h + 2], g[h + 3 < H ? h + 3 : H - 1]);
+                    if (h + 4 < H) e2 = V::acc2(e2, g[h + 4], g[h + 5 < H ? h + 5 : H - 1]);
+                    if (h + 6 < H) e3 = V::acc2(e3, g[h + 6], g[h + 7 < H ? h + 7 : H - 1]);
                 }
             }
             if constexpr (K > 1) {
@@ -910,7 +991,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
             // computes all cells of all rows, never a saturation early exit
             // (SURVEY 8(d)); H/2 ops per sequence
 #pragma unroll
-            for (int h = 0; h + 1 < H; h += 2) e1 = V::acc2(e1, g[h], g[h + 1]);
+            for (int h = 0; h < H; h += 2) e1 = V::acc2(e1, g[h], g[h + 1 < H ? h + 1 : H - 1]);
         }
         uint32_t E = V::acc2(V::acc2(e0, e1, e2), e3, e3);
         if constexpr (!V::kMsv) E = V::template group_reduce<L>(E);

@@ -287,9 +287,12 @@ def test_relaxed_variant_rescoring_is_exact(ora, alg):
         want = ora.scan_flat(int(alg), costs.bytes, db.residues, db.offsets, oq(q))
         rep = scan(costs, q, db, prof, alg=alg, variant=P.Variant.Fp16x, threshold=0.3)
         np.testing.assert_array_equal(rep.raw, want)
-        # FP16X MSV has two code forms (FP16X, FP16X_ALT); calibration picks
-        assert rep.variant in ((int(P.Variant.Fp16x), int(P.Variant.Fp16xAlt))
-                               if alg == P.Algorithm.Msv else (int(P.Variant.Fp16x),))
+        # FP16X has several code forms (FP16X, FP16X_ALT for MSV, the
+        # mixed-table FP16XM); the calibration picks one per geometry
+        assert rep.variant in ((int(P.Variant.Fp16x), int(P.Variant.Fp16xAlt),
+                                int(P.Variant.Fp16xMixed))
+                               if alg == P.Algorithm.Msv else
+                               (int(P.Variant.Fp16x), int(P.Variant.Fp16xMixed)))
         if alg == P.Algorithm.Msv:
             assert rep.stats["recomputed"] == 0
         elif prof is hmm and q == P.QuantParams():
@@ -297,7 +300,7 @@ def test_relaxed_variant_rescoring_is_exact(ora, alg):
 
 
 @pytest.mark.parametrize("L", [1, 2, 4, 8, 16, 32])
-def test_mixed_table_ssv(ora, L):
+def test_mixed_table_ssv(ora, L):  # noqa: C901
     """FP16XM (SSV): subnormal-domain f16 words and signed-byte words in one
     16-byte slot per five rows; flagged sequences rescored exactly.  Every
     lane count, the four QuantParams sets (incl. dbias 10 and 0), planted
@@ -323,7 +326,8 @@ def test_mixed_table_ssv(ora, L):
     np.testing.assert_array_equal(rep.raw, want)
 
 
-@pytest.mark.parametrize("variant", [P.Variant.Fp16x, P.Variant.Fp16xAlt], ids=lambda v: v.name)
+@pytest.mark.parametrize("variant", [P.Variant.Fp16x, P.Variant.Fp16xAlt, P.Variant.Fp16xMixed],
+                         ids=lambda v: v.name)
 @pytest.mark.parametrize("L", [1, 2, 4, 8, 16, 32])
 def test_two_mode_msv_switch(ora, L, variant):
     """FP16X MSV switches a warp to the lazy-B form once all of its
@@ -331,7 +335,7 @@ def test_two_mode_msv_switch(ora, L, variant):
     never-saturating sequences of varied lengths in the same warps, at
     default and non-saturating parameters, and compare with the oracle."""
     rng = P.Rng(0x5A7 + L)
-    m = 2 * L * rows_for(P.Variant.Fp16x, L, min(2 * L * 72, 700)) - L
+    m = 2 * L * rows_for(variant, L, min(2 * L * 70, 700)) - L
     hmm = rng.random_profile(m)
     a = rng.random_records(300, 200, 900, plant=(hmm, 0.6))
     b = rng.random_records(300, 1, 900)
@@ -342,7 +346,8 @@ def test_two_mode_msv_switch(ora, L, variant):
         costs = P.quantize_emissions(hmm, q)
         want = ora.scan_flat(0, costs.bytes, db.residues, db.offsets, oq(q))
         rep = scan(costs, q, db, hmm, alg=P.Algorithm.Msv, variant=variant, lanes=L,
-                   rows=rows_for(P.Variant.Fp16x, L, m))
+                   rows=rows_for(variant, L, m))
+        assert rep.variant == int(variant)
         np.testing.assert_array_equal(rep.raw, want, err_msg=f"L={L} q={q}")
 
 
