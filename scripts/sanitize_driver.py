@@ -38,8 +38,8 @@ def main():
     with P.Scanner(0) as s:
         s.set_profile(costs, q, hmm.lambda_, hmm.tau)
         s.set_database(db)
-        for v in (P.Variant.Fp16, P.Variant.Fp16x, P.Variant.Fp16xAlt, P.Variant.Dpx16,
-                  P.Variant.Swar8):
+        for v in (P.Variant.Fp16, P.Variant.Fp16x, P.Variant.Fp16xAlt, P.Variant.Fp16xMixed,
+                  P.Variant.Dpx16, P.Variant.Swar8):
             for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
                 if v == P.Variant.Fp16xAlt and alg == P.Algorithm.Ssv:
                     continue
