@@ -380,7 +380,7 @@ struct lhmm_context {
     DevBuf<uint8_t> d_flag;        // FP16X: per-sequence "rescore exactly"
     DevBuf<uint32_t> d_flag_count;
 
-    std::map<std::tuple<int, int, uint32_t, uint32_t, size_t>, int> occupancy;
+    std::map<std::tuple<int, int, uint32_t, uint32_t, size_t>, std::pair<int, int>> occupancy;
     // geometry policy results per (m, alg, variant, want_L, tiles)
     std::map<std::tuple<uint32_t, int, int, uint32_t, uint64_t>, std::tuple<int, uint32_t, uint32_t>>
         choices;
@@ -667,11 +667,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     DispatchFn fn = long_model ? find_dispatch_long(opt->alg, L / 32)
                                : find_dispatch(variant, opt->alg, L);
     if (!fn) return set_error(LHMM_ERR_CONTRACT, "no kernel for this variant/alg/lanes");
-    // work items: (tile, sub-batch) pairs, or single slots for long models;
-    // the persistent grid holds `units_per_cta` of them per CTA at a time
     const uint64_t items_per_tile = long_model ? 32 : L;
-    const uint64_t warps_per_cta =
-        long_model ? lhmm::kMaxThreads / 32 / (L / 32) : lhmm::kMaxThreads / 32;
 
     // profile table image (cached per profile and geometry)
     const bool rep = !long_model && use_replica(variant, L, H);
@@ -771,12 +767,18 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     auto okey = std::make_tuple(variant, opt->alg, L, H, table_bytes);
     auto it = c->occupancy.find(okey);
     if (it == c->occupancy.end()) {
+        // the query also fixes the instance's CTA size (lhmm_kernel.cuh threads_for)
         if (fn(lhmm::kOpQuery, int(H), &cfg, &p) != 0)
             return set_error(LHMM_ERR_CUDA, std::string("occupancy query failed: ") +
                                                 cudaGetErrorString(cudaGetLastError()));
-        it = c->occupancy.emplace(okey, cfg.blocks_per_sm).first;
+        it = c->occupancy.emplace(okey, std::make_pair(cfg.blocks_per_sm, cfg.threads)).first;
     }
-    const int bps = it->second;
+    const int bps = it->second.first;
+    cfg.threads = it->second.second;
+    // work items: (tile, sub-batch) pairs, or single slots for long models;
+    // the persistent grid holds warps_per_cta of them per CTA at a time
+    const uint64_t warps_per_cta = long_model ? uint64_t(cfg.threads) / 32 / (L / 32)
+                                              : uint64_t(cfg.threads) / 32;
     if (bps < 1) return set_error(LHMM_ERR_CUDA, "kernel cannot be resident (smem/registers)");
     const uint64_t need = (uint64_t(p.n_items) + warps_per_cta - 1) / warps_per_cta;
     cfg.grid = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(c->sm_count) * bps, need)));

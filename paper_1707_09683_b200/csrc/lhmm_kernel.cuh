@@ -899,8 +899,19 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
     return false;
 }
 
+// Threads per CTA: kMaxThreads (16 warps, <= 128 registers per thread), or
+// 12 warps (<= 170 registers) for the widest register rows, which would
+// otherwise spill at 128 (ptxas: stack frames from H ~ 54 up).
+#ifndef LHMM_WIDE_H
+#define LHMM_WIDE_H 54
+#endif
+template <class V, int H>
+__host__ __device__ constexpr int threads_for() {
+    return H >= LHMM_WIDE_H && kMaxThreads > 384 ? 384 : kMaxThreads;
+}
+
 template <class V, int L, int H>
-__global__ void __launch_bounds__(kMaxThreads, 1) scan_kernel(const KParams p) {
+__global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KParams p) {
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t bar;
     stage_table(smem, p.table, p.table_bytes, &bar);
@@ -1123,6 +1134,7 @@ template <class V, int L, int H>
 int launch_one(int op, LaunchCfg* c, const KParams* p) {
     auto* k = &scan_kernel<V, L, H>;
     if (op == kOpQuery) {
+        c->threads = threads_for<V, H>();
         if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(c->smem)) !=
             cudaSuccess)
             return -2;
