@@ -755,8 +755,31 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
             if constexpr (GW == 5) {
                 // mixed tables (Fp16Mixed, Fp16SatMixed): five words per
                 // 16-byte slot, three 16-bit-pair words and one word of four
-                // bytes
-                static_assert(H % 5 == 0, "mixed-table groups are five rows");
+                // bytes; with H = 5k + r (r <= 3) a top slot of r 16-bit-pair
+                // words
+                constexpr int RT = H % 5;
+                static_assert(RT <= 3, "a partial mixed-table group holds at most three rows");
+                if constexpr (RT > 0) {
+                    constexpr int hg = H / 5;
+                    const uint4 c = *reinterpret_cast<const uint4*>(tp + hg * 4 * TL);
+                    const uint32_t cw[3] = {c.x, c.y, c.z};
+#pragma unroll
+                    for (int k = RT - 1; k >= 0; --k) {
+                        const int h = 5 * hg + k;
+                        const int sl = ((h - 1 - r) % H + H) % H;
+                        const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
+                        g[sl] = V::template cell<LAZY, false, 0>(in, cw[k], st);
+                    }
+                    if constexpr (!V::kMsv) {
+                        const int t0 = ((5 * hg - 1 - r) % H + H) % H;
+                        const int t1 = ((5 * hg + (RT > 1 ? 1 : 0) - 1 - r) % H + H) % H;
+                        e3 = V::acc2(e3, g[t0], g[t1]);
+                        if constexpr (RT == 3) {
+                            const int t2 = ((5 * hg + 1 - r) % H + H) % H;
+                            e2 = V::acc2(e2, g[t2], g[t2]);
+                        }
+                    }
+                }
 #pragma unroll
                 for (int hg = H / 5 - 1; hg >= 0; --hg) {
                     const uint4 c = *reinterpret_cast<const uint4*>(tp + hg * 4 * TL);

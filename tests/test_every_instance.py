@@ -60,6 +60,9 @@ def check(s, ora, rng, alg, variant, L, H, m, q, seed_tag):
         assert "table" in str(e) or "geometry" in str(e), str(e)
         return False
     assert (rep.lanes, rep.rows) == (L, H), seed_tag
+    if L <= 32:
+        # the widest register rows run 12-warp CTAs (lhmm_kernel.cuh threads_for)
+        assert rep.stats["threads"] == (384 if H >= 54 else 512), seed_tag
     want = ora.scan_flat(int(alg), costs.bytes, db.residues, db.offsets, oq(q))
     np.testing.assert_array_equal(rep.raw, want, err_msg=f"{seed_tag} m={m} q={q}")
     lens = db.lengths()
