@@ -46,6 +46,16 @@ def main():
                 for L in (1, 4, 32):
                     rep = s.scan(P.ScanOptions(alg=alg, variant=v, lanes=L, threshold=0.2))
                     check(rep, costs, q, db, alg)
+        # FP16XM five-row groups with a three-row top slot (H = 58, 12-warp CTAs)
+        h3 = rng.random_profile(116)
+        c3 = P.quantize_emissions(h3, q)
+        s.set_profile(c3, q, h3.lambda_, h3.tau)
+        for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
+            rep = s.scan(P.ScanOptions(alg=alg, variant=P.Variant.Fp16xMixed, lanes=1, rows=58,
+                                       threshold=0.2))
+            assert rep.stats["threads"] == 384
+            check(rep, c3, q, db, alg)
+        s.set_profile(costs, q, hmm.lambda_, hmm.tau)
         # paper wrap mode
         rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv, variant=P.Variant.Fp16, lanes=8,
                                    threshold=0.2, paper_wrap=True))
