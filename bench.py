@@ -242,7 +242,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--variant", default="auto", choices=["auto", "dpx16", "fp16", "swar8", "fp16x",
-                                                       "fp16xalt", "fp16xm"])
+                                                       "fp16xalt", "fp16xm", "fp16xh"])
     ap.add_argument("--nseq", type=int, default=0, help="override sequences per GPU")
     ap.add_argument("--ref-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -291,7 +291,7 @@ def main():
     desc, wl_alg, models_m, nseq, gen = WORKLOADS[args.workload]
     variant = {"auto": P.Variant.Auto, "dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16,
                "swar8": P.Variant.Swar8, "fp16x": P.Variant.Fp16x,
-               "fp16xalt": P.Variant.Fp16xAlt, "fp16xm": P.Variant.Fp16xMixed}[args.variant]
+               "fp16xalt": P.Variant.Fp16xAlt, "fp16xm": P.Variant.Fp16xMixed, "fp16xh": P.Variant.Fp16xHybrid}[args.variant]
     q = P.QuantParams()
     algs = algs_of(wl_alg)
     threshold = 0.022
@@ -501,8 +501,8 @@ def main():
     share = sum(per_launch[dom]) / ms_max if ms_max else None
     # binding resource of the dominant kernel: the shared-memory table gather
     # (128 B/clk/SM); table bytes per cell of its code form
-    dom_form = ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm"][geo[dom][2]]
-    table_bpc = {"fp16xm": 1.6, "swar8": 1.0}.get(dom_form, 2.0)
+    dom_form = ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm", "fp16xh"][geo[dom][2]]
+    table_bpc = {"fp16xm": 1.6, "fp16xh": 1.6, "swar8": 1.0}.get(dom_form, 2.0)
     smem_peak = n_sm * sm_max * 1e6 * (128 / table_bpc) / 1e9
     clocks = clk.summary()
     cpu = None
@@ -517,7 +517,7 @@ def main():
         L, H, v, grid, smem, recomputed = geo[k]
         per_scan.append({"alg": a, "M": m, "ms": round(t, 4),
                          "gcups": round(dbstats["residues"] * m / (t * 1e-3) / 1e9, 1),
-                         "lanes": L, "rows": H, "variant": ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm"][v],
+                         "lanes": L, "rows": H, "variant": ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm", "fp16xh"][v],
                          "grid": grid, "smem_bytes": smem, "rescored_exactly": recomputed})
     line = {
         "metric": "MSV/SSV GCUPS (device-timed) vs model length",

@@ -74,11 +74,14 @@ enum lhmm_variant {
                                   pipe instead of the ALU (same results; a code-generation
                                   alternative picked per geometry from the calibration);
                                   SSV: same as FP16X */
-    LHMM_VARIANT_FP16XM = 6 /* FP16X in the f16 subnormal domain with a mixed table: per
+    LHMM_VARIANT_FP16XM = 6, /* FP16X in the f16 subnormal domain with a mixed table: per
                                five rows one 16-byte slot (three 16-bit-pair words, four
                                bytes expanded by PRMT), 1.6 table bytes per cell instead
                                of 2.  SSV: relaxed, flagged sequences rescored like FP16X;
                                MSV: two-mode on negated cells (n = 255 - v) */
+    LHMM_VARIANT_FP16XH = 7 /* MSV: two-mode hybrid -- the FP16X exact mode on a 16-bit
+                               table and the FP16XM lazy mode on a mixed table, both in
+                               shared memory; SSV: same as FP16XM */
 };
 
 /* Byte-space constants; mirror of lanehmm::QuantParams

@@ -105,6 +105,9 @@ const int* rows_list(int variant, int* n) {
     case LHMM_VARIANT_FP16XM:
         *n = int(sizeof(lhmm::kRows_fp16xm) / sizeof(int));
         return lhmm::kRows_fp16xm;
+    case LHMM_VARIANT_FP16XH:
+        *n = int(sizeof(lhmm::kRows_fp16xh) / sizeof(int));
+        return lhmm::kRows_fp16xh;
     default:
         *n = int(sizeof(lhmm::kRows_swar8) / sizeof(int));
         return lhmm::kRows_swar8;
@@ -162,6 +165,12 @@ bool rows_instantiated(int variant, uint32_t H) {
 }
 
 constexpr uint64_t kMaxTableBytes = 200 * 1024;  // leaves room for 1 CTA/SM + static smem
+// the hybrid MSV form keeps two images (FP16X + FP16XM): up to 224 KB of the
+// 227 KB a CTA may hold
+constexpr uint64_t kMaxTableBytesHybrid = 224 * 1024;
+uint64_t max_table_bytes(int variant) {
+    return variant == LHMM_VARIANT_FP16XH ? kMaxTableBytesHybrid : kMaxTableBytes;
+}
 
 // Largest model the one-warp kernels can hold (FP16 family, table in smem).
 uint32_t max_standard_capacity(int alg) {
@@ -204,7 +213,8 @@ double model_rate(int variant, int alg, uint32_t L, uint32_t H) {
     if (variant == LHMM_VARIANT_SWAR8)
         w = alg == LHMM_MSV ? 30.0 : 26.0;
     else if (variant == LHMM_VARIANT_FP16 || variant == LHMM_VARIANT_FP16X ||
-             variant == LHMM_VARIANT_FP16X_ALT || variant == LHMM_VARIANT_FP16XM)
+             variant == LHMM_VARIANT_FP16X_ALT || variant == LHMM_VARIANT_FP16XM ||
+             variant == LHMM_VARIANT_FP16XH)
         w = alg == LHMM_MSV ? 4.5 : 3.0;
     else
         w = alg == LHMM_MSV ? 4.5 : 3.5;
@@ -236,19 +246,20 @@ Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64
     // rescoring check.  Without any measurement the cost model decides.
     // FP16X stands for both of its code forms (FP16X, FP16X_ALT): the
     // measured table picks the faster one per geometry
-    const int vs_auto[5] = {LHMM_VARIANT_FP16, LHMM_VARIANT_DPX16, LHMM_VARIANT_FP16X,
-                            LHMM_VARIANT_FP16X_ALT, LHMM_VARIANT_FP16XM};
-    const int vs_x[3] = {LHMM_VARIANT_FP16X, LHMM_VARIANT_FP16X_ALT, LHMM_VARIANT_FP16XM};
+    const int vs_auto[6] = {LHMM_VARIANT_FP16, LHMM_VARIANT_DPX16, LHMM_VARIANT_FP16X,
+                            LHMM_VARIANT_FP16X_ALT, LHMM_VARIANT_FP16XM, LHMM_VARIANT_FP16XH};
+    const int vs_x[4] = {LHMM_VARIANT_FP16X, LHMM_VARIANT_FP16X_ALT, LHMM_VARIANT_FP16XM,
+                         LHMM_VARIANT_FP16XH};
     const int* vs = variant == LHMM_VARIANT_AUTO ? vs_auto : vs_x;
-    const int nv = variant == LHMM_VARIANT_AUTO ? 5 : (variant == LHMM_VARIANT_FP16X ? 3 : 1);
+    const int nv = variant == LHMM_VARIANT_AUTO ? 6 : (variant == LHMM_VARIANT_FP16X ? 4 : 1);
     for (int pass = 0; pass < 2 && best.L == 0; ++pass) {
         const bool measured_only = variant == LHMM_VARIANT_AUTO && pass == 0;
         for (int vi = 0; vi < nv; ++vi) {
             const int v = (variant == LHMM_VARIANT_AUTO || variant == LHMM_VARIANT_FP16X)
                               ? vs[vi] : variant;
-            if (!find_dispatch(v, alg, 1)) continue;  // FP16X_ALT: MSV only
+            if (!find_dispatch(v, alg, 1)) continue;  // FP16X_ALT, FP16XH: MSV only
             const bool x = v == LHMM_VARIANT_FP16X || v == LHMM_VARIANT_FP16X_ALT ||
-                           v == LHMM_VARIANT_FP16XM;
+                           v == LHMM_VARIANT_FP16XM || v == LHMM_VARIANT_FP16XH;
             // relaxed SSV needs a database large enough to amortise its flag
             // check and rescoring launch
             if (variant == LHMM_VARIANT_AUTO && x && alg == LHMM_SSV && n_tiles > 0 &&
@@ -266,7 +277,7 @@ Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64
                     const uint32_t H = uint32_t(rows[i]);
                     const uint64_t cap = uint64_t(cpw) * L * H;
                     if (cap < m) continue;
-                    if (lhmm::table_bytes_for(v, L, H, true) > kMaxTableBytes) continue;
+                    if (lhmm::table_bytes_for(v, L, H, true) > max_table_bytes(v)) continue;
                     double rate = calib_rate(v, alg, L, H);
                     if (rate < 0) {
                         if (measured_only) continue;
@@ -312,6 +323,7 @@ struct ProfileSlot {
     // device table images keyed by (variant, alg, L, H, replicated)
     struct DevTable {
         uint32_t res_stride = 0, copy_stride = 0;
+        uint32_t second_off = 0, res_stride2 = 0, copy_stride2 = 0;  // hybrid MSV
         size_t bytes = 0;
         DevBuf<uint32_t> buf;
     };
@@ -595,7 +607,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
     if (opt->alg != LHMM_MSV && opt->alg != LHMM_SSV)
         return set_error(LHMM_ERR_CONTRACT, "unknown algorithm");
-    if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_FP16XM)
+    if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_FP16XH)
         return set_error(LHMM_ERR_CONTRACT, "unknown kernel variant");
     if (opt->reorder_mode != 0 && opt->reorder_mode != 1)
         return set_error(LHMM_ERR_CONTRACT, "unknown reorder mode");
@@ -605,6 +617,8 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     int variant = opt->variant;
     if (variant == LHMM_VARIANT_FP16X_ALT && opt->alg == LHMM_SSV)
         variant = LHMM_VARIANT_FP16X;  // the ALT code form is MSV-only
+    if (variant == LHMM_VARIANT_FP16XH && opt->alg == LHMM_SSV)
+        variant = LHMM_VARIANT_FP16XM;  // the hybrid is an MSV form
 
     uint32_t L = opt->lanes, H = opt->rows;
     if (L != 0 && (L > 32 * kMaxLongK || (L & (L - 1))))
@@ -676,7 +690,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (tit == pf.tables.end()) {
         lhmm::TableImage img;
         lhmm::build_table(pf.costs.data(), pf.m, variant, opt->alg, L, H, rep, pf.q.dbias, img);
-        if (!long_model && img.words.size() * 4 > kMaxTableBytes + 16 * 1024)
+        if (!long_model && img.words.size() * 4 > max_table_bytes(variant) + 16 * 1024)
             return set_error(LHMM_ERR_DATA, "profile table does not fit in shared memory");
         ProfileSlot::DevTable t;
         if (int rc = t.buf.reserve(img.words.size())) return rc;
@@ -685,6 +699,9 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         CUDA_TRY(cudaStreamSynchronize(c->stream));
         t.res_stride = img.res_stride;
         t.copy_stride = img.copy_stride;
+        t.second_off = img.second_off;
+        t.res_stride2 = img.res_stride2;
+        t.copy_stride2 = img.copy_stride2;
         t.bytes = img.words.size() * 4;
         tit = pf.tables.emplace(tkey, std::move(t)).first;
     }
@@ -733,6 +750,9 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     p.table_bytes = uint32_t(table_bytes);
     p.res_stride = tab.res_stride;
     p.copy_stride = tab.copy_stride;
+    p.table2_off = tab.second_off;
+    p.res_stride2 = tab.res_stride2;
+    p.copy_stride2 = tab.copy_stride2;
     p.dbias = pf.q.dbias;
     p.tecjb = uint32_t(pf.q.tec) + uint32_t(pf.q.tjb);
     p.fault = opt->fault_injection ? 1u : 0u;

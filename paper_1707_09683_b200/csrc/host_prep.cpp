@@ -286,6 +286,9 @@ static uint32_t slot_rows(int variant, uint32_t H) {
 }
 
 uint64_t table_bytes_for(int variant, uint32_t L, uint32_t H, bool replicate) {
+    if (variant == LHMM_VARIANT_FP16XH)  // 16-bit exact-mode image + mixed lazy-mode image
+        return table_bytes_for(LHMM_VARIANT_FP16X, L, H, replicate) +
+               table_bytes_for(LHMM_VARIANT_FP16XM, L, H, replicate);
     (void)replicate;
     uint32_t P, copies, cs;
     strides_for(L, slot_rows(variant, H), P, copies, cs);
@@ -323,6 +326,21 @@ static uint32_t encode_word(int variant, int alg, const uint8_t* c, uint32_t cpw
 
 void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_t L, uint32_t H,
                  bool replicate, uint32_t dbias, TableImage& out) {
+    if (variant == LHMM_VARIANT_FP16XH) {
+        // hybrid two-mode MSV: the FP16X image (exact rows) followed by the
+        // FP16XM image (lazy rows)
+        TableImage a, b;
+        build_table(costs, m, LHMM_VARIANT_FP16X, alg, L, H, replicate, dbias, a);
+        build_table(costs, m, LHMM_VARIANT_FP16XM, alg, L, H, replicate, dbias, b);
+        out.res_stride = a.res_stride;
+        out.copy_stride = a.copy_stride;
+        out.second_off = uint32_t(a.words.size());
+        out.res_stride2 = b.res_stride;
+        out.copy_stride2 = b.copy_stride;
+        out.words = std::move(a.words);
+        out.words.insert(out.words.end(), b.words.begin(), b.words.end());
+        return;
+    }
     const uint32_t cpw = cells_per_word(variant);
     uint32_t P, copies, cs;
     strides_for(L, slot_rows(variant, H), P, copies, cs);

@@ -57,6 +57,8 @@ struct TableImage {
     std::vector<uint32_t> words;
     uint32_t res_stride = 0;
     uint32_t copy_stride = 0;
+    // hybrid MSV: a second (mixed) image after the first
+    uint32_t second_off = 0, res_stride2 = 0, copy_stride2 = 0;
 };
 uint32_t cells_per_word(int variant);
 uint64_t table_bytes_for(int variant, uint32_t L, uint32_t H, bool replicate);

@@ -81,6 +81,11 @@ struct KParams {
     uint32_t table_bytes;       // multiple of 16
     uint32_t res_stride;        // words per residue row (P)
     uint32_t copy_stride;       // words between per-group replicas (0: shared)
+    // hybrid MSV (Fp16SatHybrid): the lazy mode's mixed table follows the
+    // exact mode's 16-bit table in the same shared-memory image
+    uint32_t table2_off;        // words
+    uint32_t res_stride2;
+    uint32_t copy_stride2;
     uint32_t dbias;             // per-step bias
     uint32_t tecjb;             // tec + tjb (may exceed 255)
     uint32_t fault;             // fault injection (verification only)
@@ -548,6 +553,82 @@ struct Fp16SatMixed {
     __device__ static __forceinline__ bool needs_exact(uint32_t, const St&) { return false; }
 };
 
+// FP16XH, MSV ("hybrid"): the exact mode of Fp16Sat (linear-binade cells,
+// 16-bit table, four-row groups) and the lazy mode of Fp16SatMixed (negated
+// subnormal cells, mixed table, five-row groups), both tables resident in
+// shared memory.  At the switch (every E of the warp is 255) the cells are
+// converted once: n = 0x3C00 - pattern (= 255 - v), then min(n, nB).
+template <int ALG>
+struct Fp16SatHybrid {
+    static_assert(ALG == 0, "the hybrid two-mode form is MSV");
+    static constexpr int CPW = 2;
+    static constexpr int kGroupLazy = 5;
+    static constexpr bool kMsv = true;
+    static constexpr bool kRelaxed = false;
+    static constexpr bool kTwoMode = true;
+    static constexpr bool kHybrid = true;
+    static constexpr int kFpEvery = 0;
+    static constexpr uint32_t kByte0 = 0x3B013B01u;
+    static constexpr uint32_t NEG = kByte0;
+    struct St {
+        uint32_t B, base2, d1, ntj2;  // exact mode (patterns 0x3B01 + v)
+        uint32_t nd;                  // lazy mode: -dbias as a subnormal f16
+    };
+    __device__ static __forceinline__ void init(St& s, uint32_t base, const KParams& p) {
+        s.base2 = (0x3B01u + base) * 0x00010001u;
+        s.B = s.base2;
+        s.d1 = as_u32(__float2half2_rn(float(p.dbias) / 2048.f));
+        s.ntj2 = (0u - p.tecjb) & 0xffffu;
+        s.ntj2 |= s.ntj2 << 16;
+        s.nd = (0x8000u | p.dbias) * 0x00010001u;
+    }
+    __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
+    // lazy mode: B holds nB (enter_lazy)
+    template <bool LAZY = false>
+    __device__ static __forceinline__ uint32_t inject(const St& s) { return LAZY ? s.B : NEG; }
+    template <bool LAZY = false, bool FPW = false, int FORM = 0>
+    __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
+        if constexpr (LAZY) {
+            const uint32_t pp = as_u32(__hadd2_sat(as_h2(x), as_h2(s.nd)));
+            return __viaddmin_s16x2(pp, c, s.B);
+        } else {
+            const uint32_t m = as_u32(__hmax2(as_h2(x), as_h2(s.B)));
+            const uint32_t pp = as_u32(__hadd2_sat(as_h2(m), as_h2(s.d1)));
+            return __viaddmax_s16x2(pp, c, kByte0);
+        }
+    }
+    __device__ static __forceinline__ uint32_t unpack(uint32_t w, int which) {
+        return __byte_perm(w, 0u, which == 0 ? 0x4140 : 0x4342);
+    }
+    __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
+        return __vimax3_u16x2(E, a, b);
+    }
+    __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
+        return __byte_perm(top, up, 0x1076);
+    }
+    template <int L>
+    __device__ static __forceinline__ uint32_t group_reduce(uint32_t E) {
+        const uint32_t e = __vmaxu2(E, __byte_perm(E, E, 0x1032));
+        return group_max<L>(e);
+    }
+    __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
+        s.B = __viaddmax_s16x2(e, s.ntj2, s.base2);
+    }
+    __device__ static __forceinline__ bool saturated(uint32_t e) {
+        return (e & 0xffffu) == 0x3C00u;
+    }
+    template <int H>
+    __device__ static __forceinline__ void enter_lazy(uint32_t (&g)[H], St& s) {
+        // per half 0x3C00 - p lies in [0, 0xFF]: no borrow crosses the halves
+        s.B = 0x3C003C00u - s.B;
+#pragma unroll
+        for (int h = 0; h < H; ++h) g[h] = __vminu2(0x3C003C00u - g[h], s.B);
+    }
+    // E stays in the exact domain (the lazy cells, n <= 255, never exceed it)
+    __device__ static __forceinline__ uint32_t raw(uint32_t e) { return (e & 0xffffu) - 0x3B01u; }
+    __device__ static __forceinline__ bool needs_exact(uint32_t, const St&) { return false; }
+};
+
 // FP16X, MSV ("two-mode", exact throughout, no rescoring).  Byte v lives in
 // the linear f16 binade p = 1 + (v-255)/2048: bit pattern 0x3B01 + v, so
 // integer ops on the patterns are byte arithmetic and HADD2.SAT's 1.0 cap is
@@ -667,6 +748,24 @@ struct group_width<V, decltype(void(V::kGroup))> {
     static constexpr int value = V::kGroup;
 };
 
+// Group width of a mode: the hybrid policy's lazy rows use five-row groups.
+template <class V, class = void>
+struct is_hybrid {
+    static constexpr bool value = false;
+};
+template <class V>
+struct is_hybrid<V, decltype(void(V::kHybrid))> {
+    static constexpr bool value = V::kHybrid;
+};
+template <class V, bool LAZY>
+__host__ __device__ constexpr int mode_group_width() {
+    if constexpr (is_hybrid<V>::value) {
+        return LAZY ? 5 : 4;
+    } else {
+        return group_width<V>::value;
+    }
+}
+
 // Whether word k of a row group takes the FP16 form of Fp16Sat (matches the
 // table encoding in build_table: h % 4 == 3 of full groups).
 template <class V>
@@ -751,7 +850,7 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
             } else {
                 up = inject_here ? V::template inject<LAZY>(st) : g[stop];
             }
-            constexpr int GW = group_width<V>::value;
+            constexpr int GW = mode_group_width<V, LAZY>();
             if constexpr (GW == 5) {
                 // mixed tables (Fp16Mixed, Fp16SatMixed): five words per
                 // 16-byte slot, three 16-bit-pair words and one word of four
@@ -928,9 +1027,12 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
 #ifndef LHMM_WIDE_H
 #define LHMM_WIDE_H 54
 #endif
+#ifndef LHMM_WIDE_THREADS
+#define LHMM_WIDE_THREADS 384
+#endif
 template <class V, int H>
 __host__ __device__ constexpr int threads_for() {
-    return H >= LHMM_WIDE_H && kMaxThreads > 384 ? 384 : kMaxThreads;
+    return H >= LHMM_WIDE_H && kMaxThreads > LHMM_WIDE_THREADS ? LHMM_WIDE_THREADS : kMaxThreads;
 }
 
 template <class V, int L, int H>
@@ -948,6 +1050,11 @@ __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KPar
     const uint32_t grp = lane / L;
     const uint32_t P = p.res_stride;
     const uint32_t* tab_lane = smem + (grp % COPIES) * p.copy_stride + 4u * oig;
+    // the lazy rows' table: the second (mixed) image of a hybrid policy
+    const uint32_t PL = is_hybrid<V>::value ? p.res_stride2 : P;
+    const uint32_t* tab_lazy =
+        is_hybrid<V>::value ? smem + p.table2_off + (grp % COPIES) * p.copy_stride2 + 4u * oig
+                            : tab_lane;
     // word offset of this lane's pair in a two-row top group, relative to
     // tab_lane (see build_table): 2*oig, plus 2L for the upper quarter-warp
     // of a 16-lane LDS.64 wavefront when L < 16
@@ -1016,7 +1123,7 @@ __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KPar
 #pragma unroll 1
             for (; r0 < rows && !done; r0 += RPI_L)
                 done = run_chunk<V, L, H, RPI_L, true>(g, e0, e1, e2, e3, st, p, src, r0, rows,
-                                                       preL, tab_lane, P, part_off, shift_src,
+                                                       preL, tab_lazy, PL, part_off, shift_src,
                                                        inject_here);
         }
         if constexpr (V::kTwoMode) {

@@ -72,7 +72,8 @@ class Variant(enum.IntEnum):
     Swar8 = 3
     Fp16x = 4
     Fp16xAlt = 5   # MSV only: FP16X with a quarter of the cost steps on the FP16 pipe
-    Fp16xMixed = 6  # SSV only: FP16X with a mixed f16 / signed-byte table (1.6 B per cell)
+    Fp16xMixed = 6  # FP16X with a mixed 16-bit / byte table (1.6 B per cell)
+    Fp16xHybrid = 7  # MSV: FP16X exact rows + FP16XM lazy rows (two tables)
 
 
 @dataclass

@@ -22,7 +22,8 @@ import gen_instances  # noqa: E402
 ROWS = {P.Variant.Dpx16: gen_instances.ROWS["dpx16"], P.Variant.Fp16: gen_instances.ROWS["fp16"],
         P.Variant.Swar8: gen_instances.ROWS["swar8"], P.Variant.Fp16x: gen_instances.ROWS["fp16x"],
         P.Variant.Fp16xAlt: gen_instances.ROWS["fp16xalt"],
-        P.Variant.Fp16xMixed: gen_instances.ROWS["fp16xm"]}
+        P.Variant.Fp16xMixed: gen_instances.ROWS["fp16xm"],
+        P.Variant.Fp16xHybrid: gen_instances.ROWS["fp16xh"]}
 
 
 def main():
@@ -41,7 +42,7 @@ def main():
     res = db.total_residues()
     vmap = {"dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16, "swar8": P.Variant.Swar8,
             "fp16x": P.Variant.Fp16x, "fp16xalt": P.Variant.Fp16xAlt,
-            "fp16xm": P.Variant.Fp16xMixed}
+            "fp16xm": P.Variant.Fp16xMixed, "fp16xh": P.Variant.Fp16xHybrid}
     for m in [int(x) for x in args.models.split(",")]:
         hmm = P.Rng(7000 + m).random_profile(m)
         costs = P.quantize_emissions(hmm, q)

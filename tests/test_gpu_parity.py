@@ -28,7 +28,8 @@ def rows_list(variant):
     return gen_instances.ROWS[{P.Variant.Swar8: "swar8", P.Variant.Dpx16: "dpx16",
                                P.Variant.Fp16: "fp16", P.Variant.Fp16x: "fp16x",
                                P.Variant.Fp16xAlt: "fp16xalt",
-                               P.Variant.Fp16xMixed: "fp16xm"}[variant]]
+                               P.Variant.Fp16xMixed: "fp16xm",
+                               P.Variant.Fp16xHybrid: "fp16xh"}[variant]]
 
 
 def rows_for(variant, L, m):
@@ -290,7 +291,7 @@ def test_relaxed_variant_rescoring_is_exact(ora, alg):
         # FP16X has several code forms (FP16X, FP16X_ALT for MSV, the
         # mixed-table FP16XM); the calibration picks one per geometry
         assert rep.variant in ((int(P.Variant.Fp16x), int(P.Variant.Fp16xAlt),
-                                int(P.Variant.Fp16xMixed))
+                                int(P.Variant.Fp16xMixed), int(P.Variant.Fp16xHybrid))
                                if alg == P.Algorithm.Msv else
                                (int(P.Variant.Fp16x), int(P.Variant.Fp16xMixed)))
         if alg == P.Algorithm.Msv:
@@ -326,7 +327,8 @@ def test_mixed_table_ssv(ora, L):  # noqa: C901
     np.testing.assert_array_equal(rep.raw, want)
 
 
-@pytest.mark.parametrize("variant", [P.Variant.Fp16x, P.Variant.Fp16xAlt, P.Variant.Fp16xMixed],
+@pytest.mark.parametrize("variant", [P.Variant.Fp16x, P.Variant.Fp16xAlt, P.Variant.Fp16xMixed,
+                                     P.Variant.Fp16xHybrid],
                          ids=lambda v: v.name)
 @pytest.mark.parametrize("L", [1, 2, 4, 8, 16, 32])
 def test_two_mode_msv_switch(ora, L, variant):
@@ -535,7 +537,8 @@ def test_policy_feedback_from_saturation_and_rescoring(ora):
             first = s.scan(P.ScanOptions(alg=P.Algorithm.Msv))
             second = s.scan(P.ScanOptions(alg=P.Algorithm.Msv))
             np.testing.assert_array_equal(first.raw, second.raw)
-            two_mode = second.variant in (int(P.Variant.Fp16x), int(P.Variant.Fp16xAlt))
+            two_mode = second.variant in (int(P.Variant.Fp16x), int(P.Variant.Fp16xAlt),
+                                          int(P.Variant.Fp16xMixed), int(P.Variant.Fp16xHybrid))
             assert two_mode == msv_two_mode, (q, second.variant)
     planted = rng.lognormal_records(150000, 290, 0.65, 2, plant=(hmm, 0.9))
     q = P.QuantParams()
@@ -546,7 +549,8 @@ def test_policy_feedback_from_saturation_and_rescoring(ora):
         first = s.scan(P.ScanOptions(alg=P.Algorithm.Ssv))
         second = s.scan(P.ScanOptions(alg=P.Algorithm.Ssv))
         np.testing.assert_array_equal(first.raw, second.raw)
-        if first.variant == int(P.Variant.Fp16x) and first.stats["recomputed"] > 0.2 * planted.count:
+        if (first.variant in (int(P.Variant.Fp16x), int(P.Variant.Fp16xMixed))
+                and first.stats["recomputed"] > 0.2 * planted.count):
             assert second.variant == int(P.Variant.Fp16)
 
 
