@@ -39,9 +39,9 @@ def main():
         s.set_profile(costs, q, hmm.lambda_, hmm.tau)
         s.set_database(db)
         for v in (P.Variant.Fp16, P.Variant.Fp16x, P.Variant.Fp16xAlt, P.Variant.Fp16xMixed,
-                  P.Variant.Dpx16, P.Variant.Swar8):
+                  P.Variant.Fp16xHybrid, P.Variant.Dpx16, P.Variant.Swar8):
             for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
-                if v == P.Variant.Fp16xAlt and alg == P.Algorithm.Ssv:
+                if v in (P.Variant.Fp16xAlt, P.Variant.Fp16xHybrid) and alg == P.Algorithm.Ssv:
                     continue
                 for L in (1, 4, 32):
                     rep = s.scan(P.ScanOptions(alg=alg, variant=v, lanes=L, threshold=0.2))
