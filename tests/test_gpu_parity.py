@@ -218,9 +218,11 @@ def test_streamed_scan_matches_resident_scan(ora, mem_ops, monkeypatch):
         s.set_profile(costs, q, hmm.lambda_, hmm.tau)
         s.set_database(db)
         for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
-            for variant, lanes in ((P.Variant.Auto, 0), (P.Variant.Fp16x, 0),
-                                   (P.Variant.Dpx16, 0), (P.Variant.Fp16, 64)):
-                o = P.ScanOptions(alg=alg, threshold=0.3, variant=variant, lanes=lanes)
+            # (explicit L=4, H=58/60: wide register rows, 12-warp CTAs)
+            for variant, lanes, rows in ((P.Variant.Auto, 0, 0), (P.Variant.Fp16x, 0, 0),
+                                         (P.Variant.Dpx16, 0, 0), (P.Variant.Fp16, 64, 0),
+                                         (P.Variant.Fp16xMixed, 4, 58), (P.Variant.Fp16x, 4, 60)):
+                o = P.ScanOptions(alg=alg, threshold=0.3, variant=variant, lanes=lanes, rows=rows)
                 base = s.scan(o)
                 for seg in (1, 3, 8, 64):
                     st = s.scan_streamed(o, seg)
@@ -444,9 +446,11 @@ def test_out_of_core_database_streams_through_the_ring(ora):
         ooc.set_database(db)
         assert not ooc.database_resident()
         for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
-            for variant in (P.Variant.Auto, P.Variant.Fp16x, P.Variant.Dpx16):
-                a = res_s.scan(P.ScanOptions(alg=alg, variant=variant, threshold=0.05))
-                b = ooc.scan(P.ScanOptions(alg=alg, variant=variant, threshold=0.05))
+            for variant, lanes, rows in ((P.Variant.Auto, 0, 0), (P.Variant.Fp16x, 0, 0),
+                                         (P.Variant.Dpx16, 0, 0), (P.Variant.Fp16xMixed, 4, 58)):
+                o = P.ScanOptions(alg=alg, variant=variant, threshold=0.05, lanes=lanes, rows=rows)
+                a = res_s.scan(o)
+                b = ooc.scan(o)
                 np.testing.assert_array_equal(a.raw, b.raw)
                 np.testing.assert_array_equal(a.passed, b.passed)
                 assert b.stats["launches"] >= 4
