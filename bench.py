@@ -502,7 +502,21 @@ def main():
     # binding resource of the dominant kernel: the shared-memory table gather
     # (128 B/clk/SM); table bytes per cell of its code form
     dom_form = ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm", "fp16xh"][geo[dom][2]]
-    table_bpc = {"fp16xm": 1.6, "fp16xh": 1.6, "swar8": 1.0}.get(dom_form, 2.0)
+    table_bpc = {"fp16xm": 1.6, "swar8": 1.0}.get(dom_form, 2.0)
+    if dom_form == "fp16xh":
+        # lazy rows' table (csrc/hybrid_layout.hpp): 16-byte slots per lane
+        # for H rows of 2 cells -- mixed slots of five rows, 16-bit slots of
+        # four, a two-row remainder slot
+        L_dom, H_dom = geo[dom][0], geo[dom][1]
+        nm = -1
+        for k in range(H_dom // 5 + 1):
+            if (H_dom - 5 * k) % 4 not in (0, 2):
+                continue
+            if L_dom <= 8 or nm < 0 or abs(10 * k - H_dom) < abs(10 * nm - H_dom):
+                nm = k
+        rest = H_dom - 5 * nm
+        slots = nm + rest // 4 + (1 if rest % 4 else 0)
+        table_bpc = round(slots * 16 / (2 * H_dom), 3)
     smem_peak = n_sm * sm_max * 1e6 * (128 / table_bpc) / 1e9
     clocks = clk.summary()
     cpu = None

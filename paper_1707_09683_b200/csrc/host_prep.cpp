@@ -15,6 +15,7 @@
 #include <omp.h>
 
 #include "lhmm_host.hpp"
+#include "hybrid_layout.hpp"
 
 namespace lhmm {
 
@@ -286,9 +287,12 @@ static uint32_t slot_rows(int variant, uint32_t H) {
 }
 
 uint64_t table_bytes_for(int variant, uint32_t L, uint32_t H, bool replicate) {
-    if (variant == LHMM_VARIANT_FP16XH)  // 16-bit exact-mode image + mixed lazy-mode image
-        return table_bytes_for(LHMM_VARIANT_FP16X, L, H, replicate) +
-               table_bytes_for(LHMM_VARIANT_FP16XM, L, H, replicate);
+    if (variant == LHMM_VARIANT_FP16XH) {  // 16-bit exact-mode image + lazy-mode image
+        uint32_t P2, copies2, cs2;
+        strides_for(L, uint32_t(4 * hyb_slots(int(H), int(L))), P2, copies2, cs2);
+        const uint64_t w2 = copies2 > 1 ? uint64_t(copies2 - 1) * cs2 + 23ull * P2 : 23ull * P2;
+        return table_bytes_for(LHMM_VARIANT_FP16X, L, H, replicate) + (w2 * 4 + 15) / 16 * 16;
+    }
     (void)replicate;
     uint32_t P, copies, cs;
     strides_for(L, slot_rows(variant, H), P, copies, cs);
@@ -329,16 +333,54 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
     if (variant == LHMM_VARIANT_FP16XH) {
         // hybrid two-mode MSV: the FP16X image (exact rows) followed by the
         // FP16XM image (lazy rows)
-        TableImage a, b;
+        TableImage a;
         build_table(costs, m, LHMM_VARIANT_FP16X, alg, L, H, replicate, dbias, a);
-        build_table(costs, m, LHMM_VARIANT_FP16XM, alg, L, H, replicate, dbias, b);
+        // lazy image (hybrid_layout.hpp): mixed five-row slots, four-row
+        // 16-bit slots, a two-row remainder slot; entries are the costs
+        // (cells negated, see Fp16SatHybrid)
+        const int nm = hyb_mixed_groups(int(H), int(L));
+        const int n4 = (int(H) - 5 * nm) / 4;
+        uint32_t P2, copies2, cs2;
+        strides_for(L, uint32_t(4 * hyb_slots(int(H), int(L))), P2, copies2, cs2);
+        const uint64_t w2 = copies2 > 1 ? uint64_t(copies2 - 1) * cs2 + 23ull * P2 : 23ull * P2;
+        std::vector<uint32_t> b((w2 * 4 + 15) / 16 * 4, 0u);
+        auto cost_at = [&](uint32_t x, uint32_t oig, uint32_t c, int h) -> uint32_t {
+            const uint64_t node = uint64_t(2 * oig + c) * H + uint64_t(h) + 1;
+            return (h >= int(H) || node > m || x > kUnknown) ? 0xffu
+                                                              : costs[(node - 1) * 21 + x];
+        };
+        for (uint32_t x = 0; x < 23; ++x)
+            for (uint32_t oig = 0; oig < L; ++oig) {
+                for (int s = 0; s < hyb_slots(int(H), int(L)); ++s) {
+                    uint32_t slot[4] = {0, 0, 0, 0};
+                    if (s < nm) {
+                        for (int k = 0; k < 5; ++k)
+                            for (uint32_t c = 0; c < 2; ++c) {
+                                const uint32_t v = cost_at(x, oig, c, 5 * s + k);
+                                if (k < 3)
+                                    slot[k] |= v << (16 * c);
+                                else
+                                    slot[3] |= v << (8 * (2 * (k - 3) + c));
+                            }
+                    } else {
+                        const int h0 = 5 * nm + 4 * (s - nm);
+                        const int nw = s < nm + n4 ? 4 : 2;
+                        for (int k = 0; k < nw; ++k)
+                            for (uint32_t c = 0; c < 2; ++c)
+                                slot[k] |= cost_at(x, oig, c, h0 + k) << (16 * c);
+                    }
+                    const size_t at = size_t(x) * P2 + size_t(s) * 4 * L + 4 * oig;
+                    for (uint32_t g = 0; g < copies2; ++g)
+                        for (int w = 0; w < 4; ++w) b[size_t(g) * cs2 + at + w] = slot[w];
+                }
+            }
         out.res_stride = a.res_stride;
         out.copy_stride = a.copy_stride;
         out.second_off = uint32_t(a.words.size());
-        out.res_stride2 = b.res_stride;
-        out.copy_stride2 = b.copy_stride;
+        out.res_stride2 = P2;
+        out.copy_stride2 = copies2 > 1 ? cs2 : 0;
         out.words = std::move(a.words);
-        out.words.insert(out.words.end(), b.words.begin(), b.words.end());
+        out.words.insert(out.words.end(), b.begin(), b.end());
         return;
     }
     const uint32_t cpw = cells_per_word(variant);

@@ -1,0 +1,43 @@
+// Lazy-row table layout of the hybrid two-mode MSV form (FP16XH), shared by
+// the kernel (lhmm_kernel.cuh) and the table builder (host_prep.cpp).
+// Per lane the H register rows are read in 16-byte slots: NM "mixed" slots
+// of five rows (three u16 pairs + four cost bytes) at the bottom, then
+// 16-bit slots of four rows, then (H = 2 mod 4 remainder) one slot holding
+// the last two rows.  NM trades table bytes (fewer with more mixed slots)
+// against byte unpacks (PRMT, ALU): all mixed for L <= 8, about half the rows
+// for L >= 16, where the per-row shuffles and reductions already load the ALU.
+#pragma once
+
+#ifdef __CUDACC__
+#define LHMM_HD __host__ __device__
+#else
+#define LHMM_HD
+#endif
+
+namespace lhmm {
+
+LHMM_HD constexpr int hyb_abs(int v) { return v < 0 ? -v : v; }
+
+LHMM_HD constexpr int hyb_mixed_groups(int H, int L) {
+    // L <= 8 (several sequences per warp): as many mixed slots as the split
+    // allows -- measured fastest there; L >= 16: about half the rows
+    int best = -1;
+    for (int nm = 0; 5 * nm <= H; ++nm) {
+        const int r = (H - 5 * nm) % 4;
+        if (r != 0 && r != 2) continue;
+        if (L <= 8)
+            best = nm;
+        else if (best < 0 || hyb_abs(10 * nm - H) < hyb_abs(10 * best - H))
+            best = nm;
+    }
+    return best;
+}
+
+// slots per lane of the lazy image
+LHMM_HD constexpr int hyb_slots(int H, int L) {
+    const int nm = hyb_mixed_groups(H, L);
+    const int rest = H - 5 * nm;
+    return nm + rest / 4 + (rest % 4 ? 1 : 0);
+}
+
+}  // namespace lhmm

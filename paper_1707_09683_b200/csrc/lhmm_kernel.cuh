@@ -47,6 +47,8 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include "hybrid_layout.hpp"
+
 namespace lhmm {
 
 constexpr uint32_t kFull = 0xffffffffu;
@@ -851,7 +853,50 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                 up = inject_here ? V::template inject<LAZY>(st) : g[stop];
             }
             constexpr int GW = mode_group_width<V, LAZY>();
-            if constexpr (GW == 5) {
+            if constexpr (is_hybrid<V>::value && LAZY) {
+                // hybrid lazy rows (hybrid_layout.hpp): NM five-row mixed slots,
+                // then four-row 16-bit slots, then a two-row remainder slot
+                constexpr int NM = hyb_mixed_groups(H, L);
+                constexpr int R4 = H - 5 * NM;
+                constexpr int N4 = R4 / 4;
+                static_assert(NM >= 0 && (R4 % 4 == 0 || R4 % 4 == 2), "hybrid row split");
+                if constexpr (R4 % 4 == 2) {
+                    constexpr int slot = NM + N4;
+                    const uint4 c = *reinterpret_cast<const uint4*>(tp + slot * 4 * TL);
+                    const uint32_t cw[2] = {c.x, c.y};
+#pragma unroll
+                    for (int k = 1; k >= 0; --k) {
+                        const int h = 5 * NM + 4 * N4 + k;
+                        const int sl = ((h - 1 - r) % H + H) % H;
+                        const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
+                        g[sl] = V::template cell<true, false, 0>(in, cw[k], st);
+                    }
+                }
+#pragma unroll
+                for (int j = N4 - 1; j >= 0; --j) {
+                    const uint4 c = *reinterpret_cast<const uint4*>(tp + (NM + j) * 4 * TL);
+                    const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+                    for (int k = 3; k >= 0; --k) {
+                        const int h = 5 * NM + 4 * j + k;
+                        const int sl = ((h - 1 - r) % H + H) % H;
+                        const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
+                        g[sl] = V::template cell<true, false, 0>(in, cw[k], st);
+                    }
+                }
+#pragma unroll
+                for (int hg = NM - 1; hg >= 0; --hg) {
+                    const uint4 c = *reinterpret_cast<const uint4*>(tp + hg * 4 * TL);
+                    const uint32_t cw[5] = {c.x, c.y, c.z, V::unpack(c.w, 0), V::unpack(c.w, 1)};
+#pragma unroll
+                    for (int k = 4; k >= 0; --k) {
+                        const int h = 5 * hg + k;
+                        const int sl = ((h - 1 - r) % H + H) % H;
+                        const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
+                        g[sl] = V::template cell<true, false, 0>(in, cw[k], st);
+                    }
+                }
+            } else if constexpr (GW == 5) {
                 // mixed tables (Fp16Mixed, Fp16SatMixed): five words per
                 // 16-byte slot, three 16-bit-pair words and one word of four
                 // bytes; with H = 5k + r (r <= 3) a top slot of r 16-bit-pair
