@@ -378,17 +378,23 @@ def wrap_model(alg, costs, m, seq, q, base):
 
 
 @pytest.mark.parametrize("variant", [P.Variant.Fp16, P.Variant.Dpx16, P.Variant.Swar8,
-                                     P.Variant.Fp16x, P.Variant.Fp16xAlt],
+                                     P.Variant.Fp16x, P.Variant.Fp16xAlt, P.Variant.Fp16xMixed,
+                                     P.Variant.Fp16xHybrid],
                          ids=lambda v: v.name)
 @pytest.mark.parametrize("alg", [P.Algorithm.Msv, P.Algorithm.Ssv], ids=lambda a: a.name)
 def test_paper_wrap_mode(ora, variant, alg):
     """The non-normative wrap study mode runs, matches its model, and differs
     from the normative (oracle-exact) -inf injection on a consensus-heavy
     instance (test_engine.cpp:265-278)."""
+    if variant == P.Variant.Fp16xHybrid and alg == P.Algorithm.Ssv:
+        pytest.skip("the hybrid is an MSV form (SSV runs FP16XM, tested above)")
     cpw = 4 if variant == P.Variant.Swar8 else 2
     q = P.QuantParams(3.0, 120, 3, 20, 20)
     differs = False
-    for L, H in ((1, 8), (2, 8), (8, 4), (32, 4)):
+    geoms = {P.Variant.Fp16xMixed: ((1, 10), (2, 10), (8, 5), (32, 5)),
+             P.Variant.Fp16xHybrid: ((1, 8), (2, 10), (8, 8), (32, 10))}.get(
+                 variant, ((1, 8), (2, 8), (8, 4), (32, 4)))
+    for L, H in geoms:
         m = cpw * L * H
         rng = P.Rng(38 + L)
         hmm = rng.random_profile(m)
