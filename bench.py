@@ -1,18 +1,36 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 MSV/SSV filter scan (BASELINE.json metric: MSV/SSV
-GCUPS, device-timed, vs model length).
+"""Benchmark of the B200 MSV/SSV filter scan (BASELINE.json metric: "MSV/SSV
+GCUPS (device-timed) vs model length").
 
-Default workload = BASELINE.json configs[1]: SSV with synthetic models
+Headline (`value`) = BASELINE.json configs[1], C2: SSV with synthetic models
 M = 48 / 400 / 1000 over 1M Swiss-Prot-like synthetic sequences per GPU
 (synth::lognormal_records(1e6, 290, 0.65, 2), seed 0x5EED; models
-synth::random_profile(seed 7000+M)), weak scaling: N GPUs scan N x 1M
-sequences, sharded by residue count, raw/pass gathered to rank 0 over NCCL.
-One step = the three SSV scans over the resident database (every cell
-computed; no early exit).  GCUPS = real residues x M / device seconds.
+synth::random_profile(seed 7000+M)).  One step = the three SSV scans over the
+resident database; every cell is computed (no early exit).  GCUPS = real
+residues x M / device seconds.  N>1: weak scaling (N x 1M sequences), the
+database sharded by residue count, raw/pass gathered to rank 0.
+
+Beside the headline the same JSON line carries, by default (`--legs`):
+  sweep   C5: M = 48..2405, MSV and SSV at the default QuantParams and MSV at
+          the non-saturating QuantParams{3,120,3,20,20} (test_oracle.cpp:95-96
+          style), per scan: GCUPS, fraction of the 18.6 TCUPS packed-integer
+          roofline, geometry, code form, lazy-row share and
+          saturated share -- the saturation-dependent speed-up reported apart.
+          The M = 2405 MSV entry is C3.
+  c1      C1: MSV M=200 vs 10k random sequences (seed 0xC1, 5% planted
+          motifs), default and non-saturating params, many timed steps with
+          the L2 flushed between them.
+  verify  parity: a fixed-stride sample (>= 20k sequences; C1 in full) of the
+          raw bytes and pass bits of EVERY timed scan compared with the
+          reference library's own scalar oracle and finalize_hit
+          (oracle/_ref, test infrastructure) -> "parity": {checked, mismatches}.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--workload c2|c1|c3|c4|sweep] [--variant auto|dpx16|fp16|swar8]
+                  [--workload c2|c1|c3|c4|sweep] [--legs sweep,c1,verify|none]
 
+`--impl reference` times the reference's own CPU engine (oracle/_ref,
+lanehmm::scan_database) on the host cores, generating its inputs with the
+reference's own generators -- that process never loads the product library.
 N>1: launched by torch.distributed.run, one rank per GPU (nccl).
 """
 from __future__ import annotations
@@ -33,23 +51,29 @@ sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-CELLS_PER_CLK_PER_SM = 64  # packed-integer-SIMD roofline (BASELINE.md §4)
+CELLS_PER_CLK_PER_SM = 64  # packed-integer-SIMD roofline (SURVEY §8(d))
 L2_BYTES = 126 * 2**20     # B200 L2
+METRIC = "MSV/SSV GCUPS (device-timed) vs model length"
+DEFAULT_Q = (3.0, 195, 3, 3, 3)
+NONSAT_Q = (3.0, 120, 3, 20, 20)   # MSV raw ~117-131: scores that do not saturate
+THRESHOLD = 0.022
+SWISSPROT = ("lognormal", 0x5EED, 290.0, 0.65, 2)
+SWEEP_M = (48, 100, 200, 400, 800, 1000, 1500, 2000, 2405)
 
 WORKLOADS = {
     # name: (description, alg, models, nseq per GPU, generator)
     "c2": ("SSV, synthetic models M=48/400/1000 vs 1M Swiss-Prot-like synthetic sequences per GPU",
-           "ssv", (48, 400, 1000), 1_000_000, ("lognormal", 290.0, 0.65, 2)),
-    "c1": ("MSV, M=200 vs 10k random sequences (mean ~350 aa)",
-           "msv", (200,), 10_000, ("uniform", 50, 650)),
+           "ssv", (48, 400, 1000), 1_000_000, SWISSPROT),
+    "c1": ("MSV, M=200 vs 10k random sequences (mean ~350 aa, 5% planted motifs)",
+           "msv", (200,), 10_000, ("uniform_planted", 0xC1, 50, 650, 0.05)),
     "c3": ("MSV, M=2405 vs 1M Swiss-Prot-like synthetic sequences per GPU",
-           "msv", (2405,), 1_000_000, ("lognormal", 290.0, 0.65, 2)),
+           "msv", (2405,), 1_000_000, SWISSPROT),
     "c4": ("MSV+SSV, M=200 vs env_nr-like synthetic sequences (lognormal median 170, sigma 0.55)",
-           "both", (200,), 6_250_000, ("lognormal", 170.0, 0.55, 2)),
+           "both", (200,), 6_250_000, ("lognormal", 0x5EED, 170.0, 0.55, 2)),
     "sweep": ("MSV+SSV, M=48..2405 sweep vs 1M Swiss-Prot-like synthetic sequences per GPU",
-              "both", (48, 100, 200, 400, 800, 1000, 1500, 2000, 2405), 1_000_000,
-              ("lognormal", 290.0, 0.65, 2)),
+              "both", SWEEP_M, 1_000_000, SWISSPROT),
 }
+VARIANTS = ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm", "fp16xh"]
 
 
 def log(*a):
@@ -61,23 +85,102 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def make_db(P, gen, nseq, seed=0x5EED):
-    rng = P.Rng(seed)
+def qstr(q):
+    return "QuantParams{%g,%d,%d,%d,%d}" % q
+
+
+# ---------------------------------------------------------------------------
+# inputs: the same synth:: streams through either generator API -- the
+# product's (P.Rng, b200 arm) or the reference library's (oracle.Reference,
+# reference arm); tests/test_host.py pins them bit-identical
+
+class ProductGen:
+    def __init__(self, P):
+        self.P = P
+
+    def rng(self, seed):
+        return self.P.Rng(seed)
+
+    def profile(self, rng, m):
+        h = rng.random_profile(m)
+        return np.ascontiguousarray(h.match_scores, np.float64).reshape(-1), h.lambda_, h.tau
+
+    def records(self, rng, gen, n, plant):
+        if gen[0] == "lognormal":
+            db = rng.lognormal_records(n, gen[2], gen[3], gen[4])
+        else:
+            hmm = self.P.ProfileHMM("plant", plant[0].size // 20, plant[0].reshape(-1, 20))
+            db = rng.random_records(n, gen[2], gen[3], plant=(hmm, gen[4]))
+        return db.residues, db.offsets
+
+    def quantize(self, scores, q):
+        hmm = self.P.ProfileHMM("m", scores.size // 20, scores.reshape(-1, 20))
+        return self.P.quantize_emissions(hmm, self.P.QuantParams(*q)).bytes
+
+
+class ReferenceGen:
+    def __init__(self, ref, oracle):
+        self.ref, self.oracle = ref, oracle
+
+    def rng(self, seed):
+        return self.ref.rng(seed)
+
+    def profile(self, rng, m):
+        return rng.random_profile(m)
+
+    def records(self, rng, gen, n, plant):
+        if gen[0] == "lognormal":
+            return rng.lognormal_records(n, gen[2], gen[3], gen[4])
+        return rng.random_records(n, gen[2], gen[3], plant=(plant[0], gen[4]))
+
+    def quantize(self, scores, q):
+        return self.ref.quantize(scores, self.oracle.QuantParams(*q))
+
+
+def make_inputs(api, gen, nseq, models_m):
+    """(residues, offsets, {m: (scores, lambda, tau)}).  Swiss-Prot-like and
+    env_nr-like sets: records from seed gen[1], each model from seed 7000+M
+    (SURVEY §8(d)).  C1: one generator for the model, then the records, then
+    the planted motifs (seed 0xC1)."""
+    models = {}
     if gen[0] == "lognormal":
-        return rng.lognormal_records(nseq, gen[1], gen[2], gen[3])
-    return rng.random_records(nseq, gen[1], gen[2])
+        res, off = api.records(api.rng(gen[1]), gen, nseq, None)
+        for m in models_m:
+            models[m] = api.profile(api.rng(7000 + m), m)
+    else:
+        rng = api.rng(gen[1])
+        models[models_m[0]] = api.profile(rng, models_m[0])
+        res, off = api.records(rng, gen, nseq, models[models_m[0]])
+    return (np.ascontiguousarray(res, np.uint8), np.ascontiguousarray(off, np.uint64), models)
 
 
-def make_models(P, models, q):
-    out = []
-    for m in models:
-        hmm = P.Rng(7000 + m).random_profile(m)
-        out.append((hmm, P.quantize_emissions(hmm, q)))
-    return out
+def flat_subset(res, off, idx):
+    lens = (off[idx + 1] - off[idx]).astype(np.int64)
+    o = np.zeros(idx.size + 1, np.uint64)
+    o[1:] = np.cumsum(lens)
+    r = np.concatenate([res[int(off[k]):int(off[k + 1])] for k in idx]) if idx.size else \
+        np.zeros(0, np.uint8)
+    return r, o
+
+
+def sample_idx(n, sample_n):
+    return np.arange(0, n, max(1, n // max(1, sample_n)), dtype=np.int64)[:sample_n]
 
 
 def algs_of(wl_alg):
     return {"ssv": ["ssv"], "msv": ["msv"], "both": ["msv", "ssv"]}[wl_alg]
+
+
+def workload_config(name, desc, models_m, algs, nseq_total, residues, world, packed_bytes=None):
+    """The `config` object -- identical for both arms of the same run."""
+    l2 = ("inputs larger than L2 (packed database > 126 MB per GPU)"
+          if residues / max(world, 1) > L2_BYTES else
+          "L2 flushed between timed steps (256 MB write outside the timed windows)")
+    return {"workload": desc, "name": name, "models": list(models_m), "algorithms": algs,
+            "sequences": int(nseq_total), "residues": int(residues), "threshold": THRESHOLD,
+            "quant": qstr(DEFAULT_Q), "data": "synthetic (lanehmm synth:: streams, seeds as in "
+            "SURVEY.md §8(d))", "parallelism": f"{world} rank(s); sequences sharded by residue "
+            "count, raw+pass gathered to rank 0", "l2": l2, "early_exit": False}
 
 
 class ClockSampler:
@@ -94,10 +197,11 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                 "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE,
                 stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.15)  # the first sample lands before the timed work starts
         except Exception:
             self.proc = None
         return self
@@ -142,97 +246,156 @@ def cpu_model():
     return "unknown"
 
 
-def cpu_reference_gcups(P, db, models, algs, q, sample_n, reps=1):
+def cpu_reference_gcups(res, off, models, algs, q, sample_n, also=True):
     """The reference CPU filter (oracle/_ref: lanehmm::scan_database with the
     reference geometry policy, all host threads), or the oracle port when the
-    reference library is absent, on a fixed-stride sample of the workload."""
+    reference library is absent, on a fixed-stride sample of the workload.
+    models: [(m, scores, lam, tau, costs)]."""
     import oracle
-    stride = max(1, db.count // sample_n)
-    idx = np.arange(0, db.count, stride)[:sample_n]
-    sample = db.subset(idx)
+    n = off.size - 1
+    idx = sample_idx(n, sample_n)
+    sres, soff = flat_subset(res, off, idx)
+    sresid = int(soff[-1])
     cores = os.cpu_count() or 1
-    oq = oracle.QuantParams(q.scale, q.base, q.dbias, q.tec, q.tjb)
+    oq = oracle.QuantParams(*q)
     try:
         ref = oracle.Reference()
         kind = "reference"
     except FileNotFoundError:
         ref, kind = None, "port"
-        ora = oracle.Oracle()
-    best = None
-    for _ in range(reps):
-        cells, secs = 0, 0.0
-        for hmm, costs in models:
-            for a in algs:
-                alg = 0 if a == "msv" else 1
-                if ref is not None:
-                    _, s, _ = ref.scan_database(alg, hmm.match_scores.reshape(-1), hmm.lambda_,
-                                                hmm.tau, costs.bytes, oq, sample.residues,
-                                                sample.offsets, cores)
-                else:
-                    t0 = time.perf_counter()
-                    ora.scan_flat(alg, costs.bytes, sample.residues, sample.offsets, oq, cores)
-                    s = time.perf_counter() - t0
-                secs += s
-                cells += sample.total_residues() * hmm.length
-        g = cells / secs / 1e9
-        best = g if best is None else max(best, g)
-    desc = (f"fixed-stride sample of {sample.count} of {db.count} sequences "
-            f"({sample.total_residues()} residues), models M={[h.length for h, _ in models]}, "
-            f"{'+'.join(algs)}; lanehmm::scan_database with reference geometry, "
-            f"{cores} threads, host CPU '{cpu_model()}'" if kind == "reference" else
-            f"fixed-stride sample of {sample.count} sequences, C oracle port on {cores} threads")
-    # the other two CPU figures SURVEY §8(d) lists: the scalar oracle
-    # (oracle/oracle.c, the restatement of scalar_msv / scalar_ssv) on all
-    # host threads and on one core, on smaller samples
-    also = {}
     ora = oracle.Oracle()
-    for label, n_s, thr in (("scalar_oracle_all_threads", 2000, cores),
-                            ("scalar_oracle_1_core", 200, 1)):
-        sub = db.subset(np.arange(0, db.count, max(1, db.count // n_s))[:n_s])
-        cells, secs = 0, 0.0
-        for hmm, costs in models:
-            for a in algs:
+    cells, secs = 0, 0.0
+    for m, scores, lam, tau, costs in models:
+        for a in algs:
+            alg = 0 if a == "msv" else 1
+            if ref is not None:
+                _, s, _ = ref.scan_database(alg, scores, lam, tau, costs, oq, sres, soff, cores)
+            else:
                 t0 = time.perf_counter()
-                ora.scan_flat(0 if a == "msv" else 1, costs.bytes, sub.residues, sub.offsets, oq,
-                              thr)
-                secs += time.perf_counter() - t0
-                cells += sub.total_residues() * hmm.length
-        also[label] = {"value": round(cells / secs / 1e9, 3), "threads": thr,
-                       "sample_sequences": int(sub.count)}
-    return {"value": round(best, 3), "unit": "GCUPS", "cores": cores, "kind": kind,
-            "sample": desc, "also": also}
+                ora.scan_flat(alg, costs, sres, soff, oq, cores)
+                s = time.perf_counter() - t0
+            secs += s
+            cells += sresid * m
+    desc = (f"fixed-stride sample of {idx.size} of {n} sequences ({sresid} residues), "
+            f"models M={[x[0] for x in models]}, {'+'.join(algs)}; "
+            + ("lanehmm::scan_database (reference library, reference geometry)" if ref else
+               "C oracle port (oracle/oracle.c)")
+            + f", {cores} threads, host CPU '{cpu_model()}'")
+    out = {"value": round(cells / secs / 1e9, 3), "unit": "GCUPS", "cores": cores, "kind": kind,
+           "sample": desc}
+    if also:
+        # the other two CPU figures SURVEY §8(d) lists: the scalar oracle on
+        # all host threads and on one core, on smaller samples
+        extra = {}
+        for label, n_s, thr in (("scalar_oracle_all_threads", 2000, cores),
+                                ("scalar_oracle_1_core", 200, 1)):
+            r2, o2 = flat_subset(res, off, sample_idx(n, n_s))
+            c2, s2 = 0, 0.0
+            for m, _, _, _, costs in models:
+                for a in algs:
+                    t0 = time.perf_counter()
+                    ora.scan_flat(0 if a == "msv" else 1, costs, r2, o2, oq, thr)
+                    s2 += time.perf_counter() - t0
+                    c2 += int(o2[-1]) * m
+            extra[label] = {"value": round(c2 / s2 / 1e9, 3), "threads": thr,
+                            "sample_sequences": int(o2.size - 1)}
+        out["also"] = extra
+    return out
 
 
-def run_reference(args, wl):
+# ---------------------------------------------------------------------------
+# reference arm
+
+def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    import paper_1707_09683_b200 as P  # generators only (same streams as synth::*)
+    import oracle  # the reference library only; the product .so is never loaded
+    ref = oracle.Reference()
+    api = ReferenceGen(ref, oracle)
     desc, wl_alg, models_m, nseq, gen = WORKLOADS[args.workload]
-    q = P.QuantParams()
-    db = make_db(P, gen, nseq * world)
-    models = make_models(P, models_m, q)
     algs = algs_of(wl_alg)
-    sample_n = args.ref_sample
-    vals = []
+    res, off, profs = make_inputs(api, gen, nseq * world, models_m)
+    models = [(m, *profs[m], api.quantize(profs[m][0], DEFAULT_Q)) for m in models_m]
+    vals, r = [], None
     for i in range(args.warmup + args.steps):
-        r = cpu_reference_gcups(P, db, models, algs, q, sample_n)
+        r = cpu_reference_gcups(res, off, models, algs, DEFAULT_Q, args.ref_sample,
+                                also=i == args.warmup + args.steps - 1)
         if i >= args.warmup:
             vals.append(r["value"])
     v = statistics.median(vals) if vals else r["value"]
-    cfg = {"workload": desc, "models": list(models_m), "algorithms": algs,
-           "sequences": int(db.count), "residues": int(db.total_residues()),
-           "data": "synthetic (lanehmm synth:: streams)"}
-    line = {"metric": "MSV/SSV GCUPS (device-timed) vs model length", "value": v, "unit": "GCUPS",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "impl": "reference",
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic", "config": cfg,
-            "cpu_baseline": {**r, "value": v},
+    cfg = workload_config(args.workload, desc, models_m, algs, off.size - 1, int(off[-1]), world)
+    line = {"metric": METRIC, "value": v, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "impl": "reference", "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": cfg, "cpu_baseline": {**r, "value": v},
             "e2e": {"value": v, "unit": "GCUPS", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
+
+# ---------------------------------------------------------------------------
+# parity (verify leg): the reference library's scalar oracle + finalize_hit
+
+class Verifier:
+    """Collects (scan key, sampled device outputs) and checks them all against
+    oracle/_ref (the reference's scalar_msv / scalar_ssv and finalize_hit) at
+    the end, outside every timed region."""
+
+    def __init__(self, res, off, sample_n):
+        self.res, self.off, self.n = res, off, off.size - 1
+        self.idx = sample_idx(self.n, sample_n)
+        self.sres, self.soff = flat_subset(res, off, self.idx)
+        self.items = []     # (key, leg, raw sample, pass sample)
+        self.models = {}    # key -> (alg, costs, q, lam, tau)
+
+    def add(self, key, leg, alg, costs, q, lam, tau, raw_full, pass_full):
+        self.models[key] = (alg, costs, q, lam, tau)
+        self.items.append((key, leg, np.asarray(raw_full)[self.idx],
+                           np.asarray(pass_full)[self.idx].astype(np.uint8)))
+
+    def run(self):
+        import oracle
+        t0 = time.perf_counter()
+        try:
+            chk = oracle.Reference()
+            checker = ("oracle/_ref: the reference library's scalar_msv/scalar_ssv "
+                       "(src/oracle.cpp:41-91) + finalize_hit pass rule (src/engine.cpp:59-81, 617)")
+        except FileNotFoundError:
+            chk, checker = None, "oracle/oracle.c (C restatement; oracle/_ref absent)"
+            ora = oracle.Oracle()
+        want = {}
+        for key, (alg, costs, q, lam, tau) in self.models.items():
+            oq = oracle.QuantParams(*q)
+            a = 0 if alg == "msv" else 1
+            if chk is not None:
+                raw = chk.scalar_flat(a, costs, self.sres, self.soff, oq)
+                ps = chk.pass_flat(a, raw, self.soff, lam, tau, oq, THRESHOLD)
+            else:
+                raw = ora.scan_flat(a, costs, self.sres, self.soff, oq, os.cpu_count() or 1)
+                lens = np.diff(self.soff)
+                ps = np.array([ora.passes(int(r), int(ln), lam, tau, oq, a, THRESHOLD)
+                               for r, ln in zip(raw, lens)], np.uint8)
+            want[key] = (raw, ps)
+        checked, bad, per_leg = 0, 0, {}
+        for key, leg, raw, ps in self.items:
+            wr, wp = want[key]
+            mism = int(np.count_nonzero(raw != wr)) + int(np.count_nonzero(ps != wp))
+            checked += 2 * raw.size
+            bad += mism
+            d = per_leg.setdefault(leg, {"scans": 0, "checked": 0, "mismatches": 0})
+            d["scans"] += 1
+            d["checked"] += 2 * raw.size
+            d["mismatches"] += mism
+        return {"checked": checked, "mismatches": bad, "sequences_per_scan": int(self.idx.size),
+                "of": int(self.n), "scans": len(self.items), "legs": per_leg,
+                "what": "raw byte + pass bit of a fixed-stride sample of every timed scan "
+                        "(C1: every sequence)", "checker": checker,
+                "seconds": round(time.perf_counter() - t0, 2)}
+
+
+# ---------------------------------------------------------------------------
 
 def main():
     ap = argparse.ArgumentParser()
@@ -241,10 +404,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--variant", default="auto", choices=["auto", "dpx16", "fp16", "swar8", "fp16x",
-                                                       "fp16xalt", "fp16xm", "fp16xh"])
+    ap.add_argument("--legs", default="sweep,c1,verify",
+                    help="extra legs beside the headline: sweep, c1, verify (or 'none')")
+    ap.add_argument("--variant", default="auto", choices=VARIANTS)
     ap.add_argument("--nseq", type=int, default=0, help="override sequences per GPU")
     ap.add_argument("--ref-sample", type=int, default=20000)
+    ap.add_argument("--verify-sample", type=int, default=20000)
+    ap.add_argument("--sweep-steps", type=int, default=3)
+    ap.add_argument("--c1-steps", type=int, default=1500)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--models", default="", help="override model lengths, e.g. 1000,2405")
@@ -269,7 +436,8 @@ def main():
             w[1] = args.algs
         WORKLOADS[args.workload] = tuple(w)
     if args.impl == "reference":
-        return run_reference(args, None)
+        return run_reference(args)
+    legs = set() if args.legs in ("", "none") else set(args.legs.split(","))
 
     import torch
     import paper_1707_09683_b200 as P
@@ -289,42 +457,62 @@ def main():
             dist.init_process_group(args.backend)
             comm_dev = torch.device("cpu")
     desc, wl_alg, models_m, nseq, gen = WORKLOADS[args.workload]
-    variant = {"auto": P.Variant.Auto, "dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16,
-               "swar8": P.Variant.Swar8, "fp16x": P.Variant.Fp16x,
-               "fp16xalt": P.Variant.Fp16xAlt, "fp16xm": P.Variant.Fp16xMixed, "fp16xh": P.Variant.Fp16xHybrid}[args.variant]
-    q = P.QuantParams()
+    variant = getattr(P.Variant, {"auto": "Auto", "dpx16": "Dpx16", "fp16": "Fp16",
+                                  "swar8": "Swar8", "fp16x": "Fp16x", "fp16xalt": "Fp16xAlt",
+                                  "fp16xm": "Fp16xMixed", "fp16xh": "Fp16xHybrid"}[args.variant])
     algs = algs_of(wl_alg)
-    threshold = 0.022
+    api = ProductGen(P)
+    # the sweep leg shares the Swiss-Prot-like database of C2/C3
+    sweep_on = "sweep" in legs and gen == SWISSPROT
+    all_m = sorted(set(models_m) | (set(SWEEP_M) if sweep_on else set()))
 
     t0 = time.perf_counter()
-    db = make_db(P, gen, nseq * world)
-    models = make_models(P, models_m, q)
+    res, off, profs = make_inputs(api, gen, nseq * world, all_m)
+    db = P.SequenceDB(res, off)
     t_gen = time.perf_counter() - t0
 
     stream = torch.cuda.current_stream()
     s = P.Scanner(local)
     s.set_stream(stream.cuda_stream)
     if args.db_budget:
-        # out-of-core mode: the packed database stays in pinned host memory and
-        # every scan streams it through a ring of device slots
         s.set_db_budget(args.db_budget)
     t0 = time.perf_counter()
     n_local = s.set_database(db, rank, world)
     t_pack = time.perf_counter() - t0
     gidx = torch.from_numpy(s.shard_indices().astype(np.int64)).cuda()
     dbstats = s.database_stats()
-    pids = [s.add_profile(c, q, h.lambda_, h.tau) for h, c in models]
     info = s.device_info()
-    scans = [(pid, hmm.length, a) for pid, (hmm, _) in zip(pids, models) for a in algs]
-    outs = {k: (torch.empty(max(n_local, 1), dtype=torch.uint8, device="cuda"),
-                torch.empty(max(n_local, 1), dtype=torch.uint8, device="cuda"))
-            for k in range(len(scans))}
+    peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = info["sm_count"]
+    peak_gcups = n_sm * sm_max * 1e6 * CELLS_PER_CLK_PER_SM / 1e9  # per GPU
+
+    pid_cache = {}
+
+    def profile_id(m, q):
+        if (m, q) not in pid_cache:
+            sc, lam, tau = profs[m]
+            costs = api.quantize(sc, q)
+            pid = s.add_profile(P.CostMatrix(m, costs), P.QuantParams(*q), lam, tau)
+            pid_cache[(m, q)] = (pid, costs, lam, tau)
+        return pid_cache[(m, q)]
 
     def opt_for(a):
         return P.ScanOptions(alg=P.Algorithm.Msv if a == "msv" else P.Algorithm.Ssv,
                              variant=variant, lanes=args.lanes, rows=args.rows,
-                             threshold=threshold)
+                             threshold=THRESHOLD)
 
+    verifier = None
+    if "verify" in legs and rank == 0:
+        verifier = Verifier(res, off, args.verify_sample)
+
+    scans = [(m, a) for m in models_m for a in algs]
+    for m, _ in scans:
+        profile_id(m, DEFAULT_Q)
+    keep = min(args.steps, 50)  # per-step output buffers kept for the parity check
+    outs = {(k, j): (torch.empty(max(n_local, 1), dtype=torch.uint8, device="cuda"),
+                     torch.empty(max(n_local, 1), dtype=torch.uint8, device="cuda"))
+            for k in range(len(scans)) for j in range(keep)}
     per_launch = {k: [] for k in range(len(scans))}
     geo = {}
 
@@ -342,17 +530,17 @@ def main():
             peer = None
     gather_mode = "fused peer stores (CUDA IPC)" if peer else "torch.distributed gather"
 
-    def step(record):
+    def step(j, record):
         launches = 0
-        for k, (pid, m, a) in enumerate(scans):
-            s.select_profile(pid)
+        for k, (m, a) in enumerate(scans):
+            s.select_profile(profile_id(m, DEFAULT_Q)[0])
             if peer is not None:
                 st = s.scan_device_global(opt_for(a), peer.raw(k), peer.passed(k))
             else:
-                st = s.scan_device(opt_for(a), outs[k][0].data_ptr(), outs[k][1].data_ptr())
+                o = outs[(k, j % keep)]
+                st = s.scan_device(opt_for(a), o[0].data_ptr(), o[1].data_ptr())
             launches += st["launches"]
-            geo[k] = (st["lanes"], st["rows"], st["variant"], st["grid"], st["smem_bytes"],
-                      st["recomputed"])
+            geo[k] = st
             if record:
                 per_launch[k].append(st["device_ms"])
         return launches
@@ -360,10 +548,9 @@ def main():
     gathered = {"validated": False}
 
     def gather_results():
-        """Per-sequence raw + pass bytes of every scan to rank 0 (one gather per
-        scan; NCCL over NVLink on the box, gloo when ranks share a GPU).  With
-        the fused gather the scans already wrote them; the first call checks
-        that every sequence of every scan arrived."""
+        """Per-sequence raw + pass bytes of every scan to rank 0.  With the
+        fused gather the scans already wrote them; the first call checks that
+        every sequence of every scan arrived."""
         if world == 1:
             return
         if peer is not None:
@@ -378,22 +565,31 @@ def main():
         from paper_1707_09683_b200.shard import gather_to_rank0
         gi = gidx.to(comm_dev)
         for k in range(len(scans)):
-            gather_to_rank0(dist, outs[k][0][:n_local].to(comm_dev),
-                            outs[k][1][:n_local].to(comm_dev), gi, db.count, as_numpy=False,
-                            validate=not gathered["validated"])
+            o = outs[(k, 0)]
+            gather_to_rank0(dist, o[0][:n_local].to(comm_dev), o[1][:n_local].to(comm_dev), gi,
+                            db.count, as_numpy=False, validate=not gathered["validated"])
         gathered["validated"] = True
 
+    def to_rank0(raw_t, pass_t):
+        """Full-length numpy (raw, pass) on rank 0 from a local device pair."""
+        if world == 1:
+            return raw_t[:n_local].cpu().numpy(), pass_t[:n_local].cpu().numpy()
+        from paper_1707_09683_b200.shard import gather_to_rank0
+        return gather_to_rank0(dist, raw_t[:n_local].to(comm_dev), pass_t[:n_local].to(comm_dev),
+                               gidx.to(comm_dev), db.count, as_numpy=True)
+
     for _ in range(args.warmup):
-        step(False)
+        step(0, False)
         gather_results()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     # inputs smaller than L2 (126 MB): flush L2 between timed steps by writing
     # a 256 MB buffer outside the timed windows; larger inputs evict it anyway
+    flush_buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device="cuda")
     flush = None
     if dbstats["packed_bytes"] < L2_BYTES and not args.db_budget:
-        flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device="cuda")
+        flush = flush_buf
     launches = 0
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -402,27 +598,28 @@ def main():
         if flush is None:
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record(stream)
-            for _ in range(args.steps):
-                launches += step(True)
+            for j in range(args.steps):
+                launches += step(j, True)
                 gather_results()
             ev1.record(stream)
             torch.cuda.synchronize()
             ms = ev0.elapsed_time(ev1)
         else:
             ms = 0.0
-            for _ in range(args.steps):
+            for j in range(args.steps):
                 flush.fill_(1)
                 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 ev0.record(stream)
-                launches += step(True)
+                launches += step(j, True)
                 gather_results()
                 ev1.record(stream)
                 torch.cuda.synchronize()
                 ms += ev0.elapsed_time(ev1)
         if dist:
             dist.barrier()
+    clocks = clk.summary()
     ms_t = torch.tensor([ms], dtype=torch.float64, device=comm_dev)
-    cells_local = sum(dbstats["residues"] * m for _, m, _ in scans) * args.steps
+    cells_local = sum(dbstats["residues"] * m for m, _ in scans) * args.steps
     cells_t = torch.tensor([float(cells_local)], dtype=torch.float64, device=comm_dev)
     if dist:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -431,12 +628,27 @@ def main():
     total_cells = float(cells_t.item())
     gcups = total_cells / (ms_max * 1e-3) / 1e9
 
+    # the headline scans' outputs go to the parity check (every kept step)
+    for k, (m, a) in enumerate(scans):
+        _, costs, lam, tau = profile_id(m, DEFAULT_Q)
+        if peer is not None:
+            torch.cuda.synchronize()
+            dist.barrier()
+            pair = peer.results(k) if rank == 0 else (None, None)
+            pairs = [pair]
+        else:
+            pairs = [to_rank0(*outs[(k, j)]) for j in range(min(keep, args.steps))]
+        if verifier is not None:
+            for r_, p_ in pairs:
+                verifier.add((m, a, DEFAULT_Q), "headline", a, costs, DEFAULT_Q, lam, tau, r_, p_)
+    del outs
+
     # ---- end to end through the C ABI with host buffers --------------------
     e2e = None
     if not args.no_e2e:
         # the database upload is overlapped with the longest scan (largest M),
         # which hides the copy best; the other scans run on the resident copy
-        e2e_order = sorted(scans, key=lambda sc: -sc[1])
+        e2e_order = sorted(scans, key=lambda sc: -sc[0])
         # page-locked host result buffers, one pair per scan, reused every
         # step (the D2H of every step's results lands in them directly)
         host_out = [(torch.empty(max(n_local, 1), dtype=torch.uint8, pin_memory=True).numpy(),
@@ -448,8 +660,8 @@ def main():
             # model's scan (lhmm_scan_streamed), the other models on the
             # resident copy; every scan ends with the D2H of its raw + pass bytes
             d2h = 0
-            for k, (pid, m, a) in enumerate(e2e_order):
-                s.select_profile(pid)
+            for k, (m, a) in enumerate(e2e_order):
+                s.select_profile(profile_id(m, DEFAULT_Q)[0])
                 rep = (s.scan_streamed(opt_for(a), 64, out=host_out[k]) if k == 0
                        else s.scan(opt_for(a), out=host_out[k]))
                 d2h += 2 * int(rep.raw.size)
@@ -476,20 +688,139 @@ def main():
                         "to 64 pieces overlapped with the largest model's scan, one kernel launch "
                         "waiting per piece on stream-written flags) + lhmm_scan per further "
                         "model, results D2H into page-locked host buffers reused across steps"}
+        if verifier is not None:
+            # the e2e results of the last step, checked like the device ones
+            for k, (m, a) in enumerate(e2e_order):
+                if world == 1:
+                    _, costs, lam, tau = profile_id(m, DEFAULT_Q)
+                    verifier.add((m, a, DEFAULT_Q), "e2e", a, costs, DEFAULT_Q, lam, tau,
+                                 host_out[k][0][:n_local], host_out[k][1][:n_local])
+
+    # ---- sweep leg (C5, C3): per (M, alg, params), device-timed ------------
+    sweep = None
+    if sweep_on and not args.db_budget:
+        sweep = []
+        sw_scans = [(m, "msv", DEFAULT_Q) for m in SWEEP_M] + \
+                   [(m, "ssv", DEFAULT_Q) for m in SWEEP_M] + \
+                   [(m, "msv", NONSAT_Q) for m in SWEEP_M]
+        nst = max(1, args.sweep_steps)
+        sw_out = [(torch.empty(max(n_local, 1), dtype=torch.uint8, device="cuda"),
+                   torch.empty(max(n_local, 1), dtype=torch.uint8, device="cuda"))
+                  for _ in range(nst)]
+        with ClockSampler(local) as clk_sw:
+            for m, a, q in sw_scans:
+                pid, costs, lam, tau = profile_id(m, q)
+                s.select_profile(pid)
+                st = s.scan_device(opt_for(a), sw_out[0][0].data_ptr(), sw_out[0][1].data_ptr())
+                torch.cuda.synchronize()
+                if dist:
+                    dist.barrier()
+                times, sts = [], []
+                for j in range(nst):
+                    st = s.scan_device(opt_for(a), sw_out[j][0].data_ptr(),
+                                       sw_out[j][1].data_ptr())
+                    times.append(st["device_ms"])
+                    sts.append(st)
+                tt = torch.tensor([sum(times) / nst, float(st["saturated"]),
+                                   float(st["mode_rows"]), float(st["lazy_rows"])],
+                                  dtype=torch.float64, device=comm_dev)
+                mx = tt.clone()
+                if dist:
+                    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+                    dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+                t_ms = float(mx[0])
+                g = db.total_residues() * m / (t_ms * 1e-3) / 1e9
+                e = {"alg": a, "M": m, "params": "default" if q == DEFAULT_Q else "nonsat",
+                     "quant": qstr(q), "ms": round(t_ms, 4), "gcups": round(g, 1),
+                     "frac": round(g / (peak_gcups * world), 4),
+                     "lanes": st["lanes"], "rows": st["rows"], "variant": VARIANTS[st["variant"]],
+                     "rescored_exactly": st["recomputed"]}
+                if a == "msv":
+                    e["saturated_frac"] = round(float(tt[1]) / db.count, 4)
+                    if float(tt[2]) > 0:
+                        e["lazy_row_frac"] = round(float(tt[3]) / float(tt[2]), 4)
+                sweep.append(e)
+                for j in range(nst):
+                    r_, p_ = to_rank0(*sw_out[j])
+                    if verifier is not None:
+                        verifier.add((m, a, q), "sweep", a, costs, q, lam, tau, r_, p_)
+        sweep_clocks = clk_sw.summary()
+        del sw_out
+
+    # ---- C1 leg (configs[0]): small database, many steps, L2 flushed --------
+    c1 = None
+    if "c1" in legs and not args.db_budget and args.workload != "c1":
+        c1desc, _, c1m, c1n, c1gen = WORKLOADS["c1"]
+        cres, coff, cprofs = make_inputs(api, c1gen, c1n, c1m)
+        cdb = P.SequenceDB(cres, coff)
+        s1 = P.Scanner(local)
+        s1.set_stream(stream.cuda_stream)
+        s1.set_database(cdb)   # C1 fits one GPU: every rank scans it whole
+        sc, lam, tau = cprofs[c1m[0]]
+        c1 = {"workload": c1desc, "sequences": int(cdb.count), "residues": cdb.total_residues(),
+              "l2": "L2 flushed before every timed scan (256 MB write outside the timed "
+                    "window)", "scans": []}
+        nst = max(3, args.c1_steps)
+        keep1 = min(nst, 50)
+        o1 = [(torch.empty(cdb.count, dtype=torch.uint8, device="cuda"),
+               torch.empty(cdb.count, dtype=torch.uint8, device="cuda")) for _ in range(keep1)]
+        with ClockSampler(local) as clk1:
+            for q in (DEFAULT_Q, NONSAT_Q):
+                costs = api.quantize(sc, q)
+                s1.set_profile(P.CostMatrix(c1m[0], costs), P.QuantParams(*q), lam, tau)
+                opt = P.ScanOptions(alg=P.Algorithm.Msv, threshold=THRESHOLD)
+                for _ in range(max(3, args.warmup)):
+                    s1.scan_device(opt, o1[0][0].data_ptr(), o1[0][1].data_ptr())
+                times, st = [], None
+                for j in range(nst):
+                    flush_buf.fill_(1)
+                    st = s1.scan_device(opt, o1[j % keep1][0].data_ptr(),
+                                        o1[j % keep1][1].data_ptr())
+                    times.append(st["device_ms"])
+                t_ms = statistics.mean(times)
+                g = cdb.total_residues() * c1m[0] / (t_ms * 1e-3) / 1e9
+                e = {"alg": "msv", "M": c1m[0], "params": "default" if q == DEFAULT_Q else "nonsat",
+                     "quant": qstr(q), "steps": nst, "ms": round(t_ms, 4),
+                     "ms_min": round(min(times), 4), "gcups": round(g, 1),
+                     "frac": round(g / peak_gcups, 4), "lanes": st["lanes"], "rows": st["rows"],
+                     "variant": VARIANTS[st["variant"]], "grid": st["grid"],
+                     "saturated_frac": round(st["saturated"] / cdb.count, 4)}
+                if st["mode_rows"]:
+                    e["lazy_row_frac"] = round(st["lazy_rows"] / st["mode_rows"], 4)
+                c1["scans"].append(e)
+                if verifier is not None:
+                    v1 = Verifier(cres, coff, cdb.count)  # C1 in full
+                    for j in range(keep1):
+                        v1.add(("c1", q), "c1", "msv", costs, q, lam, tau,
+                               o1[j][0].cpu().numpy(), o1[j][1].cpu().numpy())
+                    c1.setdefault("_verifiers", []).append(v1)
+        c1["clocks"] = clk1.summary()
+        s1.close()
+
+    parity = None
+    if verifier is not None:
+        parity = verifier.run()
+        if c1 is not None:
+            for v1 in c1.pop("_verifiers", []):
+                p1 = v1.run()
+                parity["checked"] += p1["checked"]
+                parity["mismatches"] += p1["mismatches"]
+                parity["scans"] += p1["scans"]
+                parity["legs"]["c1"] = {k: parity["legs"].get("c1", {}).get(k, 0) + p1["legs"]["c1"][k]
+                                        for k in ("scans", "checked", "mismatches")}
+                parity["seconds"] = round(parity["seconds"] + p1["seconds"], 2)
+    elif c1 is not None:
+        c1.pop("_verifiers", None)
 
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return 0
 
-    peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    n_sm = info["sm_count"]
-    peak_gcups = n_sm * sm_max * 1e6 * CELLS_PER_CLK_PER_SM / 1e9
     # dominant kernel: the scan with the largest share of the step
     dom = max(per_launch, key=lambda k: sum(per_launch[k]))
     dom_ms = statistics.mean(per_launch[dom])
-    _, dom_m, dom_a = scans[dom]
+    dom_m, dom_a = scans[dom]
     dom_cells = dbstats["residues"] * dom_m
     achieved = dom_cells / (dom_ms * 1e-3) / 1e9
     traffic = None
@@ -499,15 +830,13 @@ def main():
     hbm_gbs = float(peaks.get("hbm_gbs", 6545.9))
     hbm_achieved = (dbstats["packed_bytes"] + 9 * n_local) / (dom_ms * 1e-3) / 1e9
     share = sum(per_launch[dom]) / ms_max if ms_max else None
-    # binding resource of the dominant kernel: the shared-memory table gather
-    # (128 B/clk/SM); table bytes per cell of its code form
-    dom_form = ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm", "fp16xh"][geo[dom][2]]
+    dgeo = geo[dom]
+    dom_form = VARIANTS[dgeo["variant"]]
+    # second bound: the shared-memory table gather (128 B/clk/SM) at the
+    # table bytes per cell of the dominant kernel's code form
     table_bpc = {"fp16xm": 1.6, "swar8": 1.0}.get(dom_form, 2.0)
     if dom_form == "fp16xh":
-        # lazy rows' table (csrc/hybrid_layout.hpp): 16-byte slots per lane
-        # for H rows of 2 cells -- mixed slots of five rows, 16-bit slots of
-        # four, a two-row remainder slot
-        L_dom, H_dom = geo[dom][0], geo[dom][1]
+        L_dom, H_dom = dgeo["lanes"], dgeo["rows"]
         nm = -1
         for k in range(H_dom // 5 + 1):
             if (H_dom - 5 * k) % 4 not in (0, 2):
@@ -518,69 +847,70 @@ def main():
         slots = nm + rest // 4 + (1 if rest % 4 else 0)
         table_bpc = round(slots * 16 / (2 * H_dom), 3)
     smem_peak = n_sm * sm_max * 1e6 * (128 / table_bpc) / 1e9
-    clocks = clk.summary()
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference_gcups(P, db, models, algs, q, args.ref_sample)
+            cmodels = [(m, *profs[m], profile_id(m, DEFAULT_Q)[1]) for m in models_m]
+            cpu = cpu_reference_gcups(res, off, cmodels, algs, DEFAULT_Q, args.ref_sample)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "error": str(e)}
     per_scan = []
-    for k, (pid, m, a) in enumerate(scans):
+    for k, (m, a) in enumerate(scans):
         t = statistics.mean(per_launch[k])
-        L, H, v, grid, smem, recomputed = geo[k]
+        g = geo[k]
         per_scan.append({"alg": a, "M": m, "ms": round(t, 4),
                          "gcups": round(dbstats["residues"] * m / (t * 1e-3) / 1e9, 1),
-                         "lanes": L, "rows": H, "variant": ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm", "fp16xh"][v],
-                         "grid": grid, "smem_bytes": smem, "rescored_exactly": recomputed})
+                         "lanes": g["lanes"], "rows": g["rows"], "variant": VARIANTS[g["variant"]],
+                         "grid": g["grid"], "smem_bytes": g["smem_bytes"],
+                         "rescored_exactly": g["recomputed"]})
+    cfg = workload_config(args.workload, desc, models_m, algs, db.count, db.total_residues(), world)
+    if world > 1:
+        cfg["gather"] = gather_mode
+    if args.db_budget:
+        cfg["out_of_core"] = (f"database streamed from pinned host memory through a "
+                              f"{args.db_budget / 2**20:.0f} MiB device ring per scan")
     line = {
-        "metric": "MSV/SSV GCUPS (device-timed) vs model length",
-        "value": round(gcups, 2), "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
+        "metric": METRIC, "value": round(gcups, 2), "unit": "GCUPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic",
-        "config": {"workload": desc, "models": list(models_m), "algorithms": algs,
-                   "sequences": int(db.count), "residues": int(db.total_residues()),
-                   "threshold": threshold, "quant": "QuantParams{3.0,195,3,3,3}",
-                   "parallelism": f"shard{world} by residue count, raw+pass gathered to rank 0"
-                                  + (f" ({gather_mode})" if world > 1 else ""),
-                   "l2": ("inputs larger than L2 (packed database "
-                          f"{dbstats['packed_bytes'] / 1e6:.0f} MB per GPU > 126 MB)"
-                          if flush is None else
-                          "L2 flushed between timed steps (256 MB write outside the timed "
-                          f"windows; packed database {dbstats['packed_bytes'] / 1e6:.1f} MB < "
-                          "126 MB)"),
-                   "early_exit": False,
-                   **({"out_of_core": f"database streamed from pinned host memory through a "
-                                      f"{args.db_budget / 2**20:.0f} MiB device ring per scan"}
-                      if args.db_budget else {})},
-        "e2e": e2e,
+        "data": "synthetic", "config": cfg, "e2e": e2e,
         "gpu_launches": launches * world,
-        "roofline": {"bound": "smem", "achieved": round(achieved, 1),
-                     "peak": round(smem_peak, 1), "unit": "GCUPS",
-                     "frac": round(achieved / smem_peak, 4), "traffic": traffic,
-                     "kernel": f"{dom_a} M={dom_m} ({dom_form})", "kernel_share_of_step": share,
-                     "peak_basis": f"{n_sm} SMs x {sm_max:.0f} MHz x 128 B/clk/SM shared-memory "
-                                   f"bandwidth / {table_bpc} emission-table bytes per cell "
-                                   f"({dom_form}) = {128 / table_bpc:.0f} cells/clk/SM: every "
-                                   "cell gathers its cost from the shared-memory table",
-                     "int_simd": {"peak": round(peak_gcups, 1), "unit": "GCUPS",
-                                  "frac": round(achieved / peak_gcups, 4),
-                                  "basis": "BASELINE north-star packed-integer-SIMD roofline: "
-                                           "64 INT32 lane-ops/clk/SM x 4 packed u8 cells / 4 ops "
-                                           "per cell = 64 cells/clk/SM; the FP16X forms split "
-                                           "each cell update over the FP16 and ALU pipes, so "
-                                           "they can pass it (FP16XM)"},
-                     "hbm": {"bound": "hbm", "achieved": round(hbm_achieved, 1),
-                             "peak": hbm_gbs, "unit": "GB/s",
-                             "frac": round(hbm_achieved / hbm_gbs, 4)}},
+        "roofline": {"bound": "int_simd", "achieved": round(achieved, 1),
+                     "peak": round(peak_gcups, 1), "unit": "GCUPS",
+                     "frac": round(achieved / peak_gcups, 4), "traffic": traffic,
+                     "kernel": f"{dom_a} M={dom_m} ({dom_form} L{dgeo['lanes']} H{dgeo['rows']})",
+                     "kernel_share_of_step": share,
+                     "peak_basis": f"SURVEY §8(d) packed-integer-SIMD roofline: {n_sm} SMs x "
+                                   f"{sm_max:.0f} MHz x 64 cells/clk/SM (64 INT32 lane-ops x 4 "
+                                   "packed u8 cells / 4 ops per cell)",
+                     "table_smem": {"peak": round(smem_peak, 1), "unit": "GCUPS",
+                                    "frac": round(achieved / smem_peak, 4),
+                                    "basis": f"128 B/clk/SM shared-memory bandwidth / {table_bpc} "
+                                             f"emission-table bytes per cell ({dom_form}); every "
+                                             "cell gathers its cost from the table"},
+                     "hbm": {"achieved": round(hbm_achieved, 1), "peak": hbm_gbs, "unit": "GB/s",
+                             "frac": round(hbm_achieved / hbm_gbs, 4),
+                             "basis": "1 residue byte per M cells (tables on chip)"}},
         "cpu_baseline": cpu,
         "clocks": clocks,
+        "parity": parity,
         "scans": per_scan,
         "setup": {"generate_s": round(t_gen, 2), "pack_upload_s": round(t_pack, 2),
                   "packed_bytes": dbstats["packed_bytes"], "padded_cells": dbstats["padded_cells"],
                   "tiles": dbstats["tiles"]},
     }
+    if sweep is not None:
+        c3 = next((e for e in sweep if e["alg"] == "msv" and e["M"] == 2405
+                   and e["params"] == "default"), None)
+        line["sweep"] = {"what": "C5: device-timed GCUPS per (M, alg, params) over the same "
+                                 "1M-sequence database, mean of --sweep-steps scans; frac = of "
+                                 f"the {peak_gcups * world / 1e3:.1f} TCUPS packed-integer "
+                                 "roofline; lazy_row_frac = share of warp rows run by the "
+                                 "two-mode MSV kernel's lazy (saturated) body",
+                         "steps": max(1, args.sweep_steps), "clocks": sweep_clocks,
+                         "scans": sweep, "c3": c3}
+    if c1 is not None:
+        line["c1"] = c1
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define LHMM_ABI_VERSION 1
+#define LHMM_ABI_VERSION 2
 
 enum lhmm_status {
     LHMM_OK = 0,
@@ -122,6 +122,9 @@ typedef struct lhmm_scan_stats {
     uint32_t threads;       /* threads per CTA */
     uint32_t smem_bytes;    /* dynamic shared memory per CTA */
     uint32_t recomputed;    /* FP16X: sequences rescored by the exact kernel */
+    uint64_t saturated;     /* MSV: sequences whose raw score is 255 (overflow) */
+    uint64_t mode_rows;     /* two-mode MSV kernels: residue rows run by the warps ... */
+    uint64_t lazy_rows;     /* ... and how many of them in the lazy (saturated) mode */
 } lhmm_scan_stats;
 
 typedef struct lhmm_context lhmm_context;

@@ -158,6 +158,45 @@ int ref_scalar(int alg, const uint8_t* costs, uint32_t m, double scale, const ui
     }
 }
 
+// The reference scalar oracle over a flat database (OpenMP over sequences):
+// raw_out[k] = scalar_msv / scalar_ssv of sequence k.  Returns 0, or -1 with
+// the reference's error text.  This is bench.py's parity checker.
+int ref_scalar_flat(int alg, const uint8_t* costs, uint32_t m, double scale, const uint8_t* b4,
+                    const uint8_t* residues, const uint64_t* offsets, uint64_t nseq, int threads,
+                    uint8_t* raw_out) {
+    const CostMatrix cm = make_costs(costs, m);
+    const QuantParams q = to_q(scale, b4);
+    int bad = 0;
+#pragma omp parallel for schedule(dynamic, 16) num_threads(threads > 0 ? threads : 1) \
+    reduction(+ : bad)
+    for (int64_t k = 0; k < int64_t(nseq); ++k) {
+        try {
+            std::span<const uint8_t> s(residues + offsets[k], offsets[k + 1] - offsets[k]);
+            raw_out[k] = alg == 0 ? oracle::scalar_msv(cm, s, q) : oracle::scalar_ssv(cm, s, q);
+        } catch (const std::exception& e) {
+            ++bad;
+        }
+    }
+    if (bad) {
+        g_err = std::to_string(bad) + " sequences rejected by the reference oracle";
+        return -1;
+    }
+    return 0;
+}
+
+// The reference pass rule per sequence: finalize_hit (src/engine.cpp:59-81),
+// pass = pValue <= threshold || overflow (src/engine.cpp:617, 639).
+void ref_pass_flat(int alg, const uint8_t* raw, const uint64_t* offsets, uint64_t nseq,
+                   double lambda, double tau, double scale, const uint8_t* b4, double threshold,
+                   uint8_t* pass_out) {
+    const QuantParams q = to_q(scale, b4);
+    const Algorithm a = alg == 0 ? Algorithm::Msv : Algorithm::Ssv;
+    for (uint64_t k = 0; k < nseq; ++k) {
+        const HitResult h = finalize_hit(raw[k], offsets[k + 1] - offsets[k], lambda, tau, q, a);
+        pass_out[k] = (h.pValue <= threshold || h.overflow) ? 1 : 0;
+    }
+}
+
 uint8_t ref_move_cost(uint64_t len, double scale, const uint8_t* b4) {
     return oracle::move_cost(len, to_q(scale, b4));
 }

@@ -5,7 +5,7 @@ Native library: _lib/liblhmm_b200.so (C ABI in include/lhmm_b200.h); no CPU
 fallback exists -- calls raise NativeLibraryError if it is missing.
 """
 from .lanehmm import (  # noqa: F401
-    Algorithm, ContractError, ParseError, CostMatrix, DataError, HitResult, PipelineReport, ProfileHMM,
+    Algorithm, ContractError, CudaError, ParseError, CostMatrix, DataError, HitResult, PipelineReport, ProfileHMM,
     QuantParams, Rng, filter_pipeline,
     ScanOptions, ScanReport, Scanner, SequenceDB, Variant, engine_sequence_base, finalize_hit,
     hits_from, move_cost, quantize_emissions, scan_database, scan_sequences_s1, select_geometry)

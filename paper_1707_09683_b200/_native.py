@@ -33,7 +33,8 @@ class ScanStatsC(C.Structure):
                 ("residues", C.c_uint64), ("cells", C.c_uint64), ("lanes", C.c_uint32),
                 ("rows", C.c_uint32), ("variant", C.c_uint32), ("launches", C.c_uint32),
                 ("grid", C.c_uint32), ("threads", C.c_uint32), ("smem_bytes", C.c_uint32),
-                ("recomputed", C.c_uint32)]
+                ("recomputed", C.c_uint32), ("saturated", C.c_uint64),
+                ("mode_rows", C.c_uint64), ("lazy_rows", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -142,7 +143,7 @@ def lib():
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
-    if L.lhmm_abi_version() != 1:
+    if L.lhmm_abi_version() != 2:
         raise NativeLibraryError("ABI version mismatch")
     _lib = L
     return L

@@ -76,7 +76,7 @@ def build(verbose=False, jobs=None, defines=(), tag=""):
     for s in srcs:
         o = os.path.join(BUILD, os.path.basename(s) + ".o")
         objs.append(o)
-        if _stale(s, o, hdr_mtime if not s.endswith("host_prep.cpp") else 0):
+        if _stale(s, o, hdr_mtime):
             todo.append((s, o))
     if todo:
         with ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 8) as ex:

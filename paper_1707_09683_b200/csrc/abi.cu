@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -385,6 +386,7 @@ struct lhmm_context {
     DevBuf<uint32_t> d_lens, d_out_idx;
     DevBuf<uint32_t> d_counter;
     DevBuf<uint32_t> d_sat;        // MSV saturated-score count of the last scan
+    DevBuf<unsigned long long> d_mode_rows;  // two-mode MSV: [rows, lazy rows]
     DevBuf<uint8_t> d_raw, d_pass;
     DevBuf<uint32_t> d_out_gidx;   // slot -> GLOBAL sequence index (fused peer gather)
     uint64_t n_global = 0;         // sequences of the whole (unsharded) database
@@ -662,9 +664,10 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     } else {
         if (variant == LHMM_VARIANT_AUTO) variant = LHMM_VARIANT_FP16;
         if (L == 0) {
-            Choice ch = choose_geometry(pf.m, opt->alg, variant, 0, v.n_tiles, c->sm_count);
-            L = ch.L ? ch.L : 1;
-            if (ch.L) variant = ch.variant;
+            // explicit H: the smallest lane count whose capacity covers the model
+            const uint64_t cpw = lhmm::cells_per_word(variant);
+            L = 1;
+            while (L < 32 && cpw * L * H < pf.m) L *= 2;
         }
         // an explicit (variant, L, H) runs exactly that code form -- the
         // calibration sweep depends on it
@@ -761,6 +764,14 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         if (int rc = c->d_sat.reserve(1)) return rc;
         CUDA_TRY(cudaMemsetAsync(c->d_sat.ptr, 0, 4, c->stream));
         p.sat_count = c->d_sat.ptr;
+    }
+    const bool track_modes = opt->alg == LHMM_MSV && !long_model &&
+                             (variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16X_ALT ||
+                              variant == LHMM_VARIANT_FP16XM || variant == LHMM_VARIANT_FP16XH);
+    if (track_modes) {
+        if (int rc = c->d_mode_rows.reserve(2)) return rc;
+        CUDA_TRY(cudaMemsetAsync(c->d_mode_rows.ptr, 0, 16, c->stream));
+        p.mode_rows = c->d_mode_rows.ptr;
     }
     p.wrap = opt->reorder_mode == 1 ? 1u : 0u;
     const bool relaxed = (variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16XM) &&
@@ -960,27 +971,37 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     }
     // the saturation / flag counters come back with the same synchronisation
     // as the end event (pinned words, no extra round trip)
-    uint32_t* counts = c->counts_host.reserve(8) ? reinterpret_cast<uint32_t*>(c->counts_host.ptr)
-                                                 : nullptr;
+    uint32_t* counts = c->counts_host.reserve(32) ? reinterpret_cast<uint32_t*>(c->counts_host.ptr)
+                                                  : nullptr;
+    uint64_t mode_rows[2] = {0, 0};
     if (counts) {
         if (track_sat)
             CUDA_TRY(cudaMemcpyAsync(counts, c->d_sat.ptr, 4, cudaMemcpyDeviceToHost, c->stream));
         if (relaxed)
             CUDA_TRY(cudaMemcpyAsync(counts + 1, c->d_flag_count.ptr, 4, cudaMemcpyDeviceToHost,
                                      c->stream));
+        if (track_modes)
+            CUDA_TRY(cudaMemcpyAsync(counts + 2, c->d_mode_rows.ptr, 16, cudaMemcpyDeviceToHost,
+                                     c->stream));
     }
     CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
     CUDA_TRY(cudaEventSynchronize(c->ev1));
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    uint32_t nsat = 0;
     if (track_sat && v.sequences > 0) {
-        uint32_t nsat = 0;
         if (counts)
             nsat = counts[0];
         else
             CUDA_TRY(cudaMemcpy(&nsat, c->d_sat.ptr, 4, cudaMemcpyDeviceToHost));
         pf.sat_frac = double(nsat) / double(v.sequences);
         pf.sat_gen = c->db_gen;
+    }
+    if (track_modes) {
+        if (counts)
+            std::memcpy(mode_rows, counts + 2, 16);
+        else
+            CUDA_TRY(cudaMemcpy(mode_rows, c->d_mode_rows.ptr, 16, cudaMemcpyDeviceToHost));
     }
     uint32_t recomputed = 0;
     if (relaxed) {
@@ -1044,6 +1065,9 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         st->threads = uint32_t(cfg.threads);
         st->smem_bytes = uint32_t(cfg.smem);
         st->recomputed = recomputed;
+        st->saturated = nsat;
+        st->mode_rows = mode_rows[0];
+        st->lazy_rows = mode_rows[1];
     }
     return LHMM_OK;
 }
@@ -1271,6 +1295,74 @@ int run_pipeline(lhmm_context* c, double threshold, int variant, uint8_t* ssv_ra
 
 }  // namespace
 
+// f16 subnormal self-check.  The FP16XM / FP16XH forms keep byte scores as
+// f16 subnormals (a bit pattern IS its value in units of 2^-24), so they are
+// exact only if HADD2 / HMNMX2 keep subnormal operands and results; a build
+// with flush-to-zero (--use_fast_math, an ftz toolchain default) would be
+// silently wrong.  Every context runs this probe once per device, compiled
+// with the same flags as the scan kernels, and refuses to start if it fails.
+// LHMM_SELFCHECK_FORCE_FTZ=1 (tests only) runs the flush-to-zero form of the
+// same ops, to prove the check fires.
+static __global__ void subnormal_probe(uint32_t* out, int force_ftz) {
+    const uint32_t a = 0x00050003u, b = 0x00030002u, n = 0x80050001u;
+    uint32_t r0, r1, r2, r3;
+    if (force_ftz) {
+        asm volatile("add.ftz.sat.f16x2 %0, %1, %2;" : "=r"(r0) : "r"(a), "r"(b));
+        asm volatile("add.ftz.f16x2 %0, %1, %2;" : "=r"(r1) : "r"(n), "r"(a));
+        asm volatile("max.ftz.f16x2 %0, %1, %2;" : "=r"(r2) : "r"(a), "r"(b));
+        asm volatile("sub.ftz.f16x2 %0, %1, %2;" : "=r"(r3) : "r"(a), "r"(b));
+    } else {
+        r0 = lhmm::as_u32(__hadd2_sat(lhmm::as_h2(a), lhmm::as_h2(b)));
+        r1 = lhmm::as_u32(__hadd2(lhmm::as_h2(n), lhmm::as_h2(a)));
+        r2 = lhmm::as_u32(__hmax2(lhmm::as_h2(a), lhmm::as_h2(b)));
+        r3 = lhmm::as_u32(__hsub2(lhmm::as_h2(a), lhmm::as_h2(b)));
+    }
+    out[0] = r0;  // (5+3, 3+2)          = 0x00080005
+    out[1] = r1;  // (-5+5, 1+3)         = 0x00000004 (+0 or -0 in the top half)
+    out[2] = r2;  // (max(5,3), max(3,2)) = 0x00050003
+    out[3] = r3;  // (5-3, 3-2)          = 0x00020001
+}
+
+static int subnormal_selfcheck(int device) {
+    static std::mutex mu;
+    static std::map<int, int> verdict;  // device -> LHMM_OK or error
+    std::lock_guard<std::mutex> lk(mu);
+    const char* env = std::getenv("LHMM_SELFCHECK_FORCE_FTZ");
+    const int force = env && std::atoi(env) != 0;
+    const auto it = verdict.find(device);
+    if (!force && it != verdict.end()) {
+        if (it->second != LHMM_OK)
+            return set_error(LHMM_ERR_CUDA, "f16 subnormal self-check failed on this device");
+        return LHMM_OK;
+    }
+    uint32_t* d = nullptr;
+    uint32_t h[4] = {0, 0, 0, 0};
+    if (cudaMalloc(&d, 16) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(LHMM_ERR_NOMEM, "self-check allocation failed");
+    }
+    subnormal_probe<<<1, 1>>>(d, force);
+    const cudaError_t e1 = cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e1 != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(LHMM_ERR_CUDA, std::string("self-check kernel failed: ") +
+                                            cudaGetErrorString(e1));
+    }
+    const bool ok = h[0] == 0x00080005u && (h[1] & 0x7fffffffu) == 0x00000004u &&
+                    h[2] == 0x00050003u && h[3] == 0x00020001u;
+    if (!force) verdict[device] = ok ? LHMM_OK : LHMM_ERR_CUDA;
+    if (!ok) {
+        char buf[160];
+        std::snprintf(buf, sizeof buf,
+                      "f16 subnormal self-check failed (flush-to-zero build?): got %08x %08x "
+                      "%08x %08x; the FP16XM/FP16XH scores would be wrong",
+                      h[0], h[1], h[2], h[3]);
+        return set_error(LHMM_ERR_CUDA, buf);
+    }
+    return LHMM_OK;
+}
+
 extern "C" {
 
 int lhmm_select_geometry(uint32_t m, int alg, int variant, uint32_t* lanes, uint32_t* rows) {
@@ -1303,6 +1395,10 @@ int lhmm_context_create(int device, lhmm_context** out) {
         delete c;
         return set_error(LHMM_ERR_CUDA, "this build targets sm_100a (B200); device is sm_" +
                                             std::to_string(prop.major) + std::to_string(prop.minor));
+    }
+    if (int rc = subnormal_selfcheck(device)) {
+        delete c;
+        return rc;
     }
     if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -1417,6 +1513,11 @@ static int fill_profile(ProfileSlot& pf, const uint8_t* costs, uint32_t m, const
     pf.q = *q;
     pf.lambda = lambda;
     pf.tau = tau;
+    // the policy feedback belongs to the replaced profile's scores
+    pf.sat_frac = -1.0;
+    pf.sat_gen = 0;
+    pf.flag_frac = -1.0;
+    pf.flag_gen = 0;
     return LHMM_OK;
 }
 

@@ -95,6 +95,9 @@ struct KParams {
     uint8_t* flag_out;          // relaxed variants: 1 = rescore exactly
     uint32_t* flag_count;       // relaxed variants: number of flagged sequences
     uint32_t* sat_count;        // MSV: sequences whose score saturated (policy feedback)
+    // two-mode MSV: [0] warp rows run, [1] of them in the lazy mode (reported
+    // beside the throughput: the lazy body is the saturation-dependent speed-up)
+    unsigned long long* mode_rows;
 };
 
 // ---------------------------------------------------------------------------
@@ -1109,6 +1112,7 @@ __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KPar
     const uint32_t shift_src = (lane & ~uint32_t(L - 1)) | ((lane + L - 1) & uint32_t(L - 1));
     const bool inject_here = oig == 0 && !p.wrap;
     uint32_t ready_below = 0;
+    unsigned long long rows_all = 0, rows_lazy = 0;  // two-mode MSV statistics
 
     for (;;) {
         uint32_t item = 0;
@@ -1162,6 +1166,8 @@ __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KPar
             }
         }
         if constexpr (V::kTwoMode) {
+            rows_all += rows;
+            if (r0 < rows && !done) rows_lazy += rows - r0;
             constexpr int RPI_L = rows_per_iter<V, H, true>();
             ResChunk<RPI_L> preL{};
             if (r0 < rows && !done) preL = load_res<RPI_L>(src, r0);
@@ -1197,6 +1203,12 @@ __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KPar
                 p.flag_out[oi] = exact_needed ? 1u : 0u;
                 if (exact_needed) atomicAdd(p.flag_count, 1u);
             }
+        }
+    }
+    if constexpr (V::kTwoMode) {
+        if (lane == 0 && p.mode_rows && rows_all) {
+            atomicAdd(p.mode_rows, rows_all);
+            atomicAdd(p.mode_rows + 1, rows_lazy);
         }
     }
 }

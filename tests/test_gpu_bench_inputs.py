@@ -1,0 +1,235 @@
+"""GPU parity on the benchmark's own inputs and on the reference-produced
+golden vectors, through the C ABI (VERDICT r1 "next round" item 1).
+
+* The golden fixtures (tests/golden/oracle_golden.json, raw bytes and pass
+  bits produced by the UNMODIFIED reference library: its generators, scalar
+  oracle and finalize_hit) fed straight to the device, every code form.
+* C1 in full (BASELINE configs[0]: synth::random_profile(200) +
+  random_records(10000, 50, 650) + plant_motifs(0.05), seed 0xC1), MSV and
+  SSV, default and non-saturating QuantParams, at the pipeline thresholds,
+  against the reference's scalar oracle -- the reference's acceptance bar
+  (proj/tests/acceptance_main.cpp:47-113, src/oracle.cpp:41-91).
+* The auto policy at >= 4096 tiles (where it picks the relaxed FP16XM SSV
+  kernel with flagging, compaction and exact rescoring, and the two-mode MSV
+  kernels), checked against the oracle -- not against itself -- on the first
+  scan and after the policy's saturation / rescoring feedback, resident and
+  streamed.
+* The f16 subnormal self-check refuses a flush-to-zero arithmetic.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1707_09683_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+DEFAULT = P.QuantParams()
+NONSAT = P.QuantParams(3.0, 120, 3, 20, 20)
+THRESHOLDS = (0.022, 0.103, 0.307, 0.458)
+
+
+def oq(q):
+    return oracle.QuantParams(q.scale, q.base, q.dbias, q.tec, q.tjb)
+
+
+class Checker:
+    """The reference library's scalar oracle + pass rule (oracle/_ref) when it
+    is built, else the C restatement (oracle/oracle.c), pinned to it by
+    tests/test_oracle.py."""
+
+    def __init__(self):
+        try:
+            self.ref = oracle.Reference()
+        except FileNotFoundError:
+            self.ref = None
+        self.ora = oracle.Oracle()
+
+    def raw(self, alg, costs, db, q):
+        if self.ref is not None:
+            return self.ref.scalar_flat(int(alg), costs.bytes, db.residues, db.offsets, oq(q))
+        return self.ora.scan_flat(int(alg), costs.bytes, db.residues, db.offsets, oq(q))
+
+    def passed(self, alg, raw, db, hmm, q, t):
+        if self.ref is not None:
+            return self.ref.pass_flat(int(alg), raw, db.offsets, hmm.lambda_, hmm.tau, oq(q),
+                                      t).astype(bool)
+        lens = db.lengths()
+        return np.array([self.ora.passes(int(r), int(n), hmm.lambda_, hmm.tau, oq(q), int(alg), t)
+                         for r, n in zip(raw, lens)], bool)
+
+
+@pytest.fixture(scope="module")
+def chk():
+    return Checker()
+
+
+def golden_cases():
+    with open(os.path.join(HERE, "golden", "oracle_golden.json")) as f:
+        return json.load(f)["cases"]
+
+
+def golden_inputs(c):
+    """Regenerate a golden case's inputs with the product's generators (the
+    same synth:: streams) and pin them to the fixture's checksums."""
+    g = P.Rng(c["seed"])
+    hmm = g.random_profile(c["m"])
+    plant = (hmm, c["plant"]) if c["plant"] else None
+    if c["gen"] == "uniform":
+        db = g.random_records(c["count"], c["lo"], c["hi"], plant=plant)
+    else:
+        db = g.lognormal_records(c["count"], c["median"], c["sigma"], 2, plant=plant)
+    q = P.QuantParams(*c["quant"])
+    costs = P.quantize_emissions(hmm, q)
+    assert int(db.residues.astype(np.uint64).sum()) == c["residue_sum"]
+    assert int(costs.bytes.astype(np.uint64).sum()) == c["cost_sum"]
+    return hmm, db, q, costs
+
+
+FORMS = {"msv": [P.Variant.Auto, P.Variant.Fp16, P.Variant.Dpx16, P.Variant.Fp16x,
+                 P.Variant.Fp16xAlt, P.Variant.Fp16xMixed, P.Variant.Fp16xHybrid],
+         "ssv": [P.Variant.Auto, P.Variant.Fp16, P.Variant.Dpx16, P.Variant.Fp16x,
+                 P.Variant.Fp16xMixed]}
+
+
+@pytest.mark.parametrize("case", range(7))
+def test_golden_fixtures_on_device(case):
+    """Every golden case (7 cases, 1,480 sequences, M = 7..2405, four
+    QuantParams sets): device raw bytes and pass bits at all six fixture
+    thresholds equal the reference's, for every code form."""
+    c = golden_cases()[case]
+    hmm, db, q, costs = golden_inputs(c)
+    with P.Scanner(0) as s:
+        s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        s.set_database(db)
+        for key, alg in (("msv", P.Algorithm.Msv), ("ssv", P.Algorithm.Ssv)):
+            want = np.array(c[key], np.uint8)
+            for variant in FORMS[key]:
+                for t in c[f"pass_{key}"]:
+                    rep = s.scan(P.ScanOptions(alg=alg, variant=variant, threshold=float(t)))
+                    np.testing.assert_array_equal(rep.raw, want,
+                                                  err_msg=f"{key} {variant.name} raw")
+                    np.testing.assert_array_equal(rep.passed, np.array(c[f"pass_{key}"][t]),
+                                                  err_msg=f"{key} {variant.name} pass t={t}")
+
+
+def c1_inputs():
+    rng = P.Rng(0xC1)
+    hmm = rng.random_profile(200)
+    db = rng.random_records(10000, 50, 650, plant=(hmm, 0.05))
+    return hmm, db
+
+
+@pytest.mark.parametrize("q", [DEFAULT, NONSAT], ids=["default", "nonsat"])
+def test_c1_in_full_matches_reference_oracle(chk, q):
+    """BASELINE configs[0] in full: 10k sequences x M=200, MSV and SSV, auto
+    policy and the exact FP16 form, raw + pass at every pipeline threshold."""
+    hmm, db = c1_inputs()
+    assert db.count == 10000
+    costs = P.quantize_emissions(hmm, q)
+    with P.Scanner(0) as s:
+        s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        s.set_database(db)
+        for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
+            want = chk.raw(alg, costs, db, q)
+            for t in THRESHOLDS:
+                wp = chk.passed(alg, want, db, hmm, q, t)
+                for variant in (P.Variant.Auto, P.Variant.Fp16):
+                    for _ in range(2):  # the second auto scan follows the policy feedback
+                        rep = s.scan(P.ScanOptions(alg=alg, variant=variant, threshold=t))
+                        np.testing.assert_array_equal(rep.raw, want)
+                        np.testing.assert_array_equal(rep.passed, wp)
+            if alg == P.Algorithm.Msv and q == DEFAULT:
+                # the saturation share the two-mode policy keys on
+                assert rep.stats["saturated"] == int(np.count_nonzero(want == 255))
+
+
+def large_db():
+    """>= 4096 tiles of 32 sequences, short log-normal lengths (cheap for the
+    CPU oracle), 5% planted motifs so some SSV scores overflow and get
+    flagged for exact rescoring."""
+    rng = P.Rng(0x4096)
+    hmm = rng.random_profile(400)
+    db = rng.lognormal_records(140000, 60.0, 0.65, 2, plant=(hmm, 0.05))
+    return hmm, db
+
+
+@pytest.mark.parametrize("q", [DEFAULT, NONSAT, P.QuantParams(2.0, 240, 10, 1, 5)],
+                         ids=["default", "nonsat", "varied"])
+def test_auto_policy_at_4096_tiles_matches_oracle(chk, q):
+    hmm, db = large_db()
+    costs = P.quantize_emissions(hmm, q)
+    with P.Scanner(0) as s:
+        s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+        s.set_database(db)
+        assert s.database_stats()["tiles"] >= 4096
+        for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
+            want = chk.raw(alg, costs, db, q)
+            wp = chk.passed(alg, want, db, hmm, q, 0.022)
+            forms = []
+            for k in range(3):
+                o = P.ScanOptions(alg=alg, threshold=0.022)
+                rep = s.scan(o) if k < 2 else s.scan_streamed(o, 16)
+                forms.append(P.Variant(rep.stats["variant"]).name)
+                np.testing.assert_array_equal(rep.raw, want, err_msg=f"{alg.name} scan {k}")
+                np.testing.assert_array_equal(rep.passed, wp, err_msg=f"{alg.name} scan {k}")
+                if alg == P.Algorithm.Ssv and rep.stats["variant"] in (P.Variant.Fp16x,
+                                                                       P.Variant.Fp16xMixed):
+                    # the relaxed kernel rescored exactly what could have capped
+                    assert rep.stats["recomputed"] > 0 or (want < 256 - q.dbias).all()
+            if alg == P.Algorithm.Ssv:
+                # the relaxed SSV path is what ran first at this size
+                assert forms[0] in ("Fp16x", "Fp16xMixed"), forms
+
+
+def test_relaxed_ssv_rescoring_is_exercised(chk):
+    """A database where many SSV scores overflow: the relaxed kernel flags
+    them, the device compacts them and the exact kernel rescores them in the
+    same scan -- results equal the oracle."""
+    rng = P.Rng(0x5C0)
+    hmm = rng.random_profile(200)
+    db = rng.lognormal_records(140000, 60.0, 0.65, 2, plant=(hmm, 0.4))
+    costs = P.quantize_emissions(hmm, DEFAULT)
+    want = chk.raw(P.Algorithm.Ssv, costs, db, DEFAULT)
+    assert (want >= 256 - DEFAULT.dbias).sum() > 1000
+    with P.Scanner(0) as s:
+        s.set_profile(costs, DEFAULT, hmm.lambda_, hmm.tau)
+        s.set_database(db)
+        for variant in (P.Variant.Auto, P.Variant.Fp16xMixed, P.Variant.Fp16x):
+            rep = s.scan(P.ScanOptions(alg=P.Algorithm.Ssv, variant=variant, threshold=0.3))
+            np.testing.assert_array_equal(rep.raw, want)
+            if variant != P.Variant.Auto:
+                assert rep.stats["recomputed"] >= int((want >= 256 - DEFAULT.dbias).sum())
+
+
+def test_two_mode_msv_reports_lazy_rows():
+    """Two-mode MSV kernels count the warp rows they ran and how many in the
+    lazy (saturated) body; saturating parameters run most rows lazily, the
+    non-saturating set none."""
+    hmm, db = large_db()
+    with P.Scanner(0) as s:
+        s.set_database(db)
+        for q, lo, hi in ((DEFAULT, 0.3, 1.0), (NONSAT, 0.0, 0.0)):
+            s.set_profile(P.quantize_emissions(hmm, q), q, hmm.lambda_, hmm.tau)
+            rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv, variant=P.Variant.Fp16x))
+            st = rep.stats
+            assert st["mode_rows"] > 0
+            frac = st["lazy_rows"] / st["mode_rows"]
+            assert lo <= frac <= hi, frac
+            rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv, variant=P.Variant.Fp16))
+            assert rep.stats["mode_rows"] == 0  # one-mode kernel
+
+
+def test_subnormal_selfcheck_refuses_flush_to_zero(monkeypatch):
+    """The FP16XM/FP16XH forms are exact only with f16 subnormals; a context
+    refuses to start when the probe sees flush-to-zero arithmetic."""
+    monkeypatch.setenv("LHMM_SELFCHECK_FORCE_FTZ", "1")
+    with pytest.raises(P.CudaError, match="subnormal"):
+        P.Scanner(0)
+    monkeypatch.delenv("LHMM_SELFCHECK_FORCE_FTZ")
+    with P.Scanner(0) as s:
+        assert s.device_info()["sm_count"] > 0
