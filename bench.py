@@ -73,7 +73,7 @@ WORKLOADS = {
     "sweep": ("MSV+SSV, M=48..2405 sweep vs 1M Swiss-Prot-like synthetic sequences per GPU",
               "both", SWEEP_M, 1_000_000, SWISSPROT),
 }
-VARIANTS = ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm", "fp16xh"]
+VARIANTS = ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm", "fp16xh", "fp16xr"]
 
 
 def log(*a):
@@ -459,7 +459,8 @@ def main():
     desc, wl_alg, models_m, nseq, gen = WORKLOADS[args.workload]
     variant = getattr(P.Variant, {"auto": "Auto", "dpx16": "Dpx16", "fp16": "Fp16",
                                   "swar8": "Swar8", "fp16x": "Fp16x", "fp16xalt": "Fp16xAlt",
-                                  "fp16xm": "Fp16xMixed", "fp16xh": "Fp16xHybrid"}[args.variant])
+                                  "fp16xm": "Fp16xMixed", "fp16xh": "Fp16xHybrid",
+                                  "fp16xr": "Fp16xRelaxed"}[args.variant])
     algs = algs_of(wl_alg)
     api = ProductGen(P)
     # the sweep leg shares the Swiss-Prot-like database of C2/C3
@@ -471,7 +472,11 @@ def main():
     db = P.SequenceDB(res, off)
     t_gen = time.perf_counter() - t0
 
-    stream = torch.cuda.current_stream()
+    # one dedicated stream for the scans, the L2 flushes and the timing events
+    # (torch's default stream is the legacy NULL stream, which a context would
+    # not share: lhmm_context_set_stream(NULL) selects its own stream)
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     s = P.Scanner(local)
     s.set_stream(stream.cuda_stream)
     if args.db_budget:
@@ -608,6 +613,7 @@ def main():
             ms = 0.0
             for j in range(args.steps):
                 flush.fill_(1)
+                torch.cuda._sleep(100000)  # ~50 us: the host enqueues the step meanwhile
                 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 ev0.record(stream)
                 launches += step(j, True)
@@ -774,6 +780,7 @@ def main():
                 times, st = [], None
                 for j in range(nst):
                     flush_buf.fill_(1)
+                    torch.cuda._sleep(100000)  # ~50 us: the host enqueues the scan meanwhile
                     st = s1.scan_device(opt, o1[j % keep1][0].data_ptr(),
                                         o1[j % keep1][1].data_ptr())
                     times.append(st["device_ms"])

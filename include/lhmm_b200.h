@@ -79,9 +79,13 @@ enum lhmm_variant {
                                bytes expanded by PRMT), 1.6 table bytes per cell instead
                                of 2.  SSV: relaxed, flagged sequences rescored like FP16X;
                                MSV: two-mode on negated cells (n = 255 - v) */
-    LHMM_VARIANT_FP16XH = 7 /* MSV: two-mode hybrid -- the FP16X exact mode on a 16-bit
+    LHMM_VARIANT_FP16XH = 7, /* MSV: two-mode hybrid -- the FP16X exact mode on a 16-bit
                                table and the FP16XM lazy mode on a mixed table, both in
                                shared memory; SSV: same as FP16XM */
+    LHMM_VARIANT_FP16XR = 8 /* MSV: relaxed -- no 255 cap, f16 subnormal domain, one
+                               HADD2.SAT + one max per cell pair; sequences whose relaxed
+                               score reaches 256-dbias are rescored exactly (the auto
+                               policy uses it for non-saturating profiles); SSV: FP16X */
 };
 
 /* Byte-space constants; mirror of lanehmm::QuantParams

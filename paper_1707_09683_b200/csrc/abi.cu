@@ -109,6 +109,9 @@ const int* rows_list(int variant, int* n) {
     case LHMM_VARIANT_FP16XH:
         *n = int(sizeof(lhmm::kRows_fp16xh) / sizeof(int));
         return lhmm::kRows_fp16xh;
+    case LHMM_VARIANT_FP16XR:
+        *n = int(sizeof(lhmm::kRows_fp16xr) / sizeof(int));
+        return lhmm::kRows_fp16xr;
     default:
         *n = int(sizeof(lhmm::kRows_swar8) / sizeof(int));
         return lhmm::kRows_swar8;
@@ -217,6 +220,8 @@ double model_rate(int variant, int alg, uint32_t L, uint32_t H) {
              variant == LHMM_VARIANT_FP16X_ALT || variant == LHMM_VARIANT_FP16XM ||
              variant == LHMM_VARIANT_FP16XH)
         w = alg == LHMM_MSV ? 4.5 : 3.0;
+    else if (variant == LHMM_VARIANT_FP16XR)
+        w = 3.5;
     else
         w = alg == LHMM_MSV ? 4.5 : 3.5;
     const double lg = std::log2(double(L));
@@ -239,20 +244,25 @@ struct Choice {
 // calibration sweep (calib_b200.inc from scripts/calibrate.py) and fill the
 // fraction of the persistent grid's warps the database's work items
 // (tiles * L) can occupy.  `want_L` pins the lane count when non-zero.
+// two_mode_ok: MSV -- scores (believed to) saturate, so the two-mode kernels
+// apply; SSV -- the relaxed kernels rescore few sequences.  relaxed_msv_ok
+// (MSV, scores known not to saturate): the relaxed FP16XR kernel rescored few
+// sequences (or has not run yet on this database).
 Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64_t n_tiles,
-                       int sm_count, bool two_mode_ok = true) {
+                       int sm_count, bool two_mode_ok = true, bool relaxed_msv_ok = false) {
     Choice best;
     // auto considers the measured variants only (calib_b200.inc); the
     // relaxed FP16X also needs a database large enough to amortise its
     // rescoring check.  Without any measurement the cost model decides.
     // FP16X stands for both of its code forms (FP16X, FP16X_ALT): the
     // measured table picks the faster one per geometry
-    const int vs_auto[6] = {LHMM_VARIANT_FP16, LHMM_VARIANT_DPX16, LHMM_VARIANT_FP16X,
-                            LHMM_VARIANT_FP16X_ALT, LHMM_VARIANT_FP16XM, LHMM_VARIANT_FP16XH};
+    const int vs_auto[7] = {LHMM_VARIANT_FP16, LHMM_VARIANT_DPX16, LHMM_VARIANT_FP16X,
+                            LHMM_VARIANT_FP16X_ALT, LHMM_VARIANT_FP16XM, LHMM_VARIANT_FP16XH,
+                            LHMM_VARIANT_FP16XR};
     const int vs_x[4] = {LHMM_VARIANT_FP16X, LHMM_VARIANT_FP16X_ALT, LHMM_VARIANT_FP16XM,
                          LHMM_VARIANT_FP16XH};
     const int* vs = variant == LHMM_VARIANT_AUTO ? vs_auto : vs_x;
-    const int nv = variant == LHMM_VARIANT_AUTO ? 6 : (variant == LHMM_VARIANT_FP16X ? 4 : 1);
+    const int nv = variant == LHMM_VARIANT_AUTO ? 7 : (variant == LHMM_VARIANT_FP16X ? 4 : 1);
     for (int pass = 0; pass < 2 && best.L == 0; ++pass) {
         const bool measured_only = variant == LHMM_VARIANT_AUTO && pass == 0;
         for (int vi = 0; vi < nv; ++vi) {
@@ -269,6 +279,10 @@ Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64
             // MSV: the two-mode kernel's table rates assume saturating scores;
             // SSV: the relaxed kernel's, that few sequences need rescoring
             if (variant == LHMM_VARIANT_AUTO && x && !two_mode_ok) continue;
+            // relaxed MSV: only for profiles whose scores do not saturate
+            if (variant == LHMM_VARIANT_AUTO && v == LHMM_VARIANT_FP16XR &&
+                (two_mode_ok || !relaxed_msv_ok))
+                continue;
             const uint32_t cpw = lhmm::cells_per_word(v);
             int n;
             const int* rows = rows_list(v, &n);
@@ -342,6 +356,9 @@ struct ProfileSlot {
     // SSV: fraction of sequences the relaxed FP16X kernel had to rescore
     double flag_frac = -1.0;
     uint64_t flag_gen = 0;
+    // MSV: fraction the relaxed FP16XR kernel had to rescore
+    double msv_flag_frac = -1.0;
+    uint64_t msv_flag_gen = 0;
     void release() {
         for (auto& kv : tables) kv.second.buf.release();
         for (auto& kv : lens) {
@@ -358,6 +375,7 @@ struct lhmm_context {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_done = nullptr;        // end of a scan's bookkeeping copies
     cudaStream_t copy_stream = nullptr;   // H2D of streamed scans
     bool stream_mem_ops = false;          // cuStreamWriteValue32 usable (single-launch streaming)
     // the driver entry point, resolved at run time (no link-time libcuda)
@@ -609,7 +627,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
     if (opt->alg != LHMM_MSV && opt->alg != LHMM_SSV)
         return set_error(LHMM_ERR_CONTRACT, "unknown algorithm");
-    if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_FP16XH)
+    if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_FP16XR)
         return set_error(LHMM_ERR_CONTRACT, "unknown kernel variant");
     if (opt->reorder_mode != 0 && opt->reorder_mode != 1)
         return set_error(LHMM_ERR_CONTRACT, "unknown reorder mode");
@@ -621,6 +639,8 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         variant = LHMM_VARIANT_FP16X;  // the ALT code form is MSV-only
     if (variant == LHMM_VARIANT_FP16XH && opt->alg == LHMM_SSV)
         variant = LHMM_VARIANT_FP16XM;  // the hybrid is an MSV form
+    if (variant == LHMM_VARIANT_FP16XR && opt->alg == LHMM_SSV)
+        variant = LHMM_VARIANT_FP16X;   // relaxed SSV is FP16X
 
     uint32_t L = opt->lanes, H = opt->rows;
     if (L != 0 && (L > 32 * kMaxLongK || (L & (L - 1))))
@@ -645,13 +665,21 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
                 ? !(view == nullptr && pf.sat_gen == c->db_gen && pf.sat_frac >= 0.0 &&
                     pf.sat_frac < 0.5)
                 : !(view == nullptr && pf.flag_gen == c->db_gen && pf.flag_frac > 0.2);
+        // non-saturating MSV: the relaxed FP16XR kernel unless it had to
+        // rescore more than 20% of this database
+        const bool relaxed_msv_ok =
+            opt->alg == LHMM_MSV &&
+            !(view == nullptr && pf.msv_flag_gen == c->db_gen && pf.msv_flag_frac > 0.2);
         const auto ckey =
-            std::make_tuple(pf.m, opt->alg, variant, L, v.n_tiles + (two_mode_ok ? 0 : (1ull << 62)));
+            std::make_tuple(pf.m, opt->alg, variant, L,
+                            v.n_tiles + (two_mode_ok ? 0 : (1ull << 62)) +
+                                (relaxed_msv_ok ? 0 : (1ull << 61)));
         const auto cit = c->choices.find(ckey);
         if (cit != c->choices.end()) {
             std::tie(ch.variant, ch.L, ch.H) = cit->second;
         } else {
-            ch = choose_geometry(pf.m, opt->alg, variant, L, v.n_tiles, c->sm_count, two_mode_ok);
+            ch = choose_geometry(pf.m, opt->alg, variant, L, v.n_tiles, c->sm_count, two_mode_ok,
+                                 relaxed_msv_ok);
             if (c->choices.size() > 256) c->choices.clear();
             c->choices.emplace(ckey, std::make_tuple(ch.variant, ch.L, ch.H));
         }
@@ -774,8 +802,9 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         p.mode_rows = c->d_mode_rows.ptr;
     }
     p.wrap = opt->reorder_mode == 1 ? 1u : 0u;
-    const bool relaxed = (variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16XM) &&
-                         opt->alg == LHMM_SSV;
+    const bool relaxed = ((variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16XM) &&
+                          opt->alg == LHMM_SSV) ||
+                         (variant == LHMM_VARIANT_FP16XR && opt->alg == LHMM_MSV);
     if (relaxed) {
         if (int rc = c->d_flag.reserve(
                 std::max<uint64_t>(global_out ? c->n_global : c->db.n_local, 1)))
@@ -974,6 +1003,9 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     uint32_t* counts = c->counts_host.reserve(32) ? reinterpret_cast<uint32_t*>(c->counts_host.ptr)
                                                   : nullptr;
     uint64_t mode_rows[2] = {0, 0};
+    // the scan kernel's window ends here; the bookkeeping copies below are
+    // synchronised through ev_done
+    CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
     if (counts) {
         if (track_sat)
             CUDA_TRY(cudaMemcpyAsync(counts, c->d_sat.ptr, 4, cudaMemcpyDeviceToHost, c->stream));
@@ -984,8 +1016,9 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             CUDA_TRY(cudaMemcpyAsync(counts + 2, c->d_mode_rows.ptr, 16, cudaMemcpyDeviceToHost,
                                      c->stream));
     }
-    CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
-    CUDA_TRY(cudaEventSynchronize(c->ev1));
+    if (!c->ev_done) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(c->ev_done, c->stream));
+    CUDA_TRY(cudaEventSynchronize(c->ev_done));
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
     uint32_t nsat = 0;
@@ -1043,8 +1076,13 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             recomputed = nsel;
         }
         if (view == nullptr && v.sequences > 0) {
-            pf.flag_frac = double(nflag) / double(v.sequences);
-            pf.flag_gen = c->db_gen;
+            if (opt->alg == LHMM_MSV) {
+                pf.msv_flag_frac = double(nflag) / double(v.sequences);
+                pf.msv_flag_gen = c->db_gen;
+            } else {
+                pf.flag_frac = double(nflag) / double(v.sequences);
+                pf.flag_gen = c->db_gen;
+            }
         }
         CUDA_TRY(cudaEventRecord(c->evr1, c->stream));
         CUDA_TRY(cudaEventSynchronize(c->evr1));
@@ -1467,6 +1505,7 @@ int lhmm_context_destroy(lhmm_context* c) {
     c->d_pass.release();
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);
+    if (c->ev_done) cudaEventDestroy(c->ev_done);
     for (auto e : c->seg_events) cudaEventDestroy(e);
     cudaStreamDestroy(c->copy_stream);
     cudaStreamDestroy(c->own_stream);
@@ -1518,6 +1557,8 @@ static int fill_profile(ProfileSlot& pf, const uint8_t* costs, uint32_t m, const
     pf.sat_gen = 0;
     pf.flag_frac = -1.0;
     pf.flag_gen = 0;
+    pf.msv_flag_frac = -1.0;
+    pf.msv_flag_gen = 0;
     return LHMM_OK;
 }
 

@@ -317,6 +317,9 @@ static uint32_t encode_word(int variant, int alg, const uint8_t* c, uint32_t cpw
                    ((variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16X_ALT) &&
                     alg == LHMM_MSV)) {
             e = uint16_t(-int(c[k]));
+        } else if (variant == LHMM_VARIANT_FP16XR) {  // MSV: dbias - cost, signed subnormal
+            const int t = int(dbias) - int(c[k]);
+            e = t >= 0 ? uint32_t(t) : 0x8000u | uint32_t(-t);
         } else if (variant == LHMM_VARIANT_FP16X) {  // SSV: (dbias - cost)/256
             e = half_bits((float(dbias) - float(c[k])) / 256.f);
         } else {  // FP16: -(cost+1)/256 (MSV) or -(cost+1)/128 (SSV)

@@ -492,6 +492,67 @@ struct Fp16Mixed {
     }
 };
 
+// FP16XR, MSV ("relaxed"): the MSV recurrence without the 255 cap, in the
+// f16 SUBNORMAL domain (a bit pattern is its value in units of 2^-24, byte v
+// is pattern v), one HADD2.SAT + one integer max per word:
+//     cell = HADD2.SAT(max(x, B), dbias - cost)      (clamp at +0 = byte 0)
+// with the table entry dbias - cost as a signed subnormal f16 (16-bit table,
+// four rows per LDS.128).  B = max(base, E (-) (tec+tjb)) runs on the same
+// patterns (HADD2.SAT, then max).  Exactness: before the first cap event the
+// relaxed and the saturating recurrences agree, and a cap event needs an input
+// above 255 - dbias -- a cell above 255 - dbias, which the running E records
+// (B itself stays <= max(base, E) and base + dbias <= 255).  So every
+// sequence with relaxed raw < 256 - dbias is exact and the others are flagged
+// and rescored by the exact Fp16 kernel in the same scan (abi.cu), as for the
+// relaxed SSV forms.  The policy uses it for profiles whose MSV scores mostly
+// do not saturate (two-mode feedback), where the two-mode kernels never leave
+// their ALU-heavier exact mode: ALU 1.5 + FP16 1 instructions per word
+// against ALU 2.5 + FP16 1.
+template <int ALG>
+struct Fp16RelaxedMsv {
+    static_assert(ALG == 0, "the relaxed MSV form (FP16XR) is MSV only");
+    static constexpr int CPW = 2;
+    static constexpr bool kMsv = true;
+    static constexpr bool kRelaxed = true;
+    static constexpr bool kTwoMode = false;
+    static constexpr uint32_t NEG = 0u;  // byte 0 in both halves
+    struct St {
+        uint32_t B, base2, ntj2, cap;
+    };
+    __device__ static __forceinline__ void init(St& s, uint32_t base, const KParams& p) {
+        s.base2 = base * 0x00010001u;
+        s.B = s.base2;
+        const uint32_t tj = p.tecjb > 1023u ? 1023u : p.tecjb;  // (tec + tjb <= 510)
+        s.ntj2 = (0x8000u | tj) * 0x00010001u;  // -(tec+tjb) as a subnormal f16
+        s.cap = 256u - p.dbias;
+    }
+    __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
+    template <bool LAZY = false>
+    __device__ static __forceinline__ uint32_t inject(const St&) { return NEG; }
+    template <bool LAZY = false, bool FPW = false>
+    __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
+        return as_u32(__hadd2_sat(as_h2(__vmaxu2(x, s.B)), as_h2(c)));
+    }
+    __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
+        return __vimax3_u16x2(E, a, b);
+    }
+    __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
+        return __byte_perm(top, up, 0x1076);
+    }
+    template <int L>
+    __device__ static __forceinline__ uint32_t group_reduce(uint32_t E) {
+        const uint32_t e = __vmaxu2(E, __byte_perm(E, E, 0x1032));
+        return group_max<L>(e);
+    }
+    __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
+        s.B = __vmaxu2(as_u32(__hadd2_sat(as_h2(e), as_h2(s.ntj2))), s.base2);
+    }
+    __device__ static __forceinline__ uint32_t raw(uint32_t e) { return e & 0xffffu; }
+    __device__ static __forceinline__ bool needs_exact(uint32_t raw, const St& s) {
+        return raw >= s.cap;
+    }
+};
+
 // FP16XM, MSV (two-mode like Fp16Sat, mixed table like Fp16Mixed).  The
 // cells live NEGATED in the f16 subnormal domain: pattern n = 255 - v (units
 // of 2^-24), so the byte cap v <= 255 is HADD2.SAT's clamp at +0, the floor
@@ -1114,10 +1175,26 @@ __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KPar
     uint32_t ready_below = 0;
     unsigned long long rows_all = 0, rows_lazy = 0;  // two-mode MSV statistics
 
+    // First wave: a static snake assignment balances the SMSPs.  Items come
+    // longest first; warp w of a CTA issues on SMSP w % 4, so round r = w / 4
+    // of SMSP s takes item r * nS + s (r even) or r * nS + nS - 1 - s (r odd),
+    // and every SMSP's first items sum to about the same number of rows (a
+    // small database has barely more items than warps, so the first wave IS
+    // the scan).  Later items are claimed from the counter, longest first.
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t n_smsp = gridDim.x * 4u;
+    const uint32_t smsp = blockIdx.x * 4u + (warp & 3u), round = warp >> 2;
+    uint32_t next_static =
+        round * n_smsp + ((round & 1u) ? n_smsp - 1u - smsp : smsp);
+    const uint32_t n_first = gridDim.x * (blockDim.x >> 5);
+
     for (;;) {
-        uint32_t item = 0;
-        if (lane == 0) item = atomicAdd(p.counter, 1u);
-        item = __shfl_sync(kFull, item, 0);
+        uint32_t item = next_static;
+        if (item == 0xffffffffu) {
+            if (lane == 0) item = n_first + atomicAdd(p.counter, 1u);
+            item = __shfl_sync(kFull, item, 0);
+        }
+        next_static = 0xffffffffu;
         if (item >= p.n_items) break;
         const uint32_t tile = p.tile_base + item / L;
         if (p.n_pieces) wait_for_tile(p, tile, ready_below);  // warp-uniform

@@ -24,16 +24,20 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--algs", default="msv,ssv")
     ap.add_argument("--lanes", default="", help="subset of lane counts, e.g. 16,32")
+    ap.add_argument("--quant", default="default", choices=["default", "nonsat"],
+                    help="nonsat = QuantParams{3,120,3,20,20} (MSV scores that do not saturate: "
+                         "the regime the relaxed FP16XR kernel is chosen for)")
     args = ap.parse_args()
     lanes = [int(x) for x in args.lanes.split(",")] if args.lanes else gen_instances.LANES
     db = P.Rng(0x5EED).lognormal_records(args.nseq, 290, 0.65, 2)
-    q = P.QuantParams()
+    q = P.QuantParams() if args.quant == "default" else P.QuantParams(3.0, 120, 3, 20, 20)
     s = P.Scanner(0)
     s.set_database(db)
     res = db.total_residues()
     vmap = {"dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16, "swar8": P.Variant.Swar8,
             "fp16x": P.Variant.Fp16x, "fp16xalt": P.Variant.Fp16xAlt,
-            "fp16xm": P.Variant.Fp16xMixed, "fp16xh": P.Variant.Fp16xHybrid}
+            "fp16xm": P.Variant.Fp16xMixed, "fp16xh": P.Variant.Fp16xHybrid,
+            "fp16xr": P.Variant.Fp16xRelaxed}
     for vn in args.variants.split(","):
         cpw = 4 if vn == "swar8" else 2
         for L in lanes:
@@ -54,6 +58,7 @@ def main():
                         continue
                     g = res * m / (t * 1e-3) / 1e9
                     print(json.dumps({"variant": vn, "alg": a, "lanes": L, "rows": H, "M": m,
+                                      "quant": args.quant,
                                       "gcups": round(g, 1),
                                       "cell_gcups": round(g * cap / m, 1)}), flush=True)
     s.close()

@@ -91,7 +91,8 @@ def golden_inputs(c):
 
 
 FORMS = {"msv": [P.Variant.Auto, P.Variant.Fp16, P.Variant.Dpx16, P.Variant.Fp16x,
-                 P.Variant.Fp16xAlt, P.Variant.Fp16xMixed, P.Variant.Fp16xHybrid],
+                 P.Variant.Fp16xAlt, P.Variant.Fp16xMixed, P.Variant.Fp16xHybrid,
+                 P.Variant.Fp16xRelaxed],
          "ssv": [P.Variant.Auto, P.Variant.Fp16, P.Variant.Dpx16, P.Variant.Fp16x,
                  P.Variant.Fp16xMixed]}
 
@@ -222,6 +223,67 @@ def test_two_mode_msv_reports_lazy_rows():
             assert lo <= frac <= hi, frac
             rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv, variant=P.Variant.Fp16))
             assert rep.stats["mode_rows"] == 0  # one-mode kernel
+
+
+QUANTS = [DEFAULT, NONSAT, P.QuantParams(2.0, 240, 10, 1, 5), P.QuantParams(3.0, 0, 0, 0, 0)]
+
+
+def fp16xr_rows():
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(P.__file__), "csrc"))
+    import gen_instances
+    return gen_instances.ROWS["fp16xr"]
+
+
+@pytest.mark.parametrize("L", [1, 2, 4, 8, 16, 32])
+def test_relaxed_msv_matches_oracle(chk, L):
+    """FP16XR (relaxed MSV, no 255 cap, f16 subnormal domain): every lane
+    count, the four QuantParams sets, full and partial top row groups, planted
+    motifs so that at the saturating parameters many sequences are flagged and
+    rescored exactly in the same scan."""
+    rng = P.Rng(0x7E1 + L)
+    rows = fp16xr_rows()
+    for t, q in enumerate(QUANTS):
+        for m in (2 * L * rows[min(len(rows) - 1, 3 + t)] - int(rng.next() % (2 * L)), 37):
+            m = max(1, m)
+            hmm = rng.random_profile(m)
+            db = rng.random_records(400, 1, 500, plant=(hmm, 0.3))
+            costs = P.quantize_emissions(hmm, q)
+            H = next(h for h in rows if 2 * L * h >= m)
+            with P.Scanner(0) as s:
+                s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+                s.set_database(db)
+                rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv, variant=P.Variant.Fp16xRelaxed,
+                                           lanes=L, rows=H, threshold=0.2))
+            assert rep.variant == int(P.Variant.Fp16xRelaxed) and rep.rows == H
+            want = chk.raw(P.Algorithm.Msv, costs, db, q)
+            np.testing.assert_array_equal(rep.raw, want, err_msg=f"L={L} m={m} q={q}")
+            np.testing.assert_array_equal(rep.passed,
+                                          chk.passed(P.Algorithm.Msv, want, db, hmm, q, 0.2))
+            flagged = int((want >= 256 - q.dbias).sum())
+            assert rep.stats["recomputed"] >= flagged
+
+
+def test_policy_picks_relaxed_msv_for_non_saturating_profiles(chk):
+    """The first MSV scan of a profile runs a two-mode kernel and counts
+    saturated scores; a non-saturating profile then runs the relaxed FP16XR
+    kernel, a saturating one stays on the two-mode kernels -- all exact."""
+    hmm, db = large_db()
+    with P.Scanner(0) as s:
+        s.set_database(db)
+        for q, later in ((NONSAT, {int(P.Variant.Fp16xRelaxed)}),
+                         (DEFAULT, {int(P.Variant.Fp16x), int(P.Variant.Fp16xAlt),
+                                    int(P.Variant.Fp16xMixed), int(P.Variant.Fp16xHybrid)})):
+            costs = P.quantize_emissions(hmm, q)
+            s.set_profile(costs, q, hmm.lambda_, hmm.tau)
+            want = chk.raw(P.Algorithm.Msv, costs, db, q)
+            seen = []
+            for _ in range(3):
+                rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv, threshold=0.022))
+                np.testing.assert_array_equal(rep.raw, want)
+                seen.append(rep.variant)
+            assert seen[0] != int(P.Variant.Fp16xRelaxed)
+            assert seen[1] in later and seen[2] in later, seen
 
 
 def test_subnormal_selfcheck_refuses_flush_to_zero(monkeypatch):

@@ -29,7 +29,8 @@ def rows_list(variant):
                                P.Variant.Fp16: "fp16", P.Variant.Fp16x: "fp16x",
                                P.Variant.Fp16xAlt: "fp16xalt",
                                P.Variant.Fp16xMixed: "fp16xm",
-                               P.Variant.Fp16xHybrid: "fp16xh"}[variant]]
+                               P.Variant.Fp16xHybrid: "fp16xh",
+                               P.Variant.Fp16xRelaxed: "fp16xr"}[variant]]
 
 
 def rows_for(variant, L, m):
@@ -379,15 +380,15 @@ def wrap_model(alg, costs, m, seq, q, base):
 
 @pytest.mark.parametrize("variant", [P.Variant.Fp16, P.Variant.Dpx16, P.Variant.Swar8,
                                      P.Variant.Fp16x, P.Variant.Fp16xAlt, P.Variant.Fp16xMixed,
-                                     P.Variant.Fp16xHybrid],
+                                     P.Variant.Fp16xHybrid, P.Variant.Fp16xRelaxed],
                          ids=lambda v: v.name)
 @pytest.mark.parametrize("alg", [P.Algorithm.Msv, P.Algorithm.Ssv], ids=lambda a: a.name)
 def test_paper_wrap_mode(ora, variant, alg):
     """The non-normative wrap study mode runs, matches its model, and differs
     from the normative (oracle-exact) -inf injection on a consensus-heavy
     instance (test_engine.cpp:265-278)."""
-    if variant == P.Variant.Fp16xHybrid and alg == P.Algorithm.Ssv:
-        pytest.skip("the hybrid is an MSV form (SSV runs FP16XM, tested above)")
+    if variant in (P.Variant.Fp16xHybrid, P.Variant.Fp16xRelaxed) and alg == P.Algorithm.Ssv:
+        pytest.skip("an MSV form (SSV runs FP16XM / FP16X, tested above)")
     cpw = 4 if variant == P.Variant.Swar8 else 2
     differs = False
     geoms = {P.Variant.Fp16xMixed: ((1, 10), (2, 10), (8, 5), (32, 5)),
@@ -418,11 +419,14 @@ def test_paper_wrap_mode(ora, variant, alg):
     assert differs
 
 
-@pytest.mark.parametrize("variant", [P.Variant.Fp16, P.Variant.Fp16x], ids=lambda v: v.name)
+@pytest.mark.parametrize("variant", [P.Variant.Fp16, P.Variant.Fp16x, P.Variant.Fp16xRelaxed],
+                         ids=lambda v: v.name)
 @pytest.mark.parametrize("alg", [P.Algorithm.Msv, P.Algorithm.Ssv], ids=lambda a: a.name)
 def test_two_row_top_group(ora, variant, alg):
     """H = 2 (mod 4): the top row group is read with LDS.64 and folded as a
     pair; every lane count, models that fill the last rows exactly."""
+    if variant == P.Variant.Fp16xRelaxed and alg == P.Algorithm.Ssv:
+        pytest.skip("FP16XR is an MSV form")
     q = P.QuantParams(3.0, 120, 3, 20, 20)
     for L in (1, 2, 4, 8, 16, 32):
         for H in (34, 38, 70):
