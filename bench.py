@@ -7,8 +7,19 @@ M = 48 / 400 / 1000 over 1M Swiss-Prot-like synthetic sequences per GPU
 (synth::lognormal_records(1e6, 290, 0.65, 2), seed 0x5EED; models
 synth::random_profile(seed 7000+M)).  One step = the three SSV scans over the
 resident database; every cell is computed (no early exit).  GCUPS = real
-residues x M / device seconds.  N>1: weak scaling (N x 1M sequences), the
-database sharded by residue count, raw/pass gathered to rank 0.
+residues x M / device seconds.
+
+Databases are built from independently seeded chunks, so every rank
+generates and packs only its own share:
+  weak (default)  rank r scans chunk r: lognormal_records(1e6, ...) from seed
+                  0x5EED + r (chunk 0 IS the C2 set); N GPUs scan N x 1M;
+  strong          the total is fixed: C2/C3/sweep split the one 1M set into
+                  contiguous slices; C4 (--workload c4 --scaling strong) is 50M
+                  env_nr-like sequences, 400 chunks of 125k (seeds 0xC4000+i),
+                  rank r scanning chunks [400r/N, 400(r+1)/N).
+Ranks hold contiguous ranges of the global order, and results reach rank 0
+through the block gather (shard.BlockGather: one bulk NVLink copy per rank
+and scan into rank 0's IPC-mapped staging buffer).
 
 Beside the headline the same JSON line carries, by default (`--legs`):
   sweep   C5: M = 48..2405, MSV and SSV at the default QuantParams and MSV at
@@ -20,13 +31,16 @@ Beside the headline the same JSON line carries, by default (`--legs`):
   c1      C1: MSV M=200 vs 10k random sequences (seed 0xC1, 5% planted
           motifs), default and non-saturating params, many timed steps with
           the L2 flushed between them.
-  verify  parity: a fixed-stride sample (>= 20k sequences; C1 in full) of the
-          raw bytes and pass bits of EVERY timed scan compared with the
-          reference library's own scalar oracle and finalize_hit
-          (oracle/_ref, test infrastructure) -> "parity": {checked, mismatches}.
+  verify  parity: a fixed-stride sample (>= 20k sequences per rank; C1 in
+          full) of the raw bytes and pass bits of EVERY timed scan compared
+          with the reference library's own scalar oracle and finalize_hit
+          (oracle/_ref, test infrastructure) -> "parity": {checked,
+          mismatches}; at N>1 each rank checks its share and rank 0 checks
+          every gathered block against the rank's CRC32.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--workload c2|c1|c3|c4|sweep] [--legs sweep,c1,verify|none]
+                  [--workload c2|c1|c3|c4|sweep] [--scaling weak|strong]
+                  [--legs sweep,c1,verify|none]
 
 `--impl reference` times the reference's own CPU engine (oracle/_ref,
 lanehmm::scan_database) on the host cores, generating its inputs with the
@@ -43,6 +57,8 @@ import subprocess
 import sys
 import threading
 import time
+import zlib
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -58,21 +74,24 @@ DEFAULT_Q = (3.0, 195, 3, 3, 3)
 NONSAT_Q = (3.0, 120, 3, 20, 20)   # MSV raw ~117-131: scores that do not saturate
 THRESHOLD = 0.022
 SWISSPROT = ("lognormal", 0x5EED, 290.0, 0.65, 2)
+ENVNR = ("lognormal", 0xC4000, 170.0, 0.55, 2)
+C4_CHUNK = 125_000
 SWEEP_M = (48, 100, 200, 400, 800, 1000, 1500, 2000, 2405)
 
 WORKLOADS = {
-    # name: (description, alg, models, nseq per GPU, generator)
+    # name: (description, alg, models, sequences (per GPU, weak), generator)
     "c2": ("SSV, synthetic models M=48/400/1000 vs 1M Swiss-Prot-like synthetic sequences per GPU",
            "ssv", (48, 400, 1000), 1_000_000, SWISSPROT),
     "c1": ("MSV, M=200 vs 10k random sequences (mean ~350 aa, 5% planted motifs)",
            "msv", (200,), 10_000, ("uniform_planted", 0xC1, 50, 650, 0.05)),
     "c3": ("MSV, M=2405 vs 1M Swiss-Prot-like synthetic sequences per GPU",
            "msv", (2405,), 1_000_000, SWISSPROT),
-    "c4": ("MSV+SSV, M=200 vs env_nr-like synthetic sequences (lognormal median 170, sigma 0.55)",
-           "both", (200,), 6_250_000, ("lognormal", 0x5EED, 170.0, 0.55, 2)),
+    "c4": ("MSV+SSV, M=200 vs env_nr-like synthetic sequences (lognormal median 170, sigma "
+           "0.55), 125k-sequence chunks", "both", (200,), 6_250_000, ENVNR),
     "sweep": ("MSV+SSV, M=48..2405 sweep vs 1M Swiss-Prot-like synthetic sequences per GPU",
               "both", SWEEP_M, 1_000_000, SWISSPROT),
 }
+C4_STRONG_TOTAL = 50_000_000
 VARIANTS = ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm", "fp16xh", "fp16xr"]
 
 
@@ -137,21 +156,67 @@ class ReferenceGen:
         return self.ref.quantize(scores, self.oracle.QuantParams(*q))
 
 
-def make_inputs(api, gen, nseq, models_m):
-    """(residues, offsets, {m: (scores, lambda, tau)}).  Swiss-Prot-like and
-    env_nr-like sets: records from seed gen[1], each model from seed 7000+M
-    (SURVEY §8(d)).  C1: one generator for the model, then the records, then
-    the planted motifs (seed 0xC1)."""
-    models = {}
-    if gen[0] == "lognormal":
-        res, off = api.records(api.rng(gen[1]), gen, nseq, None)
-        for m in models_m:
-            models[m] = api.profile(api.rng(7000 + m), m)
+def db_layout(name, scaling, world):
+    """The database as chunks [(seed, count)] and each rank's share as
+    (chunk, first, last) sequence ranges -- contiguous in the global order
+    (chunk-major), so the block gather needs no permutation."""
+    _, _, _, nseq, gen = WORKLOADS[name]
+    if name == "c4":
+        per = nseq // C4_CHUNK
+        n_chunks = C4_STRONG_TOTAL // C4_CHUNK if scaling == "strong" else per * world
+        chunks = [(gen[1] + i, C4_CHUNK) for i in range(n_chunks)]
+        share = [[(i, 0, C4_CHUNK) for i in range(n_chunks * r // world,
+                                                   n_chunks * (r + 1) // world)]
+                 for r in range(world)]
+    elif scaling == "strong" or gen[0] != "lognormal":
+        # one set (C1 / C2 / C3 / sweep) cut into contiguous slices
+        chunks = [(gen[1], nseq)]
+        share = [[(0, nseq * r // world, nseq * (r + 1) // world)] for r in range(world)]
     else:
-        rng = api.rng(gen[1])
-        models[models_m[0]] = api.profile(rng, models_m[0])
-        res, off = api.records(rng, gen, nseq, models[models_m[0]])
-    return (np.ascontiguousarray(res, np.uint8), np.ascontiguousarray(off, np.uint64), models)
+        chunks = [(gen[1] + r, nseq) for r in range(world)]
+        share = [[(r, 0, nseq)] for r in range(world)]
+    return chunks, share
+
+
+def make_chunk(api, gen, seed, count, models_m):
+    """One chunk: (residues, offsets).  Uniform planted (C1): the model is
+    drawn first from the chunk's generator, then the records and motifs."""
+    rng = api.rng(seed)
+    plant = api.profile(rng, models_m[0]) if gen[0] != "lognormal" else None
+    res, off = api.records(rng, gen, count, plant)
+    return np.ascontiguousarray(res, np.uint8), np.ascontiguousarray(off, np.uint64)
+
+
+def make_inputs(api, name, scaling, world, ranks, models_m):
+    """(residues, offsets, global index of the first sequence, {m: (scores,
+    lambda, tau)}) of the union of `ranks`' shares, chunks generated in
+    parallel (the generators release the GIL).  Models: seed 7000+M
+    (Swiss-Prot-like and env_nr-like sets); C1: the chunk's
+    own first draw."""
+    _, _, _, _, gen = WORKLOADS[name]
+    chunks, share = db_layout(name, scaling, world)
+    want = [rg for r in ranks for rg in share[r]]
+    need = sorted({c for c, _, _ in want})
+    with ThreadPoolExecutor(max_workers=min(len(need), os.cpu_count() or 1)) as ex:
+        made = dict(zip(need, ex.map(lambda c: make_chunk(api, gen, chunks[c][0], chunks[c][1],
+                                                          models_m), need)))
+    parts, lens = [], []
+    for c, lo, hi in want:
+        res, off = made[c]
+        parts.append(res[int(off[lo]):int(off[hi])])
+        lens.append(np.diff(off[lo:hi + 1]))
+    res = np.concatenate(parts) if parts else np.zeros(0, np.uint8)
+    off = np.zeros(sum(x.size for x in lens) + 1, np.uint64)
+    if off.size > 1:
+        off[1:] = np.cumsum(np.concatenate(lens))
+    c0, lo0, _ = want[0]
+    first = sum(chunks[c][1] for c in range(c0)) + lo0
+    if gen[0] == "lognormal":
+        profs = {m: api.profile(api.rng(7000 + m), m) for m in models_m}
+    else:
+        profs = {models_m[0]: api.profile(api.rng(chunks[0][0]), models_m[0])}
+    del made
+    return res, off, first, profs
 
 
 def flat_subset(res, off, idx):
@@ -171,16 +236,20 @@ def algs_of(wl_alg):
     return {"ssv": ["ssv"], "msv": ["msv"], "both": ["msv", "ssv"]}[wl_alg]
 
 
-def workload_config(name, desc, models_m, algs, nseq_total, residues, world, packed_bytes=None):
+def workload_config(name, scaling, desc, models_m, algs, nseq_total, residues, world):
     """The `config` object -- identical for both arms of the same run."""
-    l2 = ("inputs larger than L2 (packed database > 126 MB per GPU)"
-          if residues / max(world, 1) > L2_BYTES else
+    chunks, _ = db_layout(name, scaling, world)
+    per_gpu = residues / max(world, 1)
+    l2 = ("inputs larger than L2 (packed database > 126 MB per GPU)" if per_gpu > L2_BYTES else
           "L2 flushed between timed steps (256 MB write outside the timed windows)")
     return {"workload": desc, "name": name, "models": list(models_m), "algorithms": algs,
             "sequences": int(nseq_total), "residues": int(residues), "threshold": THRESHOLD,
-            "quant": qstr(DEFAULT_Q), "data": "synthetic (lanehmm synth:: streams, seeds as in "
-            "SURVEY.md §8(d))", "parallelism": f"{world} rank(s); sequences sharded by residue "
-            "count, raw+pass gathered to rank 0", "l2": l2, "early_exit": False}
+            "quant": qstr(DEFAULT_Q),
+            "database": f"{len(chunks)} chunk(s) of {chunks[0][1]} sequences from seeds "
+                        f"{chunks[0][0]:#x}..{chunks[-1][0]:#x} (synth:: streams, SURVEY §8(d))",
+            "parallelism": f"{world} rank(s), contiguous shares of the global order, "
+                           "raw+pass gathered to rank 0",
+            "l2": l2, "early_exit": False}
 
 
 class ClockSampler:
@@ -306,6 +375,11 @@ def cpu_reference_gcups(res, off, models, algs, q, sample_n, also=True):
 # ---------------------------------------------------------------------------
 # reference arm
 
+def effective_scaling(name, scaling):
+    gen = WORKLOADS[name][4]
+    return "strong" if scaling == "strong" or gen[0] != "lognormal" else "weak"
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -313,9 +387,10 @@ def run_reference(args):
     import oracle  # the reference library only; the product .so is never loaded
     ref = oracle.Reference()
     api = ReferenceGen(ref, oracle)
-    desc, wl_alg, models_m, nseq, gen = WORKLOADS[args.workload]
+    desc, wl_alg, models_m, _, _ = WORKLOADS[args.workload]
     algs = algs_of(wl_alg)
-    res, off, profs = make_inputs(api, gen, nseq * world, models_m)
+    res, off, _, profs = make_inputs(api, args.workload, args.scaling, world, range(world),
+                                     models_m)
     models = [(m, *profs[m], api.quantize(profs[m][0], DEFAULT_Q)) for m in models_m]
     vals, r = [], None
     for i in range(args.warmup + args.steps):
@@ -324,11 +399,12 @@ def run_reference(args):
         if i >= args.warmup:
             vals.append(r["value"])
     v = statistics.median(vals) if vals else r["value"]
-    cfg = workload_config(args.workload, desc, models_m, algs, off.size - 1, int(off[-1]), world)
+    cfg = workload_config(args.workload, args.scaling, desc, models_m, algs, off.size - 1,
+                          int(off[-1]), world)
     line = {"metric": METRIC, "value": v, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "impl": "reference", "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": cfg, "cpu_baseline": {**r, "value": v},
+            "scaling": effective_scaling(args.workload, args.scaling), "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic", "config": cfg, "cpu_baseline": {**r, "value": v},
             "e2e": {"value": v, "unit": "GCUPS", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -343,10 +419,11 @@ class Verifier:
     oracle/_ref (the reference's scalar_msv / scalar_ssv and finalize_hit) at
     the end, outside every timed region."""
 
-    def __init__(self, res, off, sample_n):
+    def __init__(self, res, off, sample_n, threads=0):
         self.res, self.off, self.n = res, off, off.size - 1
         self.idx = sample_idx(self.n, sample_n)
         self.sres, self.soff = flat_subset(res, off, self.idx)
+        self.threads = threads or (os.cpu_count() or 1)
         self.items = []     # (key, leg, raw sample, pass sample)
         self.models = {}    # key -> (alg, costs, q, lam, tau)
 
@@ -370,10 +447,10 @@ class Verifier:
             oq = oracle.QuantParams(*q)
             a = 0 if alg == "msv" else 1
             if chk is not None:
-                raw = chk.scalar_flat(a, costs, self.sres, self.soff, oq)
+                raw = chk.scalar_flat(a, costs, self.sres, self.soff, oq, self.threads)
                 ps = chk.pass_flat(a, raw, self.soff, lam, tau, oq, THRESHOLD)
             else:
-                raw = ora.scan_flat(a, costs, self.sres, self.soff, oq, os.cpu_count() or 1)
+                raw = ora.scan_flat(a, costs, self.sres, self.soff, oq, self.threads)
                 lens = np.diff(self.soff)
                 ps = np.array([ora.passes(int(r), int(ln), lam, tau, oq, a, THRESHOLD)
                                for r, ln in zip(raw, lens)], np.uint8)
@@ -390,24 +467,37 @@ class Verifier:
             d["mismatches"] += mism
         return {"checked": checked, "mismatches": bad, "sequences_per_scan": int(self.idx.size),
                 "of": int(self.n), "scans": len(self.items), "legs": per_leg,
-                "what": "raw byte + pass bit of a fixed-stride sample of every timed scan "
-                        "(C1: every sequence)", "checker": checker,
-                "seconds": round(time.perf_counter() - t0, 2)}
+                "checker": checker, "seconds": round(time.perf_counter() - t0, 2)}
+
+
+def merge_parity(a, b):
+    if a is None:
+        return b
+    for k in ("checked", "mismatches", "scans"):
+        a[k] += b[k]
+    for leg, d in b["legs"].items():
+        t = a["legs"].setdefault(leg, {"scans": 0, "checked": 0, "mismatches": 0})
+        for k in d:
+            t[k] += d[k]
+    a["seconds"] = round(a["seconds"] + b["seconds"], 2)
+    return a
 
 
 # ---------------------------------------------------------------------------
 
-def main():
+def main():  # noqa: C901
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: fixed work per GPU; strong: fixed total (C4: 50M sequences)")
     ap.add_argument("--legs", default="sweep,c1,verify",
                     help="extra legs beside the headline: sweep, c1, verify (or 'none')")
     ap.add_argument("--variant", default="auto", choices=VARIANTS)
-    ap.add_argument("--nseq", type=int, default=0, help="override sequences per GPU")
+    ap.add_argument("--nseq", type=int, default=0, help="override sequences per GPU (weak)")
     ap.add_argument("--ref-sample", type=int, default=20000)
     ap.add_argument("--verify-sample", type=int, default=20000)
     ap.add_argument("--sweep-steps", type=int, default=3)
@@ -418,8 +508,9 @@ def main():
     ap.add_argument("--algs", default="", help="override algorithms: msv, ssv or both")
     ap.add_argument("--backend", default=os.environ.get("LHMM_DIST_BACKEND", "nccl"),
                     help="torch.distributed backend for N>1 (gloo lets ranks share one GPU)")
-    ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
-                    help="N>1: fused peer-store gather (default) or a torch.distributed gather")
+    ap.add_argument("--gather", default="block", choices=["block", "nccl"],
+                    help="N>1: bulk peer-copy block gather (default) or a torch.distributed "
+                         "gather of 2 bytes per sequence")
     ap.add_argument("--db-budget", type=int, default=0,
                     help="device bytes for the packed database (0 = resident); larger databases "
                          "are streamed from pinned host memory on every scan")
@@ -457,6 +548,7 @@ def main():
             dist.init_process_group(args.backend)
             comm_dev = torch.device("cpu")
     desc, wl_alg, models_m, nseq, gen = WORKLOADS[args.workload]
+    scaling = effective_scaling(args.workload, args.scaling)
     variant = getattr(P.Variant, {"auto": "Auto", "dpx16": "Dpx16", "fp16": "Fp16",
                                   "swar8": "Swar8", "fp16x": "Fp16x", "fp16xalt": "Fp16xAlt",
                                   "fp16xm": "Fp16xMixed", "fp16xh": "Fp16xHybrid",
@@ -466,9 +558,11 @@ def main():
     # the sweep leg shares the Swiss-Prot-like database of C2/C3
     sweep_on = "sweep" in legs and gen == SWISSPROT
     all_m = sorted(set(models_m) | (set(SWEEP_M) if sweep_on else set()))
+    host_threads = max(1, (os.cpu_count() or 1) // world)
 
+    # this rank's share only: every rank generates and packs its own chunks
     t0 = time.perf_counter()
-    res, off, profs = make_inputs(api, gen, nseq * world, all_m)
+    res, off, first, profs = make_inputs(api, args.workload, args.scaling, world, [rank], all_m)
     db = P.SequenceDB(res, off)
     t_gen = time.perf_counter() - t0
 
@@ -482,10 +576,15 @@ def main():
     if args.db_budget:
         s.set_db_budget(args.db_budget)
     t0 = time.perf_counter()
-    n_local = s.set_database(db, rank, world)
+    n_local = s.set_database(db)
     t_pack = time.perf_counter() - t0
-    gidx = torch.from_numpy(s.shard_indices().astype(np.int64)).cuda()
     dbstats = s.database_stats()
+    tot = torch.tensor([float(n_local), float(dbstats["residues"])], dtype=torch.float64,
+                       device=comm_dev)
+    if dist:
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    n_total, residues_total = int(tot[0].item()), int(tot[1].item())
+    gidx = first + np.arange(n_local, dtype=np.int64)
     info = s.device_info()
     peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
@@ -507,9 +606,7 @@ def main():
                              variant=variant, lanes=args.lanes, rows=args.rows,
                              threshold=THRESHOLD)
 
-    verifier = None
-    if "verify" in legs and rank == 0:
-        verifier = Verifier(res, off, args.verify_sample)
+    verifier = Verifier(res, off, args.verify_sample, host_threads) if "verify" in legs else None
 
     scans = [(m, a) for m in models_m for a in algs]
     for m, _ in scans:
@@ -521,71 +618,50 @@ def main():
     per_launch = {k: [] for k in range(len(scans))}
     geo = {}
 
-    # N>1: the fused gather -- every rank's scan kernel stores its results in
-    # rank 0's buffers (CUDA IPC / NVLink peer memory) by global index; the
-    # NCCL gather below is the fallback if the mapping is unavailable
-    peer = None
-    if world > 1 and args.gather == "p2p":
-        try:
-            from paper_1707_09683_b200.shard import PeerOutputs
-            peer = PeerOutputs(dist, s, db.count, n_scans=len(scans), comm_device=comm_dev)
-            peer.mark_unwritten()
-        except Exception as e:  # noqa: BLE001
-            log(f"[bench] fused peer gather unavailable ({e}); using the NCCL gather")
-            peer = None
-    gather_mode = "fused peer stores (CUDA IPC)" if peer else "torch.distributed gather"
+    # N>1: results to rank 0 -- bulk peer copies of each rank's contiguous
+    # block into rank 0's IPC-mapped staging (shard.BlockGather), or the
+    # 2-byte-per-sequence torch.distributed gather
+    gatherer, gather_mode = None, None
+    if world > 1:
+        from paper_1707_09683_b200.shard import BlockGather, NcclGather
+        if args.gather == "block":
+            try:
+                gatherer = BlockGather(dist, s, gidx, n_total, n_scans=len(scans),
+                                       comm_device=comm_dev)
+                gatherer.mark_unwritten()
+                gather_mode = "block gather (one bulk peer copy per rank and scan, CUDA IPC)"
+            except Exception as e:  # noqa: BLE001
+                log(f"[bench] block gather unavailable ({e}); using the collective gather")
+        if gatherer is None:
+            gatherer = NcclGather(dist, gidx, n_total, comm_dev)
+            gather_mode = "torch.distributed gather, 2 bytes per sequence"
+
+    def gather_scan(k, o):
+        if world == 1:
+            return None
+        if hasattr(gatherer, "push"):
+            gatherer.push(k, o[0].data_ptr(), o[1].data_ptr())
+            return None
+        return gatherer.gather(o[0][:n_local], o[1][:n_local], as_numpy=False)
 
     def step(j, record):
         launches = 0
         for k, (m, a) in enumerate(scans):
             s.select_profile(profile_id(m, DEFAULT_Q)[0])
-            if peer is not None:
-                st = s.scan_device_global(opt_for(a), peer.raw(k), peer.passed(k))
-            else:
-                o = outs[(k, j % keep)]
-                st = s.scan_device(opt_for(a), o[0].data_ptr(), o[1].data_ptr())
+            o = outs[(k, j % keep)]
+            st = s.scan_device(opt_for(a), o[0].data_ptr(), o[1].data_ptr())
+            gather_scan(k, o)
             launches += st["launches"]
             geo[k] = st
             if record:
                 per_launch[k].append(st["device_ms"])
+        if world > 1 and hasattr(gatherer, "finish"):
+            for k in range(len(scans)):
+                gatherer.finish(k)
         return launches
 
-    gathered = {"validated": False}
-
-    def gather_results():
-        """Per-sequence raw + pass bytes of every scan to rank 0.  With the
-        fused gather the scans already wrote them; the first call checks that
-        every sequence of every scan arrived."""
-        if world == 1:
-            return
-        if peer is not None:
-            if not gathered["validated"]:
-                torch.cuda.synchronize()
-                dist.barrier()
-                if rank == 0:
-                    for k in range(len(scans)):
-                        peer.results(k)  # raises on an unwritten sequence
-                gathered["validated"] = True
-            return
-        from paper_1707_09683_b200.shard import gather_to_rank0
-        gi = gidx.to(comm_dev)
-        for k in range(len(scans)):
-            o = outs[(k, 0)]
-            gather_to_rank0(dist, o[0][:n_local].to(comm_dev), o[1][:n_local].to(comm_dev), gi,
-                            db.count, as_numpy=False, validate=not gathered["validated"])
-        gathered["validated"] = True
-
-    def to_rank0(raw_t, pass_t):
-        """Full-length numpy (raw, pass) on rank 0 from a local device pair."""
-        if world == 1:
-            return raw_t[:n_local].cpu().numpy(), pass_t[:n_local].cpu().numpy()
-        from paper_1707_09683_b200.shard import gather_to_rank0
-        return gather_to_rank0(dist, raw_t[:n_local].to(comm_dev), pass_t[:n_local].to(comm_dev),
-                               gidx.to(comm_dev), db.count, as_numpy=True)
-
-    for _ in range(args.warmup):
-        step(0, False)
-        gather_results()
+    for j in range(args.warmup):
+        step(j, False)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -605,7 +681,6 @@ def main():
             ev0.record(stream)
             for j in range(args.steps):
                 launches += step(j, True)
-                gather_results()
             ev1.record(stream)
             torch.cuda.synchronize()
             ms = ev0.elapsed_time(ev1)
@@ -617,7 +692,6 @@ def main():
                 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 ev0.record(stream)
                 launches += step(j, True)
-                gather_results()
                 ev1.record(stream)
                 torch.cuda.synchronize()
                 ms += ev0.elapsed_time(ev1)
@@ -625,28 +699,49 @@ def main():
             dist.barrier()
     clocks = clk.summary()
     ms_t = torch.tensor([ms], dtype=torch.float64, device=comm_dev)
-    cells_local = sum(dbstats["residues"] * m for m, _ in scans) * args.steps
-    cells_t = torch.tensor([float(cells_local)], dtype=torch.float64, device=comm_dev)
     if dist:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(cells_t, op=dist.ReduceOp.SUM)
     ms_max = float(ms_t.item())
-    total_cells = float(cells_t.item())
+    total_cells = float(residues_total) * sum(m for m, _ in scans) * args.steps
     gcups = total_cells / (ms_max * 1e-3) / 1e9
 
-    # the headline scans' outputs go to the parity check (every kept step)
+    # parity of the headline scans: every kept step on this rank's share, and
+    # (N>1) every rank's gathered block on rank 0 against the rank's CRC32
+    gather_check = None
+    last = (args.steps - 1) % keep
     for k, (m, a) in enumerate(scans):
         _, costs, lam, tau = profile_id(m, DEFAULT_Q)
-        if peer is not None:
-            torch.cuda.synchronize()
-            dist.barrier()
-            pair = peer.results(k) if rank == 0 else (None, None)
-            pairs = [pair]
-        else:
-            pairs = [to_rank0(*outs[(k, j)]) for j in range(min(keep, args.steps))]
         if verifier is not None:
-            for r_, p_ in pairs:
-                verifier.add((m, a, DEFAULT_Q), "headline", a, costs, DEFAULT_Q, lam, tau, r_, p_)
+            for j in range(min(keep, args.steps)):
+                verifier.add((m, a, DEFAULT_Q), "headline", a, costs, DEFAULT_Q, lam, tau,
+                             outs[(k, j)][0][:n_local].cpu().numpy(),
+                             outs[(k, j)][1][:n_local].cpu().numpy())
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
+        blocks, bad = 0, 0
+        for k in range(len(scans)):
+            o = outs[(k, last)]
+            mine = torch.tensor([zlib.crc32(o[0][:n_local].cpu().numpy().tobytes()),
+                                 zlib.crc32(o[1][:n_local].cpu().numpy().tobytes()),
+                                 first, n_local], dtype=torch.int64, device=comm_dev)
+            allc = [torch.zeros_like(mine) for _ in range(world)]
+            dist.all_gather(allc, mine)
+            if hasattr(gatherer, "results"):
+                full = gatherer.results(k) if rank == 0 else None
+            else:
+                full = gatherer.gather(o[0][:n_local], o[1][:n_local])
+            if rank == 0:
+                fr, fp = full
+                for c in allc:
+                    cr, cp, f0, n0 = (int(x) for x in c.tolist())
+                    blocks += 1
+                    bad += int(zlib.crc32(np.ascontiguousarray(fr[f0:f0 + n0]).tobytes()) != cr)
+                    bad += int(zlib.crc32(np.ascontiguousarray(fp[f0:f0 + n0]).astype(
+                        np.uint8).tobytes()) != cp)
+        gather_check = {"blocks": blocks, "mismatches": bad,
+                        "what": "CRC32 of each rank's raw and pass block as gathered on rank 0 "
+                                "equals the rank's own"}
     del outs
 
     # ---- end to end through the C ABI with host buffers --------------------
@@ -690,20 +785,20 @@ def main():
         h2d = dbstats["packed_bytes"] + 16 * dbstats["tiles"] * 32
         e2e = {"value": round(total_cells / (float(ems.item()) * 1e-3) / 1e9, 3), "unit": "GCUPS",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "path": "C ABI: lhmm_scan_streamed (H2D of the packed pinned database in up "
-                        "to 64 pieces overlapped with the largest model's scan, one kernel launch "
-                        "waiting per piece on stream-written flags) + lhmm_scan per further "
-                        "model, results D2H into page-locked host buffers reused across steps"}
+               "path": "C ABI per rank: lhmm_scan_streamed (H2D of the packed pinned database in "
+                        "up to 64 pieces overlapped with the largest model's scan, one kernel "
+                        "launch waiting per piece on stream-written flags) + lhmm_scan per "
+                        "further model, results D2H into page-locked host buffers reused across "
+                        "steps"}
         if verifier is not None:
             # the e2e results of the last step, checked like the device ones
             for k, (m, a) in enumerate(e2e_order):
-                if world == 1:
-                    _, costs, lam, tau = profile_id(m, DEFAULT_Q)
-                    verifier.add((m, a, DEFAULT_Q), "e2e", a, costs, DEFAULT_Q, lam, tau,
-                                 host_out[k][0][:n_local], host_out[k][1][:n_local])
+                _, costs, lam, tau = profile_id(m, DEFAULT_Q)
+                verifier.add((m, a, DEFAULT_Q), "e2e", a, costs, DEFAULT_Q, lam, tau,
+                             host_out[k][0][:n_local], host_out[k][1][:n_local])
 
     # ---- sweep leg (C5, C3): per (M, alg, params), device-timed ------------
-    sweep = None
+    sweep, sweep_clocks = None, None
     if sweep_on and not args.db_budget:
         sweep = []
         sw_scans = [(m, "msv", DEFAULT_Q) for m in SWEEP_M] + \
@@ -721,12 +816,11 @@ def main():
                 torch.cuda.synchronize()
                 if dist:
                     dist.barrier()
-                times, sts = [], []
+                times = []
                 for j in range(nst):
                     st = s.scan_device(opt_for(a), sw_out[j][0].data_ptr(),
                                        sw_out[j][1].data_ptr())
                     times.append(st["device_ms"])
-                    sts.append(st)
                 tt = torch.tensor([sum(times) / nst, float(st["saturated"]),
                                    float(st["mode_rows"]), float(st["lazy_rows"])],
                                   dtype=torch.float64, device=comm_dev)
@@ -735,33 +829,35 @@ def main():
                     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
                     dist.all_reduce(tt, op=dist.ReduceOp.SUM)
                 t_ms = float(mx[0])
-                g = db.total_residues() * m / (t_ms * 1e-3) / 1e9
+                g = residues_total * m / (t_ms * 1e-3) / 1e9
                 e = {"alg": a, "M": m, "params": "default" if q == DEFAULT_Q else "nonsat",
                      "quant": qstr(q), "ms": round(t_ms, 4), "gcups": round(g, 1),
                      "frac": round(g / (peak_gcups * world), 4),
                      "lanes": st["lanes"], "rows": st["rows"], "variant": VARIANTS[st["variant"]],
                      "rescored_exactly": st["recomputed"]}
                 if a == "msv":
-                    e["saturated_frac"] = round(float(tt[1]) / db.count, 4)
+                    e["saturated_frac"] = round(float(tt[1]) / n_total, 4)
                     if float(tt[2]) > 0:
                         e["lazy_row_frac"] = round(float(tt[3]) / float(tt[2]), 4)
                 sweep.append(e)
-                for j in range(nst):
-                    r_, p_ = to_rank0(*sw_out[j])
-                    if verifier is not None:
-                        verifier.add((m, a, q), "sweep", a, costs, q, lam, tau, r_, p_)
+                if verifier is not None:
+                    for j in range(nst):
+                        verifier.add((m, a, q), "sweep", a, costs, q, lam, tau,
+                                     sw_out[j][0][:n_local].cpu().numpy(),
+                                     sw_out[j][1][:n_local].cpu().numpy())
         sweep_clocks = clk_sw.summary()
         del sw_out
 
     # ---- C1 leg (configs[0]): small database, many steps, L2 flushed --------
+    # (one GPU holds it: rank 0 runs it)
     c1 = None
-    if "c1" in legs and not args.db_budget and args.workload != "c1":
-        c1desc, _, c1m, c1n, c1gen = WORKLOADS["c1"]
-        cres, coff, cprofs = make_inputs(api, c1gen, c1n, c1m)
+    if "c1" in legs and not args.db_budget and args.workload != "c1" and rank == 0:
+        c1desc, _, c1m, _, _ = WORKLOADS["c1"]
+        cres, coff, _, cprofs = make_inputs(api, "c1", "strong", 1, [0], c1m)
         cdb = P.SequenceDB(cres, coff)
         s1 = P.Scanner(local)
         s1.set_stream(stream.cuda_stream)
-        s1.set_database(cdb)   # C1 fits one GPU: every rank scans it whole
+        s1.set_database(cdb)
         sc, lam, tau = cprofs[c1m[0]]
         c1 = {"workload": c1desc, "sequences": int(cdb.count), "residues": cdb.total_residues(),
               "l2": "L2 flushed before every timed scan (256 MB write outside the timed "
@@ -770,6 +866,7 @@ def main():
         keep1 = min(nst, 50)
         o1 = [(torch.empty(cdb.count, dtype=torch.uint8, device="cuda"),
                torch.empty(cdb.count, dtype=torch.uint8, device="cuda")) for _ in range(keep1)]
+        c1_verifiers = []
         with ClockSampler(local) as clk1:
             for q in (DEFAULT_Q, NONSAT_Q):
                 costs = api.quantize(sc, q)
@@ -796,11 +893,11 @@ def main():
                     e["lazy_row_frac"] = round(st["lazy_rows"] / st["mode_rows"], 4)
                 c1["scans"].append(e)
                 if verifier is not None:
-                    v1 = Verifier(cres, coff, cdb.count)  # C1 in full
+                    v1 = Verifier(cres, coff, cdb.count, host_threads)  # C1 in full
                     for j in range(keep1):
                         v1.add(("c1", q), "c1", "msv", costs, q, lam, tau,
                                o1[j][0].cpu().numpy(), o1[j][1].cpu().numpy())
-                    c1.setdefault("_verifiers", []).append(v1)
+                    c1_verifiers.append(v1)
         c1["clocks"] = clk1.summary()
         s1.close()
 
@@ -808,16 +905,19 @@ def main():
     if verifier is not None:
         parity = verifier.run()
         if c1 is not None:
-            for v1 in c1.pop("_verifiers", []):
-                p1 = v1.run()
-                parity["checked"] += p1["checked"]
-                parity["mismatches"] += p1["mismatches"]
-                parity["scans"] += p1["scans"]
-                parity["legs"]["c1"] = {k: parity["legs"].get("c1", {}).get(k, 0) + p1["legs"]["c1"][k]
-                                        for k in ("scans", "checked", "mismatches")}
-                parity["seconds"] = round(parity["seconds"] + p1["seconds"], 2)
-    elif c1 is not None:
-        c1.pop("_verifiers", None)
+            for v1 in c1_verifiers:
+                parity = merge_parity(parity, v1.run())
+        if dist:
+            cnt = torch.tensor([float(parity["checked"]), float(parity["mismatches"]),
+                                float(parity["scans"])], dtype=torch.float64, device=comm_dev)
+            dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+            parity.update({"checked": int(cnt[0]), "mismatches": int(cnt[1]),
+                           "scans": int(cnt[2]), "ranks": world,
+                           "legs_rank0": parity.pop("legs")})
+        parity["what"] = ("raw byte + pass bit of a fixed-stride sample of every timed scan "
+                          "(C1: every sequence), per rank share")
+        if gather_check is not None:
+            parity["gather"] = gather_check
 
     if rank != 0:
         if dist:
@@ -870,7 +970,8 @@ def main():
                          "lanes": g["lanes"], "rows": g["rows"], "variant": VARIANTS[g["variant"]],
                          "grid": g["grid"], "smem_bytes": g["smem_bytes"],
                          "rescored_exactly": g["recomputed"]})
-    cfg = workload_config(args.workload, desc, models_m, algs, db.count, db.total_residues(), world)
+    cfg = workload_config(args.workload, args.scaling, desc, models_m, algs, n_total,
+                          residues_total, world)
     if world > 1:
         cfg["gather"] = gather_mode
     if args.db_budget:
@@ -879,7 +980,7 @@ def main():
     line = {
         "metric": METRIC, "value": round(gcups, 2), "unit": "GCUPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8",
         "data": "synthetic", "config": cfg, "e2e": e2e,
         "gpu_launches": launches * world,
         "roofline": {"bound": "int_simd", "achieved": round(achieved, 1),
@@ -904,14 +1005,14 @@ def main():
         "scans": per_scan,
         "setup": {"generate_s": round(t_gen, 2), "pack_upload_s": round(t_pack, 2),
                   "packed_bytes": dbstats["packed_bytes"], "padded_cells": dbstats["padded_cells"],
-                  "tiles": dbstats["tiles"]},
+                  "tiles": dbstats["tiles"], "sequences_rank0": int(n_local)},
     }
     if sweep is not None:
         c3 = next((e for e in sweep if e["alg"] == "msv" and e["M"] == 2405
                    and e["params"] == "default"), None)
         line["sweep"] = {"what": "C5: device-timed GCUPS per (M, alg, params) over the same "
-                                 "1M-sequence database, mean of --sweep-steps scans; frac = of "
-                                 f"the {peak_gcups * world / 1e3:.1f} TCUPS packed-integer "
+                                 "database, mean of --sweep-steps scans (max over ranks); frac = "
+                                 f"of the {peak_gcups * world / 1e3:.1f} TCUPS packed-integer "
                                  "roofline; lazy_row_frac = share of warp rows run by the "
                                  "two-mode MSV kernel's lazy (saturated) body",
                          "steps": max(1, args.sweep_steps), "clocks": sweep_clocks,

@@ -240,6 +240,22 @@ int lhmm_peer_buffers_release(lhmm_context* ctx);
 int lhmm_device_fill(lhmm_context* ctx, void* dptr, uint8_t value, uint64_t bytes);
 int lhmm_device_to_host(lhmm_context* ctx, const void* dptr, void* host, uint64_t bytes);
 
+/* ---- block gather (multi-GPU) ---------------------------------
+ * The bulk alternative to the per-sequence peer stores above: each rank scans
+ * into LOCAL device buffers (lhmm_scan_device), then copies its contiguous
+ * block of results (raw, pass: local_sequences bytes each) into rank 0's
+ * staging buffer at the rank's offset (the prefix sum of the shards' sizes) --
+ * one NVLink bulk copy per rank and scan instead of one remote byte store per
+ * sequence.  Rank 0 then puts staging order into global order with one
+ * scatter, dst[index[k]] = src[k] (skipped when the shards are contiguous
+ * ranges of the global order).  All calls are asynchronous on ctx's stream;
+ * lhmm_context_synchronize waits for them. */
+int lhmm_device_copy(lhmm_context* ctx, void* dst, const void* src, uint64_t bytes);
+int lhmm_scatter_results(lhmm_context* ctx, uint8_t* d_raw_dst, uint8_t* d_pass_dst,
+                         const uint8_t* d_raw_src, const uint8_t* d_pass_src,
+                         const uint64_t* d_index, uint64_t n);
+int lhmm_context_synchronize(lhmm_context* ctx);
+
 /* End-to-end scan from the packed HOST image: the database bytes are copied
  * host->device in `segments` byte-balanced pieces on a copy stream while each
  * piece is scanned as soon as it lands (H2D overlapped with the kernels);

@@ -92,6 +92,9 @@ SIGNATURES = {
     "lhmm_peer_buffers_release": (C.c_int, [vp]),
     "lhmm_device_fill": (C.c_int, [vp, vp, C.c_uint8, C.c_uint64]),
     "lhmm_device_to_host": (C.c_int, [vp, vp, vp, C.c_uint64]),
+    "lhmm_device_copy": (C.c_int, [vp, vp, vp, C.c_uint64]),
+    "lhmm_scatter_results": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_uint64]),
+    "lhmm_context_synchronize": (C.c_int, [vp]),
     "lhmm_scan_streamed": (C.c_int, [vp, C.POINTER(ScanOptionsC), C.c_int, u8p, u8p,
                                      C.POINTER(ScanStatsC)]),
     "lhmm_filter_pipeline": (C.c_int, [vp, C.c_double, C.c_int, u8p, u8p, u8p, u64p,

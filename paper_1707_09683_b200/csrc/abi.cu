@@ -1084,9 +1084,15 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
                 pf.flag_gen = c->db_gen;
             }
         }
-        CUDA_TRY(cudaEventRecord(c->evr1, c->stream));
-        CUDA_TRY(cudaEventSynchronize(c->evr1));
-        CUDA_TRY(cudaEventElapsedTime(&ms, c->evr0, c->evr1));
+        if (nflag) {
+            // the span of the relaxed kernel, the flag read, the compaction
+            // and the exact rescoring; with no flagged sequence the scan is
+            // the relaxed kernel alone (ev0..ev1 above) -- recording evr1
+            // after the host's flag read would add that round trip
+            CUDA_TRY(cudaEventRecord(c->evr1, c->stream));
+            CUDA_TRY(cudaEventSynchronize(c->evr1));
+            CUDA_TRY(cudaEventElapsedTime(&ms, c->evr0, c->evr1));
+        }
     }
     if (st) {
         std::memset(st, 0, sizeof(*st));
@@ -1332,6 +1338,19 @@ int run_pipeline(lhmm_context* c, double threshold, int variant, uint8_t* ssv_ra
 }
 
 }  // namespace
+
+// Block gather, rank 0: staging order -> global order (grid-stride).
+static __global__ void scatter_results_kernel(uint8_t* __restrict__ raw_dst, uint8_t* __restrict__ pass_dst,
+                                       const uint8_t* __restrict__ raw_src,
+                                       const uint8_t* __restrict__ pass_src,
+                                       const uint64_t* __restrict__ index, uint64_t n) {
+    for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+         k += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t g = index[k];
+        raw_dst[g] = raw_src[k];
+        pass_dst[g] = pass_src[k];
+    }
+}
 
 // f16 subnormal self-check.  The FP16XM / FP16XH forms keep byte scores as
 // f16 subnormals (a bit pattern IS its value in units of 2^-24), so they are
@@ -1722,6 +1741,36 @@ int lhmm_device_to_host(lhmm_context* c, const void* dptr, void* host, uint64_t 
     if (!c || ((!dptr || !host) && bytes)) return set_error(LHMM_ERR_CONTRACT, "null argument");
     DeviceGuard g(c->device);
     CUDA_TRY(cudaMemcpyAsync(host, dptr, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return LHMM_OK;
+}
+
+int lhmm_device_copy(lhmm_context* c, void* dst, const void* src, uint64_t bytes) {
+    if (!c || ((!dst || !src) && bytes)) return set_error(LHMM_ERR_CONTRACT, "null argument");
+    if (!bytes) return LHMM_OK;
+    DeviceGuard g(c->device);
+    // unified addressing: local, peer (NVLink) or IPC-mapped pointers alike
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
+    return LHMM_OK;
+}
+
+int lhmm_scatter_results(lhmm_context* c, uint8_t* d_raw_dst, uint8_t* d_pass_dst,
+                         const uint8_t* d_raw_src, const uint8_t* d_pass_src,
+                         const uint64_t* d_index, uint64_t n) {
+    if (!c || ((!d_raw_dst || !d_pass_dst || !d_raw_src || !d_pass_src || !d_index) && n))
+        return set_error(LHMM_ERR_CONTRACT, "null argument");
+    if (!n) return LHMM_OK;
+    DeviceGuard g(c->device);
+    const uint64_t blocks = (n + 255) / 256;
+    scatter_results_kernel<<<unsigned(std::min<uint64_t>(blocks, 1u << 20)), 256, 0, c->stream>>>(
+        d_raw_dst, d_pass_dst, d_raw_src, d_pass_src, d_index, n);
+    CUDA_TRY(cudaPeekAtLastError());
+    return LHMM_OK;
+}
+
+int lhmm_context_synchronize(lhmm_context* c) {
+    if (!c) return set_error(LHMM_ERR_CONTRACT, "null context");
+    DeviceGuard g(c->device);
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     return LHMM_OK;
 }

@@ -449,6 +449,21 @@ class Scanner:
                                                  out.ctypes.data_as(C.c_void_p), int(nbytes)))
         return out[:int(nbytes)]
 
+    def device_copy(self, dst_ptr, src_ptr, nbytes):
+        """Asynchronous device-to-device copy on the context's stream (local,
+        peer or IPC-mapped pointers): the block gather's bulk NVLink copy."""
+        _check(_native.lib().lhmm_device_copy(self._ctx, C.c_void_p(dst_ptr), C.c_void_p(src_ptr),
+                                              int(nbytes)))
+
+    def scatter_results(self, raw_dst, pass_dst, raw_src, pass_src, index_ptr, n):
+        """dst[index[k]] = src[k] for k < n (device pointers; index u64)."""
+        _check(_native.lib().lhmm_scatter_results(
+            self._ctx, C.c_void_p(raw_dst), C.c_void_p(pass_dst), C.c_void_p(raw_src),
+            C.c_void_p(pass_src), C.c_void_p(index_ptr), int(n)))
+
+    def synchronize(self):
+        _check(_native.lib().lhmm_context_synchronize(self._ctx))
+
     def scan_device(self, opt: ScanOptions, raw_ptr: int, pass_ptr: int):
         """Outputs stay on the device (e.g. torch.uint8 tensors' data_ptr())."""
         st = _native.ScanStatsC()

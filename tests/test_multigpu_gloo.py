@@ -62,3 +62,51 @@ def test_shard_and_gather_to_rank0(tmp_path, world):
     res = tmp_path / "result.txt"
     mp.spawn(_worker, args=(world, _free_port(), str(res)), nprocs=world, join=True)
     assert res.read_text() == "ok"
+
+
+def _worker_nccl_gather(rank, world, port, result_path):
+    """NcclGather: indices exchanged once, then 2 bytes per sequence per
+    gather; contiguous chunk shares (shard.chunk_plan) and LPT shares."""
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    import paper_1707_09683_b200 as P
+    from paper_1707_09683_b200.shard import NcclGather, chunk_plan, shard_plan
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = P.Rng(77)
+        hmm = rng.random_profile(90)
+        db = rng.lognormal_records(1200, 150, 0.6, 2)
+        q = oracle.QuantParams()
+        ora = oracle.Oracle()
+        costs = ora.quantize(hmm.match_scores.reshape(-1), q)
+        full = ora.scan_flat(1, costs, db.residues, db.offsets, q, 1)
+        ok = True
+        # contiguous shares: 12 chunks of 100 sequences
+        mine = chunk_plan(12, rank, world)
+        idx_c = np.arange(mine.start * 100, mine.stop * 100, dtype=np.int64)
+        for idx in (idx_c, shard_plan(db.offsets, rank, world).astype(np.int64)):
+            g = NcclGather(dist, idx, db.count)
+            for salt in range(3):  # the same gatherer, several scans
+                raw = torch.from_numpy(full[idx] ^ np.uint8(salt))
+                ps = torch.from_numpy((full[idx] & 1).astype(np.uint8))
+                out_raw, out_pass = g.gather(raw, ps)
+                if rank == 0:
+                    ok = ok and np.array_equal(out_raw, full ^ np.uint8(salt))
+                    ok = ok and np.array_equal(out_pass, (full & 1).astype(bool))
+        if rank == 0:
+            with open(result_path, "w") as f:
+                f.write("ok" if ok else "mismatch")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_nccl_gather_two_bytes_per_sequence(tmp_path, world):
+    res = tmp_path / "result.txt"
+    mp.spawn(_worker_nccl_gather, args=(world, _free_port(), str(res)), nprocs=world, join=True)
+    assert res.read_text() == "ok"
