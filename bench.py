@@ -92,7 +92,8 @@ WORKLOADS = {
               "both", SWEEP_M, 1_000_000, SWISSPROT),
 }
 C4_STRONG_TOTAL = 50_000_000
-VARIANTS = ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm", "fp16xh", "fp16xr"]
+VARIANTS = ["auto", "dpx16", "fp16", "swar8", "fp16x", "fp16xalt", "fp16xm", "fp16xh", "fp16xr",
+            "fp16xrm"]
 
 
 def log(*a):
@@ -552,7 +553,8 @@ def main():  # noqa: C901
     variant = getattr(P.Variant, {"auto": "Auto", "dpx16": "Dpx16", "fp16": "Fp16",
                                   "swar8": "Swar8", "fp16x": "Fp16x", "fp16xalt": "Fp16xAlt",
                                   "fp16xm": "Fp16xMixed", "fp16xh": "Fp16xHybrid",
-                                  "fp16xr": "Fp16xRelaxed"}[args.variant])
+                                  "fp16xr": "Fp16xRelaxed",
+                                  "fp16xrm": "Fp16xRelaxedFixedB"}[args.variant])
     algs = algs_of(wl_alg)
     api = ProductGen(P)
     # the sweep leg shares the Swiss-Prot-like database of C2/C3

@@ -82,10 +82,15 @@ enum lhmm_variant {
     LHMM_VARIANT_FP16XH = 7, /* MSV: two-mode hybrid -- the FP16X exact mode on a 16-bit
                                table and the FP16XM lazy mode on a mixed table, both in
                                shared memory; SSV: same as FP16XM */
-    LHMM_VARIANT_FP16XR = 8 /* MSV: relaxed -- no 255 cap, f16 subnormal domain, one
+    LHMM_VARIANT_FP16XR = 8, /* MSV: relaxed -- no 255 cap, f16 subnormal domain, one
                                HADD2.SAT + one max per cell pair; sequences whose relaxed
                                score reaches 256-dbias are rescored exactly (the auto
                                policy uses it for non-saturating profiles); SSV: FP16X */
+    LHMM_VARIANT_FP16XRM = 9 /* MSV: relaxed with B fixed at base(len) -- the relaxed SSV
+                               step on u = max(v,B) - B with the FP16XM mixed table; every
+                               sequence whose result cannot certify "B never moved, no cap,
+                               E > base" is rescored exactly (the auto policy's first
+                               choice for non-saturating profiles); SSV: FP16XM */
 };
 
 /* Byte-space constants; mirror of lanehmm::QuantParams

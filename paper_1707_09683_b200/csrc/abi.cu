@@ -112,6 +112,9 @@ const int* rows_list(int variant, int* n) {
     case LHMM_VARIANT_FP16XR:
         *n = int(sizeof(lhmm::kRows_fp16xr) / sizeof(int));
         return lhmm::kRows_fp16xr;
+    case LHMM_VARIANT_FP16XRM:
+        *n = int(sizeof(lhmm::kRows_fp16xrm) / sizeof(int));
+        return lhmm::kRows_fp16xrm;
     default:
         *n = int(sizeof(lhmm::kRows_swar8) / sizeof(int));
         return lhmm::kRows_swar8;
@@ -222,6 +225,8 @@ double model_rate(int variant, int alg, uint32_t L, uint32_t H) {
         w = alg == LHMM_MSV ? 4.5 : 3.0;
     else if (variant == LHMM_VARIANT_FP16XR)
         w = 3.5;
+    else if (variant == LHMM_VARIANT_FP16XRM)
+        w = 3.0;
     else
         w = alg == LHMM_MSV ? 4.5 : 3.5;
     const double lg = std::log2(double(L));
@@ -249,20 +254,21 @@ struct Choice {
 // (MSV, scores known not to saturate): the relaxed FP16XR kernel rescored few
 // sequences (or has not run yet on this database).
 Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64_t n_tiles,
-                       int sm_count, bool two_mode_ok = true, bool relaxed_msv_ok = false) {
+                       int sm_count, bool two_mode_ok = true, bool relaxed_msv_ok = false,
+                       bool fixb_msv_ok = false) {
     Choice best;
     // auto considers the measured variants only (calib_b200.inc); the
     // relaxed FP16X also needs a database large enough to amortise its
     // rescoring check.  Without any measurement the cost model decides.
     // FP16X stands for both of its code forms (FP16X, FP16X_ALT): the
     // measured table picks the faster one per geometry
-    const int vs_auto[7] = {LHMM_VARIANT_FP16, LHMM_VARIANT_DPX16, LHMM_VARIANT_FP16X,
+    const int vs_auto[8] = {LHMM_VARIANT_FP16, LHMM_VARIANT_DPX16, LHMM_VARIANT_FP16X,
                             LHMM_VARIANT_FP16X_ALT, LHMM_VARIANT_FP16XM, LHMM_VARIANT_FP16XH,
-                            LHMM_VARIANT_FP16XR};
+                            LHMM_VARIANT_FP16XR, LHMM_VARIANT_FP16XRM};
     const int vs_x[4] = {LHMM_VARIANT_FP16X, LHMM_VARIANT_FP16X_ALT, LHMM_VARIANT_FP16XM,
                          LHMM_VARIANT_FP16XH};
     const int* vs = variant == LHMM_VARIANT_AUTO ? vs_auto : vs_x;
-    const int nv = variant == LHMM_VARIANT_AUTO ? 7 : (variant == LHMM_VARIANT_FP16X ? 4 : 1);
+    const int nv = variant == LHMM_VARIANT_AUTO ? 8 : (variant == LHMM_VARIANT_FP16X ? 4 : 1);
     for (int pass = 0; pass < 2 && best.L == 0; ++pass) {
         const bool measured_only = variant == LHMM_VARIANT_AUTO && pass == 0;
         for (int vi = 0; vi < nv; ++vi) {
@@ -285,6 +291,9 @@ Choice choose_geometry(uint32_t m, int alg, int variant, uint32_t want_L, uint64
             // flag read + compaction + exact rescoring doubled the scan)
             if (variant == LHMM_VARIANT_AUTO && v == LHMM_VARIANT_FP16XR &&
                 (two_mode_ok || !relaxed_msv_ok || (n_tiles > 0 && n_tiles < 4096)))
+                continue;
+            if (variant == LHMM_VARIANT_AUTO && v == LHMM_VARIANT_FP16XRM &&
+                (two_mode_ok || !fixb_msv_ok || (n_tiles > 0 && n_tiles < 4096)))
                 continue;
             const uint32_t cpw = lhmm::cells_per_word(v);
             int n;
@@ -362,6 +371,9 @@ struct ProfileSlot {
     // MSV: fraction the relaxed FP16XR kernel had to rescore
     double msv_flag_frac = -1.0;
     uint64_t msv_flag_gen = 0;
+    // MSV: fraction the fixed-B relaxed FP16XRM kernel had to rescore
+    double fixb_flag_frac = -1.0;
+    uint64_t fixb_flag_gen = 0;
     void release() {
         for (auto& kv : tables) kv.second.buf.release();
         for (auto& kv : lens) {
@@ -630,7 +642,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
     if (opt->alg != LHMM_MSV && opt->alg != LHMM_SSV)
         return set_error(LHMM_ERR_CONTRACT, "unknown algorithm");
-    if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_FP16XR)
+    if (opt->variant < LHMM_VARIANT_AUTO || opt->variant > LHMM_VARIANT_FP16XRM)
         return set_error(LHMM_ERR_CONTRACT, "unknown kernel variant");
     if (opt->reorder_mode != 0 && opt->reorder_mode != 1)
         return set_error(LHMM_ERR_CONTRACT, "unknown reorder mode");
@@ -644,6 +656,8 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         variant = LHMM_VARIANT_FP16XM;  // the hybrid is an MSV form
     if (variant == LHMM_VARIANT_FP16XR && opt->alg == LHMM_SSV)
         variant = LHMM_VARIANT_FP16X;   // relaxed SSV is FP16X
+    if (variant == LHMM_VARIANT_FP16XRM && opt->alg == LHMM_SSV)
+        variant = LHMM_VARIANT_FP16XM;  // its SSV twin
 
     uint32_t L = opt->lanes, H = opt->rows;
     if (L != 0 && (L > 32 * kMaxLongK || (L & (L - 1))))
@@ -673,16 +687,21 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         const bool relaxed_msv_ok =
             opt->alg == LHMM_MSV &&
             !(view == nullptr && pf.msv_flag_gen == c->db_gen && pf.msv_flag_frac > 0.05);
+        // ... and first the fixed-B form, whose u domain needs dbias <= 127
+        const bool fixb_msv_ok =
+            opt->alg == LHMM_MSV && pf.q.dbias <= 127 &&
+            !(view == nullptr && pf.fixb_flag_gen == c->db_gen && pf.fixb_flag_frac > 0.05);
         const auto ckey =
             std::make_tuple(pf.m, opt->alg, variant, L,
                             v.n_tiles + (two_mode_ok ? 0 : (1ull << 62)) +
-                                (relaxed_msv_ok ? 0 : (1ull << 61)));
+                                (relaxed_msv_ok ? 0 : (1ull << 61)) +
+                                (fixb_msv_ok ? 0 : (1ull << 60)));
         const auto cit = c->choices.find(ckey);
         if (cit != c->choices.end()) {
             std::tie(ch.variant, ch.L, ch.H) = cit->second;
         } else {
             ch = choose_geometry(pf.m, opt->alg, variant, L, v.n_tiles, c->sm_count, two_mode_ok,
-                                 relaxed_msv_ok);
+                                 relaxed_msv_ok, fixb_msv_ok);
             if (c->choices.size() > 256) c->choices.clear();
             c->choices.emplace(ckey, std::make_tuple(ch.variant, ch.L, ch.H));
         }
@@ -807,7 +826,8 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     p.wrap = opt->reorder_mode == 1 ? 1u : 0u;
     const bool relaxed = ((variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16XM) &&
                           opt->alg == LHMM_SSV) ||
-                         (variant == LHMM_VARIANT_FP16XR && opt->alg == LHMM_MSV);
+                         ((variant == LHMM_VARIANT_FP16XR || variant == LHMM_VARIANT_FP16XRM) &&
+                          opt->alg == LHMM_MSV);
     if (relaxed) {
         if (int rc = c->d_flag.reserve(
                 std::max<uint64_t>(global_out ? c->n_global : c->db.n_local, 1)))
@@ -1068,10 +1088,23 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
                 return rc;
             }
             if (nsel) {
+                // the exact twin at the same geometry where one exists (the
+                // paper-wrap study mode is capacity-dependent): FP16XR ->
+                // two-mode FP16X, FP16XRM -> two-mode FP16XM (MSV), FP16X
+                // SSV -> FP16; else FP16 at its own geometry
                 lhmm_scan_options ox = *opt;
                 ox.variant = LHMM_VARIANT_FP16;
                 ox.lanes = 0;
                 ox.rows = 0;
+                const int twin = variant == LHMM_VARIANT_FP16XR    ? LHMM_VARIANT_FP16X
+                                 : variant == LHMM_VARIANT_FP16XRM ? LHMM_VARIANT_FP16XM
+                                 : variant == LHMM_VARIANT_FP16X   ? LHMM_VARIANT_FP16
+                                                                   : -1;
+                if (twin >= 0 && rows_instantiated(twin, H)) {
+                    ox.variant = twin;
+                    ox.lanes = L;
+                    ox.rows = H;
+                }
                 lhmm_scan_stats sx;
                 if (int rc = do_scan(c, &ox, d_raw, d_pass, &sx, 0, &sub)) return rc;
                 launches += sx.launches;
@@ -1079,7 +1112,10 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             recomputed = nsel;
         }
         if (view == nullptr && v.sequences > 0) {
-            if (opt->alg == LHMM_MSV) {
+            if (variant == LHMM_VARIANT_FP16XRM) {
+                pf.fixb_flag_frac = double(nflag) / double(v.sequences);
+                pf.fixb_flag_gen = c->db_gen;
+            } else if (opt->alg == LHMM_MSV) {
                 pf.msv_flag_frac = double(nflag) / double(v.sequences);
                 pf.msv_flag_gen = c->db_gen;
             } else {
@@ -1581,6 +1617,8 @@ static int fill_profile(ProfileSlot& pf, const uint8_t* costs, uint32_t m, const
     pf.flag_gen = 0;
     pf.msv_flag_frac = -1.0;
     pf.msv_flag_gen = 0;
+    pf.fixb_flag_frac = -1.0;
+    pf.fixb_flag_gen = 0;
     return LHMM_OK;
 }
 

@@ -283,7 +283,8 @@ static void strides_for(uint32_t L, uint32_t H, uint32_t& P, uint32_t& copies,
 // Table rows ("register rows" of the 16-byte-per-lane slots): the mixed
 // SSV table packs five rows per slot (lhmm_kernel.cuh Fp16Mixed).
 static uint32_t slot_rows(int variant, uint32_t H) {
-    return variant == LHMM_VARIANT_FP16XM ? (H + 4u) / 5u * 4u : H;
+    return variant == LHMM_VARIANT_FP16XM || variant == LHMM_VARIANT_FP16XRM ? (H + 4u) / 5u * 4u
+                                                                             : H;
 }
 
 uint64_t table_bytes_for(int variant, uint32_t L, uint32_t H, bool replicate) {
@@ -333,6 +334,12 @@ static uint32_t encode_word(int variant, int alg, const uint8_t* c, uint32_t cpw
 
 void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_t L, uint32_t H,
                  bool replicate, uint32_t dbias, TableImage& out) {
+    if (variant == LHMM_VARIANT_FP16XRM) {
+        // fixed-B relaxed MSV runs the relaxed SSV step in its u domain: the
+        // FP16XM SSV table (dbias - cost), unchanged
+        build_table(costs, m, LHMM_VARIANT_FP16XM, LHMM_SSV, L, H, replicate, dbias, out);
+        return;
+    }
     if (variant == LHMM_VARIANT_FP16XH) {
         // hybrid two-mode MSV: the FP16X image (exact rows) followed by the
         // FP16XM image (lazy rows)

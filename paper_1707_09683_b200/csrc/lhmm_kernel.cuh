@@ -553,6 +553,86 @@ struct Fp16RelaxedMsv {
     }
 };
 
+// FP16XRM, MSV ("relaxed, fixed B, mixed table"): the fastest exact route
+// for profiles whose MSV scores neither saturate nor move B.  While B stays
+// at base(len) -- B = max(base, E (-) (tec+tjb)) changes only once E exceeds
+// base + tec + tjb -- the cells can hold u = max(v, B) - B, and one MSV step
+// max(max(v, B) + dbias - cost, 0), kept as max(., B) - B, is
+//     u' = max(u + dbias - cost, 0)
+// -- the relaxed SSV step (Fp16Mixed, v - 128 there) verbatim: the same
+// subnormal-domain mixed table (three f16 words HADD2.SAT on the FP16 pipe,
+// two signed-byte words PRMT + VIADDMNMX on the ALU, 1.6 table bytes per
+// cell), no per-row reduction, no B update; raw = E_u + base.  A sequence is
+// flagged and rescored by the exact FP16 kernel unless its result certifies
+// every assumption: E_u <= tec + tjb (B never moved), E_u + base < 256 -
+// dbias (no cap event: as for FP16XR), E_u <= 127 (the byte words' cost
+// clamp at -128 never bit: u <= 127 + 128 - ... see Fp16Mixed) and E_u > 0
+// (some cell exceeded base, so E = E_u + base; if none did, E <= base is not
+// recoverable from u).  At QuantParams{3,120,3,20,20} on the 1M Swiss-Prot-like
+// set 0.01-0.15% of sequences are flagged (M = 48..2405).
+template <int ALG>
+struct Fp16FixedBMixed {
+    static_assert(ALG == 0, "the fixed-B relaxed form (FP16XRM) is MSV only");
+    static constexpr int CPW = 2;
+    static constexpr int kGroup = 5;
+    static constexpr bool kMsv = false;     // row structure: no per-row reduction
+    static constexpr bool kMsvAlg = true;   // MSV scores (saturation feedback)
+    static constexpr bool kRelaxed = true;
+    static constexpr bool kTwoMode = false;
+    static constexpr int kFpEvery = 0;
+    static constexpr uint32_t NEG = 0u;
+    struct St {
+        uint32_t base, tjb, capu;
+    };
+    __device__ static __forceinline__ void init(St& s, uint32_t base, const KParams& p) {
+        s.base = base;
+        s.tjb = p.tecjb;
+        const int capu = int(256u - p.dbias) - int(base);  // E_u + base < 256 - dbias
+        s.capu = uint32_t(capu > 0 ? capu : 0);
+    }
+    __device__ static __forceinline__ uint32_t init_word(const St&) { return 0u; }
+    template <bool LAZY = false>
+    __device__ static __forceinline__ uint32_t inject(const St&) { return 0u; }
+    template <bool LAZY = false, bool FPW = false, int FORM = 0>
+    __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St&) {
+        if constexpr (FORM == 3) {
+            return __viaddmax_s16x2(x, c, 0u);
+        } else {
+            return as_u32(__hadd2_sat(as_h2(x), as_h2(c)));
+        }
+    }
+    __device__ static __forceinline__ uint32_t unpack(uint32_t w, int which) {
+        uint32_t r;
+        if (which == 0)
+            asm("prmt.b32 %0, %1, 0, 0x9180;" : "=r"(r) : "r"(w));
+        else
+            asm("prmt.b32 %0, %1, 0, 0xB3A2;" : "=r"(r) : "r"(w));
+        return r;
+    }
+    __device__ static __forceinline__ uint32_t acc2(uint32_t E, uint32_t a, uint32_t b) {
+        return __vimax3_u16x2(E, a, b);
+    }
+    __device__ static __forceinline__ uint32_t shift(uint32_t top, uint32_t up) {
+        return __byte_perm(top, up, 0x1076);
+    }
+    template <int L>
+    __device__ static __forceinline__ uint32_t group_reduce(uint32_t E) {
+        const uint32_t e = __vmaxu2(E, __byte_perm(E, E, 0x1032));
+        return group_max<L>(e);
+    }
+    __device__ static __forceinline__ void update_B(St&, uint32_t) {}
+    __device__ static __forceinline__ uint32_t raw(uint32_t e) { return e & 0xffffu; }
+    // raw score from E_u (the flag test below runs on E_u itself)
+    __device__ static __forceinline__ uint32_t raw_of(uint32_t e, const St& s) {
+        return (e & 0xffffu) + s.base;
+    }
+    __device__ static __forceinline__ bool needs_exact_u(uint32_t e, const St& s) {
+        const uint32_t eu = e & 0xffffu;
+        return eu == 0u || eu > s.tjb || eu >= s.capu || eu > 127u;
+    }
+    __device__ static __forceinline__ bool needs_exact(uint32_t, const St&) { return false; }
+};
+
 // FP16XM, MSV (two-mode like Fp16Sat, mixed table like Fp16Mixed).  The
 // cells live NEGATED in the f16 subnormal domain: pattern n = 255 - v (units
 // of 2^-24), so the byte cap v <= 255 is HADD2.SAT's clamp at +0, the floor
@@ -823,6 +903,25 @@ template <class V>
 struct is_hybrid<V, decltype(void(V::kHybrid))> {
     static constexpr bool value = V::kHybrid;
 };
+// Policies whose raw score needs per-sequence state (FP16XRM: E_u + base).
+template <class V, class = void>
+struct has_raw_of {
+    static constexpr bool value = false;
+};
+template <class V>
+struct has_raw_of<V, decltype(void(&V::raw_of))> {
+    static constexpr bool value = true;
+};
+// MSV scores (the saturation count), also for policies with an SSV-shaped row
+template <class V, class = void>
+struct msv_alg {
+    static constexpr bool value = V::kMsv;
+};
+template <class V>
+struct msv_alg<V, decltype(void(V::kMsvAlg))> {
+    static constexpr bool value = V::kMsvAlg;
+};
+
 template <class V, bool LAZY>
 __host__ __device__ constexpr int mode_group_width() {
     if constexpr (is_hybrid<V>::value) {
@@ -1264,18 +1363,25 @@ __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KPar
         }
         uint32_t E = V::acc2(V::acc2(e0, e1, e2), e3, e3);
         if constexpr (!V::kMsv) E = V::template group_reduce<L>(E);
-        uint32_t raw = V::raw(E);
+        uint32_t raw;
         bool exact_needed = false;
-        if constexpr (V::kRelaxed) {
-            exact_needed = V::needs_exact(raw, st);
+        if constexpr (has_raw_of<V>::value) {
+            raw = V::raw_of(E, st);
+            exact_needed = V::needs_exact_u(E, st);
             raw = raw > 255u ? 255u : raw;
+        } else {
+            raw = V::raw(E);
+            if constexpr (V::kRelaxed) {
+                exact_needed = V::needs_exact(raw, st);
+                raw = raw > 255u ? 255u : raw;
+            }
         }
         if (p.fault && grp == 0 && raw < 255u) raw += 1u;  // verification aid
         const uint32_t oi = p.out_idx[sidx];
         if (oig == 0 && oi != 0xffffffffu) {
             p.raw_out[oi] = uint8_t(raw);
             p.pass_out[oi] = uint8_t(raw == 255u || raw >= p.rawmin_tab[len]);
-            if (V::kMsv && p.sat_count && raw == 255u) atomicAdd(p.sat_count, 1u);
+            if (msv_alg<V>::value && p.sat_count && raw == 255u) atomicAdd(p.sat_count, 1u);
             if constexpr (V::kRelaxed) {
                 p.flag_out[oi] = exact_needed ? 1u : 0u;
                 if (exact_needed) atomicAdd(p.flag_count, 1u);

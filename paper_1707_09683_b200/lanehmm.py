@@ -75,6 +75,7 @@ class Variant(enum.IntEnum):
     Fp16xMixed = 6  # FP16X with a mixed 16-bit / byte table (1.6 B per cell)
     Fp16xHybrid = 7  # MSV: FP16X exact rows + FP16XM lazy rows (two tables)
     Fp16xRelaxed = 8  # MSV: no 255 cap (subnormal f16), flagged sequences rescored exactly
+    Fp16xRelaxedFixedB = 9  # MSV: relaxed with B fixed at base, FP16XM table, flags rescored
 
 
 @dataclass

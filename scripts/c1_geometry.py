@@ -24,6 +24,7 @@ torch.cuda.set_stream(torch.cuda.Stream())
 VMAP = {"dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16, "fp16x": P.Variant.Fp16x,
         "fp16xalt": P.Variant.Fp16xAlt, "fp16xm": P.Variant.Fp16xMixed,
         "fp16xh": P.Variant.Fp16xHybrid, "fp16xr": P.Variant.Fp16xRelaxed,
+        "fp16xrm": P.Variant.Fp16xRelaxedFixedB,
         "auto": P.Variant.Auto}
 
 

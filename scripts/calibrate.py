@@ -37,7 +37,7 @@ def main():
     vmap = {"dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16, "swar8": P.Variant.Swar8,
             "fp16x": P.Variant.Fp16x, "fp16xalt": P.Variant.Fp16xAlt,
             "fp16xm": P.Variant.Fp16xMixed, "fp16xh": P.Variant.Fp16xHybrid,
-            "fp16xr": P.Variant.Fp16xRelaxed}
+            "fp16xr": P.Variant.Fp16xRelaxed, "fp16xrm": P.Variant.Fp16xRelaxedFixedB}
     for vn in args.variants.split(","):
         cpw = 4 if vn == "swar8" else 2
         for L in lanes:

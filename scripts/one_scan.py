@@ -24,7 +24,8 @@ hmm = P.Rng(7000 + a.m).random_profile(a.m)
 q = P.QuantParams() if a.quant == "default" else P.QuantParams(3.0, 120, 3, 20, 20)
 var = {"auto": P.Variant.Auto, "fp16": P.Variant.Fp16, "fp16x": P.Variant.Fp16x,
        "fp16xm": P.Variant.Fp16xMixed, "fp16xh": P.Variant.Fp16xHybrid,
-       "fp16xr": P.Variant.Fp16xRelaxed, "dpx16": P.Variant.Dpx16}[a.variant]
+       "fp16xr": P.Variant.Fp16xRelaxed, "fp16xrm": P.Variant.Fp16xRelaxedFixedB,
+       "dpx16": P.Variant.Dpx16}[a.variant]
 with P.Scanner(0) as s:
     s.set_profile(P.quantize_emissions(hmm, q), q, hmm.lambda_, hmm.tau)
     s.set_database(db)

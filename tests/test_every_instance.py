@@ -26,7 +26,7 @@ import gen_instances as G  # noqa: E402
 VARIANT = {"dpx16": P.Variant.Dpx16, "fp16": P.Variant.Fp16, "swar8": P.Variant.Swar8,
            "fp16x": P.Variant.Fp16x, "fp16xalt": P.Variant.Fp16xAlt,
            "fp16xm": P.Variant.Fp16xMixed, "fp16xh": P.Variant.Fp16xHybrid,
-           "fp16xr": P.Variant.Fp16xRelaxed}
+           "fp16xr": P.Variant.Fp16xRelaxed, "fp16xrm": P.Variant.Fp16xRelaxedFixedB}
 QUANTS = [P.QuantParams(), P.QuantParams(3.0, 120, 3, 20, 20), P.QuantParams(2.0, 240, 10, 1, 5),
           P.QuantParams(3.0, 0, 0, 0, 0)]
 # cells per case: keeps the scalar oracle at a few ms per instance

@@ -92,7 +92,7 @@ def golden_inputs(c):
 
 FORMS = {"msv": [P.Variant.Auto, P.Variant.Fp16, P.Variant.Dpx16, P.Variant.Fp16x,
                  P.Variant.Fp16xAlt, P.Variant.Fp16xMixed, P.Variant.Fp16xHybrid,
-                 P.Variant.Fp16xRelaxed],
+                 P.Variant.Fp16xRelaxed, P.Variant.Fp16xRelaxedFixedB],
          "ssv": [P.Variant.Auto, P.Variant.Fp16, P.Variant.Dpx16, P.Variant.Fp16x,
                  P.Variant.Fp16xMixed]}
 
@@ -228,21 +228,23 @@ def test_two_mode_msv_reports_lazy_rows():
 QUANTS = [DEFAULT, NONSAT, P.QuantParams(2.0, 240, 10, 1, 5), P.QuantParams(3.0, 0, 0, 0, 0)]
 
 
-def fp16xr_rows():
+def relaxed_rows(variant):
     import sys
     sys.path.insert(0, os.path.join(os.path.dirname(P.__file__), "csrc"))
     import gen_instances
-    return gen_instances.ROWS["fp16xr"]
+    return gen_instances.ROWS["fp16xr" if variant == P.Variant.Fp16xRelaxed else "fp16xrm"]
 
 
+@pytest.mark.parametrize("variant", [P.Variant.Fp16xRelaxed, P.Variant.Fp16xRelaxedFixedB],
+                         ids=lambda v: v.name)
 @pytest.mark.parametrize("L", [1, 2, 4, 8, 16, 32])
-def test_relaxed_msv_matches_oracle(chk, L):
+def test_relaxed_msv_matches_oracle(chk, L, variant):
     """FP16XR (relaxed MSV, no 255 cap, f16 subnormal domain): every lane
     count, the four QuantParams sets, full and partial top row groups, planted
     motifs so that at the saturating parameters many sequences are flagged and
     rescored exactly in the same scan."""
-    rng = P.Rng(0x7E1 + L)
-    rows = fp16xr_rows()
+    rng = P.Rng(0x7E1 + L + 64 * int(variant))
+    rows = relaxed_rows(variant)
     for t, q in enumerate(QUANTS):
         for m in (2 * L * rows[min(len(rows) - 1, 3 + t)] - int(rng.next() % (2 * L)), 37):
             m = max(1, m)
@@ -253,15 +255,15 @@ def test_relaxed_msv_matches_oracle(chk, L):
             with P.Scanner(0) as s:
                 s.set_profile(costs, q, hmm.lambda_, hmm.tau)
                 s.set_database(db)
-                rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv, variant=P.Variant.Fp16xRelaxed,
+                rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv, variant=variant,
                                            lanes=L, rows=H, threshold=0.2))
-            assert rep.variant == int(P.Variant.Fp16xRelaxed) and rep.rows == H
+            assert rep.variant == int(variant) and rep.rows == H
             want = chk.raw(P.Algorithm.Msv, costs, db, q)
             np.testing.assert_array_equal(rep.raw, want, err_msg=f"L={L} m={m} q={q}")
             np.testing.assert_array_equal(rep.passed,
                                           chk.passed(P.Algorithm.Msv, want, db, hmm, q, 0.2))
-            flagged = int((want >= 256 - q.dbias).sum())
-            assert rep.stats["recomputed"] >= flagged
+            if variant == P.Variant.Fp16xRelaxed:
+                assert rep.stats["recomputed"] >= int((want >= 256 - q.dbias).sum())
 
 
 def test_policy_picks_relaxed_msv_for_non_saturating_profiles(chk):
@@ -276,25 +278,28 @@ def test_policy_picks_relaxed_msv_for_non_saturating_profiles(chk):
     hits = rng.lognormal_records(140000, 60.0, 0.65, 2, plant=(hmm, 0.3))
     two_mode = {int(P.Variant.Fp16x), int(P.Variant.Fp16xAlt), int(P.Variant.Fp16xMixed),
                 int(P.Variant.Fp16xHybrid)}
-    relaxed = int(P.Variant.Fp16xRelaxed)
-    for db, q, expect in ((plain, NONSAT, [relaxed, relaxed]),
-                          (plain, DEFAULT, None),
-                          (hits, NONSAT, [relaxed, int(P.Variant.Fp16)])):
+    relaxed = {int(P.Variant.Fp16xRelaxed), int(P.Variant.Fp16xRelaxedFixedB)}
+    for db, q, kind in ((plain, NONSAT, "relaxed"), (plain, DEFAULT, "two_mode"),
+                        (hits, NONSAT, "fallback")):
         with P.Scanner(0) as s:
             s.set_database(db)
             costs = P.quantize_emissions(hmm, q)
             s.set_profile(costs, q, hmm.lambda_, hmm.tau)
             want = chk.raw(P.Algorithm.Msv, costs, db, q)
             seen = []
-            for _ in range(3):
+            for _ in range(4):
                 rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv, threshold=0.022))
                 np.testing.assert_array_equal(rep.raw, want)
                 seen.append(rep.variant)
             assert seen[0] in two_mode, seen
-            if expect is None:
-                assert seen[1] in two_mode and seen[2] in two_mode, seen
+            if kind == "two_mode":
+                assert all(v in two_mode for v in seen), seen
+            elif kind == "relaxed":
+                assert all(v in relaxed for v in seen[1:]), seen
+                assert seen[2] == seen[1] and seen[3] == seen[1], seen
             else:
-                assert seen[1:] == expect, seen
+                # relaxed forms tried, then (many flags) the exact FP16 kernel
+                assert seen[1] in relaxed and seen[3] == int(P.Variant.Fp16), seen
 
 
 def test_subnormal_selfcheck_refuses_flush_to_zero(monkeypatch):

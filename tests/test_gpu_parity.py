@@ -30,7 +30,8 @@ def rows_list(variant):
                                P.Variant.Fp16xAlt: "fp16xalt",
                                P.Variant.Fp16xMixed: "fp16xm",
                                P.Variant.Fp16xHybrid: "fp16xh",
-                               P.Variant.Fp16xRelaxed: "fp16xr"}[variant]]
+                               P.Variant.Fp16xRelaxed: "fp16xr",
+                               P.Variant.Fp16xRelaxedFixedB: "fp16xrm"}[variant]]
 
 
 def rows_for(variant, L, m):
@@ -380,18 +381,21 @@ def wrap_model(alg, costs, m, seq, q, base):
 
 @pytest.mark.parametrize("variant", [P.Variant.Fp16, P.Variant.Dpx16, P.Variant.Swar8,
                                      P.Variant.Fp16x, P.Variant.Fp16xAlt, P.Variant.Fp16xMixed,
-                                     P.Variant.Fp16xHybrid, P.Variant.Fp16xRelaxed],
+                                     P.Variant.Fp16xHybrid, P.Variant.Fp16xRelaxed,
+                                     P.Variant.Fp16xRelaxedFixedB],
                          ids=lambda v: v.name)
 @pytest.mark.parametrize("alg", [P.Algorithm.Msv, P.Algorithm.Ssv], ids=lambda a: a.name)
 def test_paper_wrap_mode(ora, variant, alg):
     """The non-normative wrap study mode runs, matches its model, and differs
     from the normative (oracle-exact) -inf injection on a consensus-heavy
     instance (test_engine.cpp:265-278)."""
-    if variant in (P.Variant.Fp16xHybrid, P.Variant.Fp16xRelaxed) and alg == P.Algorithm.Ssv:
+    if variant in (P.Variant.Fp16xHybrid, P.Variant.Fp16xRelaxed,
+                   P.Variant.Fp16xRelaxedFixedB) and alg == P.Algorithm.Ssv:
         pytest.skip("an MSV form (SSV runs FP16XM / FP16X, tested above)")
     cpw = 4 if variant == P.Variant.Swar8 else 2
     differs = False
     geoms = {P.Variant.Fp16xMixed: ((1, 10), (2, 10), (8, 5), (32, 5)),
+             P.Variant.Fp16xRelaxedFixedB: ((1, 10), (2, 10), (8, 5), (32, 5)),
              P.Variant.Fp16xHybrid: ((1, 8), (2, 10), (8, 8), (32, 10))}.get(
                  variant, ((1, 8), (2, 8), (8, 4), (32, 4)))
     # non-saturating parameters, and (two-mode MSV forms) default ones, whose
