@@ -1088,10 +1088,11 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
                 return rc;
             }
             if (nsel) {
-                // the exact twin at the same geometry where one exists (the
-                // paper-wrap study mode is capacity-dependent): FP16XR ->
-                // two-mode FP16X, FP16XRM -> two-mode FP16XM (MSV), FP16X
-                // SSV -> FP16; else FP16 at its own geometry
+                // FP16 at the geometry the policy picks for the few flagged
+                // sequences (large L: short row chains); the paper-wrap study
+                // mode is capacity-dependent, so there the exact twin at the
+                // same geometry: FP16XR -> two-mode FP16X, FP16XRM ->
+                // two-mode FP16XM (MSV), FP16X SSV -> FP16
                 lhmm_scan_options ox = *opt;
                 ox.variant = LHMM_VARIANT_FP16;
                 ox.lanes = 0;
@@ -1100,7 +1101,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
                                  : variant == LHMM_VARIANT_FP16XRM ? LHMM_VARIANT_FP16XM
                                  : variant == LHMM_VARIANT_FP16X   ? LHMM_VARIANT_FP16
                                                                    : -1;
-                if (twin >= 0 && rows_instantiated(twin, H)) {
+                if (opt->reorder_mode == 1 && twin >= 0 && rows_instantiated(twin, H)) {
                     ox.variant = twin;
                     ox.lanes = L;
                     ox.rows = H;

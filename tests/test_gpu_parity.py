@@ -230,10 +230,12 @@ def test_streamed_scan_matches_resident_scan(ora, mem_ops, monkeypatch):
                     st = s.scan_streamed(o, seg)
                     np.testing.assert_array_equal(st.raw, base.raw)
                     np.testing.assert_array_equal(st.passed, base.passed)
+                    # (+1 when a relaxed kernel's flagged sequences were rescored)
+                    extra = 1 if st.stats["recomputed"] else 0
                     if mem_ops == "1":
-                        assert st.stats["launches"] == 1
+                        assert st.stats["launches"] == 1 + extra
                     else:
-                        assert 1 <= st.stats["launches"] <= seg
+                        assert 1 <= st.stats["launches"] <= seg + extra
         np.testing.assert_array_equal(s.scan(P.ScanOptions(alg=P.Algorithm.Msv)).raw, want)
 
 
