@@ -379,6 +379,17 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
                             for (uint32_t c = 0; c < 2; ++c)
                                 slot[k] |= cost_at(x, oig, c, h0 + k) << (16 * c);
                     }
+                    if (s >= nm + n4) {
+                        // two-row remainder slot: pairs packed densely, with
+                        // the exact table's quarter-warp duplicate for L < 16
+                        // (lhmm_kernel.cuh part_off): a conflict-free LDS.64
+                        const size_t at2 = size_t(x) * P2 + size_t(s) * 4 * L + 2 * oig;
+                        for (uint32_t g = 0; g < copies2; ++g)
+                            for (uint32_t qw = 0; qw < (L < 16 ? 2u : 1u); ++qw)
+                                for (int w = 0; w < 2; ++w)
+                                    b[size_t(g) * cs2 + at2 + qw * 2 * L + w] = slot[w];
+                        continue;
+                    }
                     const size_t at = size_t(x) * P2 + size_t(s) * 4 * L + 4 * oig;
                     for (uint32_t g = 0; g < copies2; ++g)
                         for (int w = 0; w < 4; ++w) b[size_t(g) * cs2 + at + w] = slot[w];

@@ -1024,8 +1024,11 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                 constexpr int N4 = R4 / 4;
                 static_assert(NM >= 0 && (R4 % 4 == 0 || R4 % 4 == 2), "hybrid row split");
                 if constexpr (R4 % 4 == 2) {
+                    // two-row remainder slot: word pairs packed densely like
+                    // the exact table's top group (conflict-free LDS.64)
                     constexpr int slot = NM + N4;
-                    const uint4 c = *reinterpret_cast<const uint4*>(tp + slot * 4 * TL);
+                    const uint2 c =
+                        *reinterpret_cast<const uint2*>(tp + part_off + slot * 4 * TL);
                     const uint32_t cw[2] = {c.x, c.y};
 #pragma unroll
                     for (int k = 1; k >= 0; --k) {
