@@ -196,6 +196,11 @@ int lhmm_set_profile(lhmm_context* ctx, const uint8_t* costs, uint32_t m, const 
 int lhmm_add_profile(lhmm_context* ctx, const uint8_t* costs, uint32_t m, const lhmm_quant* q,
                      double lambda, double tau, uint32_t* profile_id);
 int lhmm_select_profile(lhmm_context* ctx, uint32_t profile_id);
+/* Replace resident profile `profile_id` in place (its device tables and
+ * policy feedback are dropped) and make it current: bounded profile caches
+ * (the engine.hpp drop-in's LRU) reuse slots instead of growing. */
+int lhmm_update_profile(lhmm_context* ctx, uint32_t profile_id, const uint8_t* costs, uint32_t m,
+                        const lhmm_quant* q, double lambda, double tau);
 
 /* Database: flat residue codes (0..20) with nseq+1 offsets.  Packs the
  * shard (shard_rank of shard_count, balanced by residue count) into

@@ -78,6 +78,8 @@ SIGNATURES = {
     "lhmm_add_profile": (C.c_int, [vp, u8p, C.c_uint32, C.POINTER(Quant), C.c_double,
                                    C.c_double, u32p]),
     "lhmm_select_profile": (C.c_int, [vp, C.c_uint32]),
+    "lhmm_update_profile": (C.c_int, [vp, C.c_uint32, u8p, C.c_uint32, C.POINTER(Quant), C.c_double,
+                                      C.c_double]),
     "lhmm_set_database": (C.c_int, [vp, u8p, u64p, C.c_uint64, C.c_uint32, C.c_uint32, u64p]),
     "lhmm_shard_indices": (C.c_int, [vp, u64p]),
     "lhmm_database_stats": (C.c_int, [vp, u64p, u64p, u64p, u64p]),

@@ -1646,6 +1646,17 @@ int lhmm_add_profile(lhmm_context* c, const uint8_t* costs, uint32_t m, const lh
     return LHMM_OK;
 }
 
+int lhmm_update_profile(lhmm_context* c, uint32_t id, const uint8_t* costs, uint32_t m,
+                        const lhmm_quant* q, double lambda, double tau) {
+    if (!c) return set_error(LHMM_ERR_CONTRACT, "null context");
+    if (id >= c->profiles.size() || c->profiles[id].m == 0)
+        return set_error(LHMM_ERR_CONTRACT, "unknown profile id");
+    DeviceGuard g(c->device);
+    if (int rc = fill_profile(c->profiles[id], costs, m, q, lambda, tau)) return rc;
+    c->current = int(id);
+    return LHMM_OK;
+}
+
 int lhmm_select_profile(lhmm_context* c, uint32_t id) {
     if (!c) return set_error(LHMM_ERR_CONTRACT, "null context");
     if (id >= c->profiles.size() || c->profiles[id].m == 0)

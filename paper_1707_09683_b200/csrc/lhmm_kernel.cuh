@@ -108,9 +108,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 // Stage `bytes` (multiple of 16) from global into shared memory with the
-// bulk-copy (TMA) engine, completing on an mbarrier.
-__device__ __forceinline__ void stage_table(uint32_t* smem, const uint32_t* gsrc, uint32_t bytes,
-                                            uint64_t* bar) {
+// bulk-copy (TMA) engine, completing on an mbarrier: stage_table_issue (all
+// threads: barrier init, one thread issues the copies) and
+// stage_table_wait (any thread, before its first table read) -- a warp can
+// claim its first work item and start its residue loads while the table
+// lands.
+__device__ __forceinline__ void stage_table_issue(uint32_t* smem, const uint32_t* gsrc,
+                                                  uint32_t bytes, uint64_t* bar) {
     const uint32_t b = smem_u32(bar);
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
@@ -131,6 +135,10 @@ __device__ __forceinline__ void stage_table(uint32_t* smem, const uint32_t* gsrc
                 : "memory");
         }
     }
+}
+
+__device__ __forceinline__ void stage_table_wait(uint64_t* bar) {
+    const uint32_t b = smem_u32(bar);
     uint32_t done = 0;
     while (!done) {
         asm volatile(
@@ -1250,7 +1258,8 @@ template <class V, int L, int H>
 __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KParams p) {
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t bar;
-    stage_table(smem, p.table, p.table_bytes, &bar);
+    stage_table_issue(smem, p.table, p.table_bytes, &bar);
+    bool table_ready = false;
 
     static_assert(H % 2 == 0 || group_width<V>::value == 5,
                   "rows are read four (or, in the top group, two) at a time");
@@ -1297,7 +1306,11 @@ __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KPar
             item = __shfl_sync(kFull, item, 0);
         }
         next_static = 0xffffffffu;
-        if (item >= p.n_items) break;
+        if (item >= p.n_items) {
+            // no CTA may exit with its table copy in flight
+            if (!table_ready && threadIdx.x < 32) stage_table_wait(&bar);
+            break;
+        }
         const uint32_t tile = p.tile_base + item / L;
         if (p.n_pieces) wait_for_tile(p, tile, ready_below);  // warp-uniform
         const uint32_t sub = item % L;
@@ -1328,6 +1341,10 @@ __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KPar
         bool done = false;
         ResChunk<RPI> pre{};
         if (rows > 0) pre = load_res<RPI>(src, 0);
+        if (!table_ready) {  // the first item's residues are in flight
+            stage_table_wait(&bar);
+            table_ready = true;
+        }
 #pragma unroll 1
         for (; r0 < rows && !done; r0 += RPI) {
             done = run_chunk<V, L, H, RPI, false>(g, e0, e1, e2, e3, st, p, src, r0, rows, pre,

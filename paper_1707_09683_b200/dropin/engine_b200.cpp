@@ -64,7 +64,8 @@ struct Slot {
     lhmm_context* ctx = nullptr;
     bool have_db = false;
     uint64_t db_hash = 0;
-    std::map<uint64_t, uint32_t> profiles;  // content hash -> profile id
+    std::map<uint64_t, std::pair<uint32_t, uint64_t>> profiles;  // hash -> (id, last use)
+    uint64_t clock = 0;
 };
 
 constexpr size_t kMaxSlots = 4;
@@ -283,13 +284,21 @@ DeviceScan device_scan(const CostMatrix& costs, Flat& flat, const QuantParams& q
     }
     const auto pit = slot.profiles.find(ph);
     if (pit != slot.profiles.end()) {
-        check(lhmm_select_profile(c, pit->second));
+        check(lhmm_select_profile(c, pit->second.first));
+        pit->second.second = ++slot.clock;
     } else if (slot.profiles.size() < kMaxCachedProfiles) {
         uint32_t id = 0;
         check(lhmm_add_profile(c, costs.bytes.data(), costs.modelLength, &lq, lambda, tau, &id));
-        slot.profiles.emplace(ph, id);
+        slot.profiles.emplace(ph, std::make_pair(id, ++slot.clock));
     } else {
-        check(lhmm_set_profile(c, costs.bytes.data(), costs.modelLength, &lq, lambda, tau));
+        // full: the least recently used profile's slot takes the new one
+        auto lru = slot.profiles.begin();
+        for (auto it = slot.profiles.begin(); it != slot.profiles.end(); ++it)
+            if (it->second.second < lru->second.second) lru = it;
+        const uint32_t id = lru->second.first;
+        slot.profiles.erase(lru);
+        check(lhmm_update_profile(c, id, costs.bytes.data(), costs.modelLength, &lq, lambda, tau));
+        slot.profiles.emplace(ph, std::make_pair(id, ++slot.clock));
     }
     lhmm_scan_options o{};
     o.alg = alg_code(alg);

@@ -39,9 +39,11 @@ def main():
         s.set_profile(costs, q, hmm.lambda_, hmm.tau)
         s.set_database(db)
         for v in (P.Variant.Fp16, P.Variant.Fp16x, P.Variant.Fp16xAlt, P.Variant.Fp16xMixed,
-                  P.Variant.Fp16xHybrid, P.Variant.Dpx16, P.Variant.Swar8):
+                  P.Variant.Fp16xHybrid, P.Variant.Fp16xRelaxed, P.Variant.Fp16xRelaxedFixedB,
+                  P.Variant.Dpx16, P.Variant.Swar8):
             for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
-                if v in (P.Variant.Fp16xAlt, P.Variant.Fp16xHybrid) and alg == P.Algorithm.Ssv:
+                if v in (P.Variant.Fp16xAlt, P.Variant.Fp16xHybrid, P.Variant.Fp16xRelaxed,
+                         P.Variant.Fp16xRelaxedFixedB) and alg == P.Algorithm.Ssv:
                     continue
                 for L in (1, 4, 32):
                     rep = s.scan(P.ScanOptions(alg=alg, variant=v, lanes=L, threshold=0.2))
@@ -82,6 +84,28 @@ def main():
         s.set_database(big)
         for alg in (P.Algorithm.Msv, P.Algorithm.Ssv):
             check(s.scan(P.ScanOptions(alg=alg, threshold=0.2)), costs, q, big, alg)
+    # relaxed MSV forms with rescoring (planted hits flag sequences) at
+    # non-saturating parameters, and the block gather's scatter kernel
+    qn = P.QuantParams(3.0, 120, 3, 20, 20)
+    hits = rng.random_records(600, 1, 300, plant=(hmm, 0.5))
+    cn = P.quantize_emissions(hmm, qn)
+    with P.Scanner(0) as s:
+        s.set_profile(cn, qn, hmm.lambda_, hmm.tau)
+        s.set_database(hits)
+        for v in (P.Variant.Fp16xRelaxed, P.Variant.Fp16xRelaxedFixedB):
+            for L in (1, 8, 32):
+                rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv, variant=v, lanes=L, threshold=0.2))
+                check(rep, cn, qn, hits, P.Algorithm.Msv)
+                assert rep.stats["recomputed"] > 0
+        import torch
+        n = hits.count
+        perm = torch.randperm(n, device="cuda")
+        src = torch.randint(0, 255, (2, n), dtype=torch.uint8, device="cuda")
+        dst = torch.zeros((2, n), dtype=torch.uint8, device="cuda")
+        s.scatter_results(dst[0].data_ptr(), dst[1].data_ptr(), src[0].data_ptr(),
+                          src[1].data_ptr(), perm.data_ptr(), n)
+        s.synchronize()
+        assert torch.equal(dst[:, perm], src)
     print(f"sanitize driver ok: {checked} scans bit-exact")
 
 
