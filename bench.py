@@ -663,7 +663,23 @@ def main():  # noqa: C901
         return launches
 
     for j in range(args.warmup):
-        step(j, False)
+        try:
+            step(j, False)
+        except Exception as e:  # noqa: BLE001
+            # the block gather's peer copies failed at run time on some rank:
+            # every rank switches to the collective gather (agreed below)
+            if world == 1 or not hasattr(gatherer, "push"):
+                raise
+            log(f"[bench] block gather failed ({e}); using the collective gather")
+            gatherer = None
+        if world > 1:
+            ok = torch.tensor([1 if gatherer is not None else 0], dtype=torch.int32,
+                              device=comm_dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 0 and (gatherer is None or hasattr(gatherer, "push")):
+                from paper_1707_09683_b200.shard import NcclGather
+                gatherer = NcclGather(dist, gidx, n_total, comm_dev)
+                gather_mode = "torch.distributed gather, 2 bytes per sequence"
     torch.cuda.synchronize()
     if dist:
         dist.barrier()

@@ -1560,6 +1560,7 @@ int lhmm_context_destroy(lhmm_context* c) {
     if (c->evr1) cudaEventDestroy(c->evr1);
     c->d_counter.release();
     c->d_sat.release();
+    c->d_mode_rows.release();
     c->d_raw.release();
     c->d_pass.release();
     cudaEventDestroy(c->ev0);

@@ -1258,7 +1258,18 @@ template <class V, int L, int H>
 __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KParams p) {
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t bar;
-    stage_table_issue(smem, p.table, p.table_bytes, &bar);
+    // per-CTA tallies (saturated and flagged sequences, two-mode row counts),
+    // flushed with one global atomic each at the end: a small database's
+    // warps all finish together, and per-warp global atomics on one address
+    // serialised in L2 at the kernel's tail
+    __shared__ uint32_t s_sat, s_flag;
+    __shared__ unsigned long long s_rows[2];
+    if (threadIdx.x == 0) {
+        s_sat = 0u;
+        s_flag = 0u;
+        s_rows[0] = s_rows[1] = 0ull;
+    }
+    stage_table_issue(smem, p.table, p.table_bytes, &bar);  // (its __syncthreads publishes them)
     bool table_ready = false;
 
     static_assert(H % 2 == 0 || group_width<V>::value == 5,
@@ -1398,20 +1409,34 @@ __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KPar
         }
         if (p.fault && grp == 0 && raw < 255u) raw += 1u;  // verification aid
         const uint32_t oi = p.out_idx[sidx];
-        if (oig == 0 && oi != 0xffffffffu) {
+        const bool writer = oig == 0 && oi != 0xffffffffu;
+        if (writer) {
             p.raw_out[oi] = uint8_t(raw);
             p.pass_out[oi] = uint8_t(raw == 255u || raw >= p.rawmin_tab[len]);
-            if (msv_alg<V>::value && p.sat_count && raw == 255u) atomicAdd(p.sat_count, 1u);
-            if constexpr (V::kRelaxed) {
-                p.flag_out[oi] = exact_needed ? 1u : 0u;
-                if (exact_needed) atomicAdd(p.flag_count, 1u);
-            }
+            if constexpr (V::kRelaxed) p.flag_out[oi] = exact_needed ? 1u : 0u;
+        }
+        if constexpr (msv_alg<V>::value) {
+            const uint32_t m = __ballot_sync(kFull, writer && raw == 255u);
+            if (lane == 0 && m) atomicAdd(&s_sat, uint32_t(__popc(m)));
+        }
+        if constexpr (V::kRelaxed) {
+            const uint32_t m = __ballot_sync(kFull, writer && exact_needed);
+            if (lane == 0 && m) atomicAdd(&s_flag, uint32_t(__popc(m)));
         }
     }
     if constexpr (V::kTwoMode) {
-        if (lane == 0 && p.mode_rows && rows_all) {
-            atomicAdd(p.mode_rows, rows_all);
-            atomicAdd(p.mode_rows + 1, rows_lazy);
+        if (lane == 0 && rows_all) {
+            atomicAdd(&s_rows[0], rows_all);
+            atomicAdd(&s_rows[1], rows_lazy);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (p.sat_count && s_sat) atomicAdd(p.sat_count, s_sat);
+        if (p.flag_count && s_flag) atomicAdd(p.flag_count, s_flag);
+        if (p.mode_rows && s_rows[0]) {
+            atomicAdd(p.mode_rows, s_rows[0]);
+            atomicAdd(p.mode_rows + 1, s_rows[1]);
         }
     }
 }

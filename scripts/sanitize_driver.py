@@ -106,6 +106,9 @@ def main():
                           src[1].data_ptr(), perm.data_ptr(), n)
         s.synchronize()
         assert torch.equal(dst[:, perm], src)
+        del perm, src, dst
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()  # the caching allocator's blocks (memcheck leak check)
     print(f"sanitize driver ok: {checked} scans bit-exact")
 
 
