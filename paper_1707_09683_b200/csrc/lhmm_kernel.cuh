@@ -108,13 +108,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 // Stage `bytes` (multiple of 16) from global into shared memory with the
-// bulk-copy (TMA) engine, completing on an mbarrier: stage_table_issue (all
-// threads: barrier init, one thread issues the copies) and
-// stage_table_wait (any thread, before its first table read) -- a warp can
-// claim its first work item and start its residue loads while the table
-// lands.
-__device__ __forceinline__ void stage_table_issue(uint32_t* smem, const uint32_t* gsrc,
-                                                  uint32_t bytes, uint64_t* bar) {
+// bulk-copy (TMA) engine, completing on an mbarrier.
+__device__ __forceinline__ void stage_table(uint32_t* smem, const uint32_t* gsrc, uint32_t bytes,
+                                            uint64_t* bar) {
     const uint32_t b = smem_u32(bar);
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
@@ -135,10 +131,6 @@ __device__ __forceinline__ void stage_table_issue(uint32_t* smem, const uint32_t
                 : "memory");
         }
     }
-}
-
-__device__ __forceinline__ void stage_table_wait(uint64_t* bar) {
-    const uint32_t b = smem_u32(bar);
     uint32_t done = 0;
     while (!done) {
         asm volatile(
@@ -1258,19 +1250,7 @@ template <class V, int L, int H>
 __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KParams p) {
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t bar;
-    // per-CTA tallies (saturated and flagged sequences, two-mode row counts),
-    // flushed with one global atomic each at the end: a small database's
-    // warps all finish together, and per-warp global atomics on one address
-    // serialised in L2 at the kernel's tail
-    __shared__ uint32_t s_sat, s_flag;
-    __shared__ unsigned long long s_rows[2];
-    if (threadIdx.x == 0) {
-        s_sat = 0u;
-        s_flag = 0u;
-        s_rows[0] = s_rows[1] = 0ull;
-    }
-    stage_table_issue(smem, p.table, p.table_bytes, &bar);  // (its __syncthreads publishes them)
-    bool table_ready = false;
+    stage_table(smem, p.table, p.table_bytes, &bar);
 
     static_assert(H % 2 == 0 || group_width<V>::value == 5,
                   "rows are read four (or, in the top group, two) at a time");
@@ -1317,11 +1297,7 @@ __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KPar
             item = __shfl_sync(kFull, item, 0);
         }
         next_static = 0xffffffffu;
-        if (item >= p.n_items) {
-            // no CTA may exit with its table copy in flight
-            if (!table_ready && threadIdx.x < 32) stage_table_wait(&bar);
-            break;
-        }
+        if (item >= p.n_items) break;
         const uint32_t tile = p.tile_base + item / L;
         if (p.n_pieces) wait_for_tile(p, tile, ready_below);  // warp-uniform
         const uint32_t sub = item % L;
@@ -1352,10 +1328,6 @@ __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KPar
         bool done = false;
         ResChunk<RPI> pre{};
         if (rows > 0) pre = load_res<RPI>(src, 0);
-        if (!table_ready) {  // the first item's residues are in flight
-            stage_table_wait(&bar);
-            table_ready = true;
-        }
 #pragma unroll 1
         for (; r0 < rows && !done; r0 += RPI) {
             done = run_chunk<V, L, H, RPI, false>(g, e0, e1, e2, e3, st, p, src, r0, rows, pre,
@@ -1409,34 +1381,20 @@ __global__ void __launch_bounds__(threads_for<V, H>(), 1) scan_kernel(const KPar
         }
         if (p.fault && grp == 0 && raw < 255u) raw += 1u;  // verification aid
         const uint32_t oi = p.out_idx[sidx];
-        const bool writer = oig == 0 && oi != 0xffffffffu;
-        if (writer) {
+        if (oig == 0 && oi != 0xffffffffu) {
             p.raw_out[oi] = uint8_t(raw);
             p.pass_out[oi] = uint8_t(raw == 255u || raw >= p.rawmin_tab[len]);
-            if constexpr (V::kRelaxed) p.flag_out[oi] = exact_needed ? 1u : 0u;
-        }
-        if constexpr (msv_alg<V>::value) {
-            const uint32_t m = __ballot_sync(kFull, writer && raw == 255u);
-            if (lane == 0 && m) atomicAdd(&s_sat, uint32_t(__popc(m)));
-        }
-        if constexpr (V::kRelaxed) {
-            const uint32_t m = __ballot_sync(kFull, writer && exact_needed);
-            if (lane == 0 && m) atomicAdd(&s_flag, uint32_t(__popc(m)));
+            if (msv_alg<V>::value && p.sat_count && raw == 255u) atomicAdd(p.sat_count, 1u);
+            if constexpr (V::kRelaxed) {
+                p.flag_out[oi] = exact_needed ? 1u : 0u;
+                if (exact_needed) atomicAdd(p.flag_count, 1u);
+            }
         }
     }
     if constexpr (V::kTwoMode) {
-        if (lane == 0 && rows_all) {
-            atomicAdd(&s_rows[0], rows_all);
-            atomicAdd(&s_rows[1], rows_lazy);
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (p.sat_count && s_sat) atomicAdd(p.sat_count, s_sat);
-        if (p.flag_count && s_flag) atomicAdd(p.flag_count, s_flag);
-        if (p.mode_rows && s_rows[0]) {
-            atomicAdd(p.mode_rows, s_rows[0]);
-            atomicAdd(p.mode_rows + 1, s_rows[1]);
+        if (lane == 0 && p.mode_rows && rows_all) {
+            atomicAdd(p.mode_rows, rows_all);
+            atomicAdd(p.mode_rows + 1, rows_lazy);
         }
     }
 }
