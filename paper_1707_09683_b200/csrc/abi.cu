@@ -417,15 +417,24 @@ struct lhmm_context {
     DevBuf<uint8_t> d_db;
     DevBuf<uint64_t> d_tile_off;
     DevBuf<uint32_t> d_lens, d_out_idx;
-    DevBuf<uint32_t> d_counter;
-    DevBuf<uint32_t> d_sat;        // MSV saturated-score count of the last scan
-    DevBuf<unsigned long long> d_mode_rows;  // two-mode MSV: [rows, lazy rows]
-    DevBuf<uint8_t> d_raw, d_pass;
+    // one 32-byte block of per-scan counters, cleared with one memset and read
+    // back with one copy: u32 [0] work-item counter, [1] MSV saturated
+    // scores, [2] relaxed-kernel flags; u64 [2..3] two-mode rows, lazy rows
+    DevBuf<unsigned long long> d_counts;
+    uint32_t* counter32() { return reinterpret_cast<uint32_t*>(d_counts.ptr); }
+    // raw | pass of the resident database, contiguous (one result copy)
+    DevBuf<uint8_t> d_raw;
+    struct {
+        uint8_t* ptr = nullptr;
+        void release() { ptr = nullptr; }
+    } d_pass;
+    // lhmm_scan: the kernel's results are copied to out_host right behind it
+    // (one host round trip per scan) when nothing needs rescoring
+    bool stage_out = false, staged = false;
     DevBuf<uint32_t> d_out_gidx;   // slot -> GLOBAL sequence index (fused peer gather)
     uint64_t n_global = 0;         // sequences of the whole (unsharded) database
     std::vector<void*> peer_own, peer_open;  // exported / mapped peer output buffers
     DevBuf<uint8_t> d_flag;        // FP16X: per-sequence "rescore exactly"
-    DevBuf<uint32_t> d_flag_count;
 
     std::map<std::tuple<int, int, uint32_t, uint32_t, size_t>, std::pair<int, int>> occupancy;
     // geometry policy results per (m, alg, variant, want_L, tiles)
@@ -512,8 +521,8 @@ int upload_db(lhmm_context* c) {
     if (int rc = c->d_tile_off.reserve(db.tile_off.size())) return rc;
     if (int rc = c->d_lens.reserve(db.lens.size())) return rc;
     if (int rc = c->d_out_idx.reserve(db.out_idx.size())) return rc;
-    if (int rc = c->d_raw.reserve(db.n_local)) return rc;
-    if (int rc = c->d_pass.reserve(db.n_local)) return rc;
+    if (int rc = c->d_raw.reserve(2 * std::max<uint64_t>(db.n_local, 1))) return rc;
+    c->d_pass.ptr = c->d_raw.ptr + db.n_local;
     if (!c->host_resident)
         CUDA_TRY(cudaMemcpyAsync(c->d_db.ptr, db.data, db.data_bytes, cudaMemcpyHostToDevice,
                                  c->stream));
@@ -588,9 +597,10 @@ int outputs_to_host(lhmm_context* c, uint8_t* raw, uint8_t* pass, uint64_t n) {
         return LHMM_OK;
     }
     uint8_t* h = c->out_host.ptr;
-    CUDA_TRY(cudaMemcpyAsync(h, c->d_raw.ptr, n, cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaMemcpyAsync(h + n, c->d_pass.ptr, n, cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (!c->staged) {
+        CUDA_TRY(cudaMemcpyAsync(h, c->d_raw.ptr, 2 * n, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+    }
     constexpr uint64_t kChunk = 1 << 18;
     const int64_t chunks = int64_t((2 * n + kChunk - 1) / kChunk);
 #pragma omp parallel for schedule(static) if (chunks > 1)
@@ -786,7 +796,8 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         }
         lit = pf.lens.emplace(lkey, std::move(lt)).first;
     }
-    if (int rc = c->d_counter.reserve(1)) return rc;
+    if (int rc = c->d_counts.reserve(4)) return rc;
+    CUDA_TRY(cudaMemsetAsync(c->d_counts.ptr, 0, 32, c->stream));
 
     lhmm::KParams p{};
     p.db = v.db;
@@ -798,7 +809,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     p.table = tab.buf.ptr;
     p.raw_out = d_raw;
     p.pass_out = d_pass;
-    p.counter = c->d_counter.ptr;
+    p.counter = c->counter32();
     p.n_items = uint32_t(v.n_tiles * items_per_tile);
     p.table_bytes = uint32_t(table_bytes);
     p.res_stride = tab.res_stride;
@@ -810,19 +821,11 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     p.tecjb = uint32_t(pf.q.tec) + uint32_t(pf.q.tjb);
     p.fault = opt->fault_injection ? 1u : 0u;
     const bool track_sat = opt->alg == LHMM_MSV && view == nullptr;
-    if (track_sat) {
-        if (int rc = c->d_sat.reserve(1)) return rc;
-        CUDA_TRY(cudaMemsetAsync(c->d_sat.ptr, 0, 4, c->stream));
-        p.sat_count = c->d_sat.ptr;
-    }
+    if (track_sat) p.sat_count = c->counter32() + 1;
     const bool track_modes = opt->alg == LHMM_MSV && !long_model &&
                              (variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16X_ALT ||
                               variant == LHMM_VARIANT_FP16XM || variant == LHMM_VARIANT_FP16XH);
-    if (track_modes) {
-        if (int rc = c->d_mode_rows.reserve(2)) return rc;
-        CUDA_TRY(cudaMemsetAsync(c->d_mode_rows.ptr, 0, 16, c->stream));
-        p.mode_rows = c->d_mode_rows.ptr;
-    }
+    if (track_modes) p.mode_rows = c->d_counts.ptr + 2;
     p.wrap = opt->reorder_mode == 1 ? 1u : 0u;
     const bool relaxed = ((variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16XM) &&
                           opt->alg == LHMM_SSV) ||
@@ -832,15 +835,13 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         if (int rc = c->d_flag.reserve(
                 std::max<uint64_t>(global_out ? c->n_global : c->db.n_local, 1)))
             return rc;
-        if (int rc = c->d_flag_count.reserve(1)) return rc;
         if (!c->evr0) {
             CUDA_TRY(cudaEventCreate(&c->evr0));
             CUDA_TRY(cudaEventCreate(&c->evr1));
         }
-        CUDA_TRY(cudaMemsetAsync(c->d_flag_count.ptr, 0, 4, c->stream));
         CUDA_TRY(cudaEventRecord(c->evr0, c->stream));
         p.flag_out = c->d_flag.ptr;
-        p.flag_count = c->d_flag_count.ptr;
+        p.flag_count = c->counter32() + 2;
     }
 
     lhmm::LaunchCfg cfg{};
@@ -902,7 +903,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             const uint64_t need_s = (uint64_t(ps.n_items) + warps_per_cta - 1) / warps_per_cta;
             cs.grid = int(std::max<uint64_t>(
                 1, std::min<uint64_t>(uint64_t(c->sm_count) * bps, need_s)));
-            CUDA_TRY(cudaMemsetAsync(c->d_counter.ptr, 0, sizeof(uint32_t), c->stream));
+            CUDA_TRY(cudaMemsetAsync(c->counter32(), 0, sizeof(uint32_t), c->stream));
             if (fn(lhmm::kOpLaunch, int(H), &cs, &ps) != 0)
                 return set_error(LHMM_ERR_CUDA, std::string("kernel launch failed: ") +
                                                     cudaGetErrorString(cudaGetLastError()));
@@ -911,8 +912,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             t0 = t1;
         }
     } else if (segments <= 0) {
-        CUDA_TRY(cudaMemsetAsync(c->d_counter.ptr, 0, sizeof(uint32_t), c->stream));
-        CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+        CUDA_TRY(cudaEventRecord(c->ev0, c->stream));  // (counters cleared above)
         if (p.n_items > 0) {
             if (fn(lhmm::kOpLaunch, int(H), &cfg, &p) != 0)
                 return set_error(LHMM_ERR_CUDA, std::string("kernel launch failed: ") +
@@ -956,7 +956,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         ps.piece_end = c->d_pieces.ptr;
         ps.piece_ready = c->d_pieces.ptr + kMaxPieces;
         ps.n_pieces = uint32_t(ends.size());
-        CUDA_TRY(cudaMemsetAsync(c->d_counter.ptr, 0, sizeof(uint32_t), c->stream));
+        CUDA_TRY(cudaMemsetAsync(c->counter32(), 0, sizeof(uint32_t), c->stream));
         if (p.n_items > 0 && fn(lhmm::kOpLaunch, int(H), &cfg, &ps) != 0)
             return set_error(LHMM_ERR_CUDA, std::string("kernel launch failed: ") +
                                                 cudaGetErrorString(cudaGetLastError()));
@@ -1013,7 +1013,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             const uint64_t need_s = (uint64_t(ps.n_items) + warps_per_cta - 1) / warps_per_cta;
             cs.grid = int(std::max<uint64_t>(
                 1, std::min<uint64_t>(uint64_t(c->sm_count) * bps, need_s)));
-            CUDA_TRY(cudaMemsetAsync(c->d_counter.ptr, 0, sizeof(uint32_t), c->stream));
+            CUDA_TRY(cudaMemsetAsync(c->counter32(), 0, sizeof(uint32_t), c->stream));
             if (fn(lhmm::kOpLaunch, int(H), &cs, &ps) != 0)
                 return set_error(LHMM_ERR_CUDA, std::string("kernel launch failed: ") +
                                                     cudaGetErrorString(cudaGetLastError()));
@@ -1021,23 +1021,25 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
             t0 = t1;
         }
     }
-    // the saturation / flag counters come back with the same synchronisation
-    // as the end event (pinned words, no extra round trip)
+    // the counters (and, for lhmm_scan, the results) come back with the same
+    // synchronisation as the end event: one 32-byte copy into pinned words
     uint32_t* counts = c->counts_host.reserve(32) ? reinterpret_cast<uint32_t*>(c->counts_host.ptr)
                                                   : nullptr;
     uint64_t mode_rows[2] = {0, 0};
     // the scan kernel's window ends here; the bookkeeping copies below are
     // synchronised through ev_done
     CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
-    if (counts) {
-        if (track_sat)
-            CUDA_TRY(cudaMemcpyAsync(counts, c->d_sat.ptr, 4, cudaMemcpyDeviceToHost, c->stream));
-        if (relaxed)
-            CUDA_TRY(cudaMemcpyAsync(counts + 1, c->d_flag_count.ptr, 4, cudaMemcpyDeviceToHost,
-                                     c->stream));
-        if (track_modes)
-            CUDA_TRY(cudaMemcpyAsync(counts + 2, c->d_mode_rows.ptr, 16, cudaMemcpyDeviceToHost,
-                                     c->stream));
+    if (!counts) return set_error(LHMM_ERR_NOMEM, "cannot allocate pinned counter words");
+    if (track_sat || relaxed || track_modes)
+        CUDA_TRY(cudaMemcpyAsync(counts, c->d_counts.ptr, 32, cudaMemcpyDeviceToHost, c->stream));
+    // lhmm_scan's results right behind the kernel (valid unless rescored)
+    const uint64_t nres = c->db.n_local;
+    c->staged = false;
+    if (c->stage_out && view == nullptr && !global_out && d_raw == c->d_raw.ptr &&
+        d_pass == c->d_pass.ptr && nres > 0 && c->out_host.reserve(2 * nres)) {
+        CUDA_TRY(cudaMemcpyAsync(c->out_host.ptr, c->d_raw.ptr, 2 * nres, cudaMemcpyDeviceToHost,
+                                 c->stream));
+        c->staged = true;
     }
     if (!c->ev_done) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
     CUDA_TRY(cudaEventRecord(c->ev_done, c->stream));
@@ -1046,31 +1048,17 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     CUDA_TRY(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
     uint32_t nsat = 0;
     if (track_sat && v.sequences > 0) {
-        if (counts)
-            nsat = counts[0];
-        else
-            CUDA_TRY(cudaMemcpy(&nsat, c->d_sat.ptr, 4, cudaMemcpyDeviceToHost));
+        nsat = counts[1];
         pf.sat_frac = double(nsat) / double(v.sequences);
         pf.sat_gen = c->db_gen;
     }
-    if (track_modes) {
-        if (counts)
-            std::memcpy(mode_rows, counts + 2, 16);
-        else
-            CUDA_TRY(cudaMemcpy(mode_rows, c->d_mode_rows.ptr, 16, cudaMemcpyDeviceToHost));
-    }
+    if (track_modes) std::memcpy(mode_rows, counts + 4, 16);
     uint32_t recomputed = 0;
     if (relaxed) {
         // rescore the flagged sequences with the exact kernel; the reported
         // time spans the relaxed kernel, the flag check and the rescoring
-        uint32_t nflag = 0;
-        if (counts) {
-            nflag = counts[1];
-        } else {
-            CUDA_TRY(cudaMemcpyAsync(&nflag, c->d_flag_count.ptr, 4, cudaMemcpyDeviceToHost,
-                                     c->stream));
-            CUDA_TRY(cudaStreamSynchronize(c->stream));
-        }
+        const uint32_t nflag = counts[2];
+        if (nflag) c->staged = false;  // the staged results predate the rescoring
         if (nflag) {
             DbView sub;
             uint32_t nsel = 0;
@@ -1555,12 +1543,9 @@ int lhmm_context_destroy(lhmm_context* c) {
     c->pipe.release();
     c->resc.release();
     c->d_flag.release();
-    c->d_flag_count.release();
     if (c->evr0) cudaEventDestroy(c->evr0);
     if (c->evr1) cudaEventDestroy(c->evr1);
-    c->d_counter.release();
-    c->d_sat.release();
-    c->d_mode_rows.release();
+    c->d_counts.release();
     c->d_raw.release();
     c->d_pass.release();
     cudaEventDestroy(c->ev0);
@@ -1835,8 +1820,16 @@ int lhmm_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* raw, uint8
     if (!raw || !pass) return set_error(LHMM_ERR_CONTRACT, "null output");
     DeviceGuard g(c->device);
     if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
-    if (int rc = do_scan(c, opt, c->d_raw.ptr, c->d_pass.ptr, st)) return rc;
-    return outputs_to_host(c, raw, pass, c->db.n_local);
+    c->stage_out = !(page_locked(raw) && page_locked(pass));
+    const int rc = do_scan(c, opt, c->d_raw.ptr, c->d_pass.ptr, st);
+    c->stage_out = false;
+    if (rc) {
+        c->staged = false;
+        return rc;
+    }
+    const int orc = outputs_to_host(c, raw, pass, c->db.n_local);
+    c->staged = false;
+    return orc;
 }
 
 int lhmm_scan_streamed(lhmm_context* c, const lhmm_scan_options* opt, int segments,

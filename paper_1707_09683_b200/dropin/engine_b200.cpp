@@ -345,7 +345,7 @@ DeviceScan device_scan(const CostMatrix& costs, Flat& flat, const QuantParams& q
     // (uninitialised: first touched by the parallel loop)
     std::unique_ptr<Final[]> fin(new Final[n]);
     const bool msv = alg == Algorithm::Msv;
-#pragma omp parallel for schedule(static) num_threads(std::max(1, workers)) if (n > 4096)
+#pragma omp parallel for schedule(static) num_threads(std::max(1, workers)) if (n > 1024)
     for (int64_t i = 0; i < int64_t(n); ++i) {
         const Proto& p = flat.protos[size_t(i)];
         const uint8_t r = raw[size_t(i)];
