@@ -420,14 +420,15 @@ struct lhmm_context {
     // one 32-byte block of per-scan counters, cleared with one memset and read
     // back with one copy: u32 [0] work-item counter, [1] MSV saturated
     // scores, [2] relaxed-kernel flags; u64 [2..3] two-mode rows, lazy rows
-    DevBuf<unsigned long long> d_counts;
-    uint32_t* counter32() { return reinterpret_cast<uint32_t*>(d_counts.ptr); }
-    // raw | pass of the resident database, contiguous (one result copy)
-    DevBuf<uint8_t> d_raw;
-    struct {
+    // [32-byte counters | raw n | pass n] of the resident database in one
+    // allocation: lhmm_scan brings counters and results back in one copy
+    DevBuf<uint8_t> d_block;
+    struct NonOwning {
         uint8_t* ptr = nullptr;
         void release() { ptr = nullptr; }
-    } d_pass;
+    } d_raw, d_pass;
+    unsigned long long* counts_dev() { return reinterpret_cast<unsigned long long*>(d_block.ptr); }
+    uint32_t* counter32() { return reinterpret_cast<uint32_t*>(d_block.ptr); }
     // lhmm_scan: the kernel's results are copied to out_host right behind it
     // (one host round trip per scan) when nothing needs rescoring
     bool stage_out = false, staged = false;
@@ -521,7 +522,8 @@ int upload_db(lhmm_context* c) {
     if (int rc = c->d_tile_off.reserve(db.tile_off.size())) return rc;
     if (int rc = c->d_lens.reserve(db.lens.size())) return rc;
     if (int rc = c->d_out_idx.reserve(db.out_idx.size())) return rc;
-    if (int rc = c->d_raw.reserve(2 * std::max<uint64_t>(db.n_local, 1))) return rc;
+    if (int rc = c->d_block.reserve(32 + 2 * std::max<uint64_t>(db.n_local, 1))) return rc;
+    c->d_raw.ptr = c->d_block.ptr + 32;
     c->d_pass.ptr = c->d_raw.ptr + db.n_local;
     if (!c->host_resident)
         CUDA_TRY(cudaMemcpyAsync(c->d_db.ptr, db.data, db.data_bytes, cudaMemcpyHostToDevice,
@@ -589,14 +591,14 @@ bool page_locked(const void* p) {
 
 int outputs_to_host(lhmm_context* c, uint8_t* raw, uint8_t* pass, uint64_t n) {
     if (!n) return LHMM_OK;
-    if ((page_locked(raw) && page_locked(pass)) || !c->out_host.reserve(2 * n)) {
+    if ((page_locked(raw) && page_locked(pass)) || !c->out_host.reserve(32 + 2 * n)) {
         // caller's buffers are page-locked (direct DMA), or no staging area
         CUDA_TRY(cudaMemcpyAsync(raw, c->d_raw.ptr, n, cudaMemcpyDeviceToHost, c->stream));
         CUDA_TRY(cudaMemcpyAsync(pass, c->d_pass.ptr, n, cudaMemcpyDeviceToHost, c->stream));
         CUDA_TRY(cudaStreamSynchronize(c->stream));
         return LHMM_OK;
     }
-    uint8_t* h = c->out_host.ptr;
+    uint8_t* h = c->out_host.ptr + 32;  // the staging area mirrors d_block
     if (!c->staged) {
         CUDA_TRY(cudaMemcpyAsync(h, c->d_raw.ptr, 2 * n, cudaMemcpyDeviceToHost, c->stream));
         CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -796,8 +798,8 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         }
         lit = pf.lens.emplace(lkey, std::move(lt)).first;
     }
-    if (int rc = c->d_counts.reserve(4)) return rc;
-    CUDA_TRY(cudaMemsetAsync(c->d_counts.ptr, 0, 32, c->stream));
+    if (!c->d_block.ptr) return set_error(LHMM_ERR_CONTRACT, "no database set");
+    CUDA_TRY(cudaMemsetAsync(c->d_block.ptr, 0, 32, c->stream));
 
     lhmm::KParams p{};
     p.db = v.db;
@@ -825,7 +827,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     const bool track_modes = opt->alg == LHMM_MSV && !long_model &&
                              (variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16X_ALT ||
                               variant == LHMM_VARIANT_FP16XM || variant == LHMM_VARIANT_FP16XH);
-    if (track_modes) p.mode_rows = c->d_counts.ptr + 2;
+    if (track_modes) p.mode_rows = c->counts_dev() + 2;
     p.wrap = opt->reorder_mode == 1 ? 1u : 0u;
     const bool relaxed = ((variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16XM) &&
                           opt->alg == LHMM_SSV) ||
@@ -1030,16 +1032,18 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     // synchronised through ev_done
     CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
     if (!counts) return set_error(LHMM_ERR_NOMEM, "cannot allocate pinned counter words");
-    if (track_sat || relaxed || track_modes)
-        CUDA_TRY(cudaMemcpyAsync(counts, c->d_counts.ptr, 32, cudaMemcpyDeviceToHost, c->stream));
-    // lhmm_scan's results right behind the kernel (valid unless rescored)
+    // lhmm_scan: counters and results right behind the kernel in one copy
+    // (the results are final unless the scan rescores)
     const uint64_t nres = c->db.n_local;
     c->staged = false;
     if (c->stage_out && view == nullptr && !global_out && d_raw == c->d_raw.ptr &&
-        d_pass == c->d_pass.ptr && nres > 0 && c->out_host.reserve(2 * nres)) {
-        CUDA_TRY(cudaMemcpyAsync(c->out_host.ptr, c->d_raw.ptr, 2 * nres, cudaMemcpyDeviceToHost,
-                                 c->stream));
+        d_pass == c->d_pass.ptr && nres > 0 && c->out_host.reserve(32 + 2 * nres)) {
+        CUDA_TRY(cudaMemcpyAsync(c->out_host.ptr, c->d_block.ptr, 32 + 2 * nres,
+                                 cudaMemcpyDeviceToHost, c->stream));
         c->staged = true;
+        counts = reinterpret_cast<uint32_t*>(c->out_host.ptr);
+    } else if (track_sat || relaxed || track_modes) {
+        CUDA_TRY(cudaMemcpyAsync(counts, c->d_block.ptr, 32, cudaMemcpyDeviceToHost, c->stream));
     }
     if (!c->ev_done) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
     CUDA_TRY(cudaEventRecord(c->ev_done, c->stream));
@@ -1545,7 +1549,7 @@ int lhmm_context_destroy(lhmm_context* c) {
     c->d_flag.release();
     if (c->evr0) cudaEventDestroy(c->evr0);
     if (c->evr1) cudaEventDestroy(c->evr1);
-    c->d_counts.release();
+    c->d_block.release();
     c->d_raw.release();
     c->d_pass.release();
     cudaEventDestroy(c->ev0);
