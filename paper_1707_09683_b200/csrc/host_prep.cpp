@@ -282,9 +282,14 @@ static void strides_for(uint32_t L, uint32_t H, uint32_t& P, uint32_t& copies,
 
 // Table rows ("register rows" of the 16-byte-per-lane slots): the mixed
 // SSV table packs five rows per slot (lhmm_kernel.cuh Fp16Mixed).
-static uint32_t slot_rows(int variant, uint32_t H) {
-    return variant == LHMM_VARIANT_FP16XM || variant == LHMM_VARIANT_FP16XRM ? (H + 4u) / 5u * 4u
-                                                                             : H;
+// (alg < 0: the largest layout over both algorithms, for size checks; the
+// relaxed SSV table -- FP16XM SSV, FP16XRM -- has six-row slots at the bottom,
+// hybrid_layout.hpp xm_six_slots)
+static uint32_t slot_rows(int variant, uint32_t H, int alg = -1, uint32_t L = 0) {
+    if (variant == LHMM_VARIANT_FP16XRM) alg = LHMM_SSV;
+    if (variant != LHMM_VARIANT_FP16XM) return H;
+    if (alg == LHMM_SSV && L > 0) return uint32_t(4 * xm_slots(int(H), int(L)));
+    return (H + 4u) / 5u * 4u;
 }
 
 uint64_t table_bytes_for(int variant, uint32_t L, uint32_t H, bool replicate) {
@@ -406,22 +411,32 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
     }
     const uint32_t cpw = cells_per_word(variant);
     uint32_t P, copies, cs;
-    strides_for(L, slot_rows(variant, H), P, copies, cs);
+    strides_for(L, slot_rows(variant, H, alg, L), P, copies, cs);
     out.res_stride = P;
     out.copy_stride = copies > 1 ? cs : 0;
-    out.words.assign(table_bytes_for(variant, L, H, replicate) / 4, 0);
+    {
+        const uint64_t words = copies > 1 ? uint64_t(copies - 1) * cs + 23ull * P : 23ull * P;
+        out.words.assign((words * 4 + 15) / 16 * 4, 0);
+    }
     if (variant == LHMM_VARIANT_FP16XM) {
         // f16 subnormal domain (units of 2^-24): per lane and five-row group
         // one 16-byte slot = rows 5g..5g+2 as 16-bit pairs, then rows 5g+3,
         // 5g+4 as four bytes.  SSV (Fp16Mixed): signed subnormal dbias - cost,
         // bytes dbias - cost clamped to [-128, 127].  MSV (Fp16SatMixed, cells
         // negated): the cost itself, in both forms
+        // SSV (relaxed) tables start with A six-row slots: rows 6s, 6s+1 as
+        // f16 pairs, rows 6s+2..6s+5 as four signed-byte pairs
+        const uint32_t A = alg == LHMM_MSV ? 0u : uint32_t(xm_six_slots(int(H), int(L)));
+        const uint32_t nslots = alg == LHMM_MSV ? (H + 4) / 5 : uint32_t(xm_slots(int(H), int(L)));
         for (uint32_t x = 0; x < 23; ++x)
-            for (uint32_t hg = 0; hg < (H + 4) / 5; ++hg)
+            for (uint32_t hg = 0; hg < nslots; ++hg)
                 for (uint32_t oig = 0; oig < L; ++oig) {
                     uint32_t slot[4] = {0, 0, 0, 0};
-                    for (uint32_t k = 0; k < 5; ++k) {
-                        const uint32_t h = 5 * hg + k;
+                    const bool six = hg < A;
+                    const uint32_t hb = six ? 6 * hg : 6 * A + 5 * (hg - A);
+                    const uint32_t nf = six ? 2u : 3u;  // f16 words of the slot
+                    for (uint32_t k = 0; k < (six ? 6u : 5u); ++k) {
+                        const uint32_t h = hb + k;
                         for (uint32_t c = 0; c < 2; ++c) {
                             const uint64_t node = uint64_t(2 * oig + c) * H + h + 1;
                             const int cost = (h >= H || node > m || x > kUnknown)
@@ -435,12 +450,14 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
                                 continue;
                             }
                             const int t = int(dbias) - cost;
-                            if (k < 3) {
+                            if (k < nf) {
                                 const uint32_t f = t >= 0 ? uint32_t(t) : 0x8000u | uint32_t(-t);
                                 slot[k] |= f << (16 * c);
                             } else {
+                                // byte words: word nf + (k - nf) / 2, pair (k - nf) % 2
                                 const int b = t < -128 ? -128 : (t > 127 ? 127 : t);
-                                slot[3] |= (uint32_t(b) & 0xffu) << (8 * (2 * (k - 3) + c));
+                                const uint32_t kb = k - nf;
+                                slot[nf + kb / 2] |= (uint32_t(b) & 0xffu) << (8 * (2 * (kb % 2) + c));
                             }
                         }
                     }

@@ -40,4 +40,24 @@ LHMM_HD constexpr int hyb_slots(int H, int L) {
     return nm + rest / 4 + (rest % 4 ? 1 : 0);
 }
 
+// Six-row slots of the relaxed SSV mixed table (Fp16Mixed SSV and the
+// FP16XRM MSV form that shares it): a slot of two f16 words and four
+// signed-byte words (1.33 table bytes per cell) beside the five-row slots
+// (1.6 B/cell).  They trade table bandwidth (the C2 bound) for byte unpacks
+// and integer adds on the ALU, which pays only where it removes a slot:
+// H = 5k + 3 from 48 up becomes three six-row slots + k - 3 five-row slots,
+// all full (no three-row top slot: one LDS.128 fewer per row), measured
+// +3.4% at L8 H63; where the slot count stays (H = 5k, e.g. L4 H50: -3%) and
+// at L = 32 (ALU-bound by the row shuffles: -0.6% at H38) there are none.
+LHMM_HD constexpr int xm_six_slots(int H, int L) {
+    return (L < 32 && H >= 48 && H % 5 == 3) ? 3 : 0;
+}
+
+// slots per lane of a relaxed SSV mixed table with H rows
+LHMM_HD constexpr int xm_slots(int H, int L) {
+    const int a = xm_six_slots(H, L);
+    const int h5 = H - 6 * a;
+    return a + h5 / 5 + (h5 % 5 ? 1 : 0);
+}
+
 }  // namespace lhmm

@@ -442,6 +442,7 @@ struct Fp16Mixed {
     static_assert(ALG == 1, "the mixed-table form is an SSV form of FP16X");
     static constexpr int CPW = 2;
     static constexpr int kGroup = 5;  // words per 16-byte table slot
+    static constexpr bool kSix = true;  // six-row slots at the bottom (xm_six_slots)
     static constexpr bool kMsv = false;
     static constexpr bool kRelaxed = true;
     static constexpr bool kTwoMode = false;
@@ -575,6 +576,7 @@ struct Fp16FixedBMixed {
     static_assert(ALG == 0, "the fixed-B relaxed form (FP16XRM) is MSV only");
     static constexpr int CPW = 2;
     static constexpr int kGroup = 5;
+    static constexpr bool kSix = true;  // the relaxed SSV table layout
     static constexpr bool kMsv = false;     // row structure: no per-row reduction
     static constexpr bool kMsvAlg = true;   // MSV scores (saturation feedback)
     static constexpr bool kRelaxed = true;
@@ -903,6 +905,16 @@ template <class V>
 struct is_hybrid<V, decltype(void(V::kHybrid))> {
     static constexpr bool value = V::kHybrid;
 };
+// Policies on the relaxed SSV mixed table with six-row slots (kSix).
+template <class V, class = void>
+struct six_rows {
+    static constexpr bool value = false;
+};
+template <class V>
+struct six_rows<V, decltype(void(V::kSix))> {
+    static constexpr bool value = V::kSix;
+};
+
 // Policies whose raw score needs per-sequence state (FP16XRM: E_u + base).
 template <class V, class = void>
 struct has_raw_of {
@@ -1063,40 +1075,46 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                     }
                 }
             } else if constexpr (GW == 5) {
-                // mixed tables (Fp16Mixed, Fp16SatMixed): five words per
-                // 16-byte slot, three 16-bit-pair words and one word of four
-                // bytes; with H = 5k + r (r <= 3) a top slot of r 16-bit-pair
-                // words
-                constexpr int RT = H % 5;
+                // mixed tables (Fp16Mixed, Fp16SatMixed, Fp16FixedBMixed):
+                // five words per 16-byte slot, three 16-bit-pair words and
+                // one word of four bytes; with H - 6A = 5k + r (r <= 3) a top
+                // slot of r 16-bit-pair words.  The relaxed SSV table (kSix)
+                // starts with A six-row slots (two 16-bit-pair words, two
+                // words of four bytes; hybrid_layout.hpp xm_six_slots)
+                constexpr int A = six_rows<V>::value ? xm_six_slots(H, L) : 0;
+                constexpr int B6 = 6 * A;          // first row of the five-row part
+                constexpr int NG = (H - B6) / 5;   // five-row slots
+                constexpr int RT = (H - B6) % 5;
                 static_assert(RT <= 3, "a partial mixed-table group holds at most three rows");
                 if constexpr (RT > 0) {
-                    constexpr int hg = H / 5;
-                    const uint4 c = *reinterpret_cast<const uint4*>(tp + hg * 4 * TL);
+                    constexpr int hb = B6 + 5 * NG;
+                    const uint4 c = *reinterpret_cast<const uint4*>(tp + (A + NG) * 4 * TL);
                     const uint32_t cw[3] = {c.x, c.y, c.z};
 #pragma unroll
                     for (int k = RT - 1; k >= 0; --k) {
-                        const int h = 5 * hg + k;
+                        const int h = hb + k;
                         const int sl = ((h - 1 - r) % H + H) % H;
                         const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
                         g[sl] = V::template cell<LAZY, false, 0>(in, cw[k], st);
                     }
                     if constexpr (!V::kMsv) {
-                        const int t0 = ((5 * hg - 1 - r) % H + H) % H;
-                        const int t1 = ((5 * hg + (RT > 1 ? 1 : 0) - 1 - r) % H + H) % H;
+                        const int t0 = ((hb - 1 - r) % H + H) % H;
+                        const int t1 = ((hb + (RT > 1 ? 1 : 0) - 1 - r) % H + H) % H;
                         e3 = V::acc2(e3, g[t0], g[t1]);
                         if constexpr (RT == 3) {
-                            const int t2 = ((5 * hg + 1 - r) % H + H) % H;
+                            const int t2 = ((hb + 1 - r) % H + H) % H;
                             e2 = V::acc2(e2, g[t2], g[t2]);
                         }
                     }
                 }
 #pragma unroll
-                for (int hg = H / 5 - 1; hg >= 0; --hg) {
-                    const uint4 c = *reinterpret_cast<const uint4*>(tp + hg * 4 * TL);
+                for (int hg = NG - 1; hg >= 0; --hg) {
+                    const int hb = B6 + 5 * hg;
+                    const uint4 c = *reinterpret_cast<const uint4*>(tp + (A + hg) * 4 * TL);
                     const uint32_t cw[5] = {c.x, c.y, c.z, V::unpack(c.w, 0), V::unpack(c.w, 1)};
 #pragma unroll
                     for (int k = 4; k >= 0; --k) {
-                        const int h = 5 * hg + k;
+                        const int h = hb + k;
                         const int sl = ((h - 1 - r) % H + H) % H;
                         const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
                         if (k >= 3)
@@ -1109,22 +1127,52 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                     // the fifth words of two groups share a third fold (the
                     // upper group's word keeps its value for the rest of
                     // the row)
-                    const int s0 = ((5 * hg - 1 - r) % H + H) % H;
-                    const int s1 = ((5 * hg - r) % H + H) % H;
-                    const int s2 = ((5 * hg + 1 - r) % H + H) % H;
-                    const int s3 = ((5 * hg + 2 - r) % H + H) % H;
-                    const int s4 = ((5 * hg + 3 - r) % H + H) % H;
+                    const int s0 = ((hb - 1 - r) % H + H) % H;
+                    const int s1 = ((hb - r) % H + H) % H;
+                    const int s2 = ((hb + 1 - r) % H + H) % H;
+                    const int s3 = ((hb + 2 - r) % H + H) % H;
+                    const int s4 = ((hb + 3 - r) % H + H) % H;
                     uint32_t* acc[4] = {&e0, &e1, &e2, &e3};
                     *acc[(2 * hg) % 4] = V::acc2(*acc[(2 * hg) % 4], g[s0], g[s1]);
                     *acc[(2 * hg + 1) % 4] = V::acc2(*acc[(2 * hg + 1) % 4], g[s2], g[s3]);
-                    constexpr int NG = H / 5;
                     if ((NG - 1 - hg) % 2 == 1) {
                         // pair with the fifth word of group hg + 1
-                        const int s4u = ((5 * hg + 8 - r) % H + H) % H;
+                        const int s4u = ((hb + 8 - r) % H + H) % H;
                         *acc[(hg + 2) % 4] = V::acc2(*acc[(hg + 2) % 4], g[s4], g[s4u]);
                     } else if (hg == 0) {
                         *acc[2] = V::acc2(*acc[2], g[s4], g[s4]);  // odd group count
                     }
+                    }
+                }
+                if constexpr (A > 0) {
+#pragma unroll
+                    for (int hs = A - 1; hs >= 0; --hs) {
+                        const int hb = 6 * hs;
+                        const uint4 c = *reinterpret_cast<const uint4*>(tp + hs * 4 * TL);
+                        const uint32_t cw[6] = {c.x, c.y, V::unpack(c.z, 0), V::unpack(c.z, 1),
+                                                V::unpack(c.w, 0), V::unpack(c.w, 1)};
+#pragma unroll
+                        for (int k = 5; k >= 0; --k) {
+                            const int h = hb + k;
+                            const int sl = ((h - 1 - r) % H + H) % H;
+                            const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
+                            if (k >= 2)
+                                g[sl] = V::template cell<LAZY, false, 3>(in, cw[k], st);
+                            else
+                                g[sl] = V::template cell<LAZY, false, 0>(in, cw[k], st);
+                        }
+                        // E: three folds per six-row slot (SSV-shaped rows)
+                        static_assert(!V::kMsv, "six-row slots belong to the relaxed SSV table");
+                        const int s0 = ((hb - 1 - r) % H + H) % H;
+                        const int s1 = ((hb - r) % H + H) % H;
+                        const int s2 = ((hb + 1 - r) % H + H) % H;
+                        const int s3 = ((hb + 2 - r) % H + H) % H;
+                        const int s4 = ((hb + 3 - r) % H + H) % H;
+                        const int s5 = ((hb + 4 - r) % H + H) % H;
+                        uint32_t* acc[4] = {&e0, &e1, &e2, &e3};
+                        *acc[(3 * hs + 1) % 4] = V::acc2(*acc[(3 * hs + 1) % 4], g[s0], g[s1]);
+                        *acc[(3 * hs + 2) % 4] = V::acc2(*acc[(3 * hs + 2) % 4], g[s2], g[s3]);
+                        *acc[(3 * hs + 3) % 4] = V::acc2(*acc[(3 * hs + 3) % 4], g[s4], g[s5]);
                     }
                 }
             } else {
