@@ -164,11 +164,21 @@ struct Flat {
     std::vector<Proto> protos;
     uint64_t residue_count = 0;
 
+    // compact per-sequence lengths and the distinct lengths seen (for the
+    // per-length finalize terms), gathered while flattening
+    std::vector<uint64_t> lens;
+    std::vector<uint8_t> len_seen;
+    uint64_t max_len = 0;
+
     void add(const uint8_t* s, uint64_t n, Proto p) {
         residues.insert(residues.end(), s, s + n);
         offsets.push_back(residues.size());
         residue_count += n;
         protos.push_back(std::move(p));
+        lens.push_back(n);
+        if (n >= len_seen.size()) len_seen.resize(std::max<uint64_t>(n + 1, 2 * len_seen.size()), 0);
+        len_seen[n] = 1;
+        max_len = std::max(max_len, n);
     }
 };
 
@@ -307,16 +317,12 @@ DeviceScan device_scan(const CostMatrix& costs, Flat& flat, const QuantParams& q
     o.fault_injection = fault ? 1 : 0;
     o.reorder_mode = wrap ? 1 : 0;
     lhmm_scan_stats st{};
-    std::vector<double> len_corr, move;
+    // finalize_hit's length terms (log2 length correction, move cost), once
+    // per distinct length, on a helper thread while a large scan runs
+    std::vector<double> len_corr(flat.max_len + 1, 0.0), move(flat.max_len + 1, 0.0);
     auto length_terms = [&] {
-        uint64_t max_len = 0;
-        for (const Proto& p : flat.protos) max_len = std::max(max_len, p.len);
-        len_corr.assign(max_len + 1, 0.0);
-        move.assign(max_len + 1, 0.0);
-        std::vector<uint8_t> seen(max_len + 1, 0);
-        for (const Proto& p : flat.protos) seen[p.len] = 1;
-        for (uint64_t L = 0; L <= max_len; ++L)
-            if (seen[L]) {
+        for (uint64_t L = 0; L <= flat.max_len; ++L)
+            if (flat.len_seen[L]) {
                 len_corr[L] = std::log2((double(L) + 3.0) / 3.0);
                 move[L] = double(lhmm_move_cost(L, &lq));
             }
@@ -328,8 +334,14 @@ DeviceScan device_scan(const CostMatrix& costs, Flat& flat, const QuantParams& q
     std::thread container;
     if (n > 65536) container = std::thread([&] { ds.hits.resize(n); });
     const auto t1 = std::chrono::steady_clock::now();
+    // (small sets: inline -- a thread start costs more than the terms)
+    std::thread terms;
+    if (n > 65536) terms = std::thread(length_terms);
     int scan_rc = lhmm_scan(c, &o, raw.data(), pass.data(), &st);
-    length_terms();
+    if (terms.joinable())
+        terms.join();
+    else
+        length_terms();
     const auto t2 = std::chrono::steady_clock::now();
     lk.unlock();
     if (scan_rc != LHMM_OK) {
@@ -347,10 +359,10 @@ DeviceScan device_scan(const CostMatrix& costs, Flat& flat, const QuantParams& q
     const bool msv = alg == Algorithm::Msv;
 #pragma omp parallel for schedule(static) num_threads(std::max(1, workers)) if (n > 1024)
     for (int64_t i = 0; i < int64_t(n); ++i) {
-        const Proto& p = flat.protos[size_t(i)];
+        const uint64_t len = flat.lens[size_t(i)];
         const uint8_t r = raw[size_t(i)];
-        const double b = msv ? (double(r) - double(q.base) + move[p.len]) / q.scale - len_corr[p.len]
-                             : (double(r) - 128.0) / q.scale - len_corr[p.len];
+        const double b = msv ? (double(r) - double(q.base) + move[len]) / q.scale - len_corr[len]
+                             : (double(r) - 128.0) / q.scale - len_corr[len];
         fin[size_t(i)] = Final{b, r == 0xff ? 0.0 : std::min(1.0, std::exp(-lambda * (b - tau)))};
     }
     const auto t3 = std::chrono::steady_clock::now();
