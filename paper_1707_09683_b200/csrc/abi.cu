@@ -605,7 +605,10 @@ int outputs_to_host(lhmm_context* c, uint8_t* raw, uint8_t* pass, uint64_t n) {
     }
     constexpr uint64_t kChunk = 1 << 18;
     const int64_t chunks = int64_t((2 * n + kChunk - 1) / kChunk);
-#pragma omp parallel for schedule(static) if (chunks > 1)
+    // a few threads saturate the copy; a machine-wide team would stall at its
+    // barrier whenever the caller's own threads preempt a member
+    const int team = int(std::min<int64_t>(chunks, 4));
+#pragma omp parallel for schedule(static) num_threads(team) if (chunks > 1)
     for (int64_t k = 0; k < chunks; ++k) {
         const uint64_t a = uint64_t(k) * kChunk, b = std::min<uint64_t>(2 * n, a + kChunk);
         // [a, b) of raw|pass, split at the boundary

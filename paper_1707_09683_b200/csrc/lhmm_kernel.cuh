@@ -227,7 +227,7 @@ struct Dpx16 {
         s.ntj2 = (0u - p.tecjb) & 0xffffu;
         s.ntj2 |= s.ntj2 << 16;
     }
-    template <bool LAZY = false, bool FPW = false>
+    template <bool LAZY = false, bool FPW = false, int FORM = 0>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
         if constexpr (kMsv) {
             uint32_t y = __viaddmin_u16x2(__vmaxu2(x, s.B), s.d2, 0x00ff00ffu);
@@ -292,7 +292,7 @@ struct Fp16 {
         }
         s.B = s.base2;
     }
-    template <bool LAZY = false, bool FPW = false>
+    template <bool LAZY = false, bool FPW = false, int FORM = 0>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
         if constexpr (kMsv) {
             const uint32_t m = __vmaxu2(x, s.B);
@@ -346,7 +346,7 @@ struct Swar8 {
         s.d4 = p.dbias * 0x01010101u;
         s.tj4 = (p.tecjb > 255u ? 255u : p.tecjb) * 0x01010101u;
     }
-    template <bool LAZY = false, bool FPW = false>
+    template <bool LAZY = false, bool FPW = false, int FORM = 0>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
         if constexpr (kMsv) {
             return __vsubus4(__vaddus4(__vmaxu4(x, s.B), s.d4), c);
@@ -400,7 +400,7 @@ struct Fp16Relaxed {
     __device__ static __forceinline__ uint32_t init_word(const St&) { return 0u; }
     template <bool LAZY = false>
     __device__ static __forceinline__ uint32_t inject(const St&) { return 0u; }
-    template <bool LAZY = false, bool FPW = false>
+    template <bool LAZY = false, bool FPW = false, int FORM = 0>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St&) {
         return as_u32(__hadd2_sat(as_h2(x), as_h2(c)));
     }
@@ -530,7 +530,7 @@ struct Fp16RelaxedMsv {
     __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
     template <bool LAZY = false>
     __device__ static __forceinline__ uint32_t inject(const St&) { return NEG; }
-    template <bool LAZY = false, bool FPW = false>
+    template <bool LAZY = false, bool FPW = false, int FORM = 0>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
         return as_u32(__hadd2_sat(as_h2(__vmaxu2(x, s.B)), as_h2(c)));
     }
@@ -701,6 +701,27 @@ struct Fp16SatMixed {
     __device__ static __forceinline__ bool needs_exact(uint32_t, const St&) { return false; }
 };
 
+// Relu form of the two-mode exact step (linear-binade cells, patterns
+// 0x3B01 + v in [0.8755, 1]):  max(x, B) (+) dbias = sat(relu(x - B) + (B + d)).
+// x - B is a multiple of 2^-11 below 1/8 in magnitude (exact), sub.sat
+// clamps it at 0; B + d is exact up to 1, and above 1 it rounds to >= 1, where
+// the final clamp at 1.0 gives the same byte 255 as the exact sum would.  Two
+// FP16-pipe ops replace HMNMX2 (ALU) + HADD2.SAT; B + d is one HADD2 per row.
+__device__ __forceinline__ uint32_t relu_bias(uint32_t B, uint32_t d1) {
+    return as_u32(__hadd2(as_h2(B), as_h2(d1)));
+}
+__device__ __forceinline__ uint32_t relu_step(uint32_t x, uint32_t B, uint32_t Bd1) {
+    const uint32_t r = as_u32(__hsub2_sat(as_h2(x), as_h2(B)));
+    return as_u32(__hadd2_sat(as_h2(r), as_h2(Bd1)));
+}
+
+// Which words of a four-word group take the relu form in the two-mode exact
+// mode (bit k of LHMM_RELU_MASK: word k): half of them balances the ALU
+// (HMNMX2 + VIADDMNMX + E fold) against the FP16 pipe.
+#ifndef LHMM_RELU_MASK
+#define LHMM_RELU_MASK 0xA
+#endif
+
 // FP16XH, MSV ("hybrid"): the exact mode of Fp16Sat (linear-binade cells,
 // 16-bit table, four-row groups) and the lazy mode of Fp16SatMixed (negated
 // subnormal cells, mixed table, five-row groups), both tables resident in
@@ -715,12 +736,14 @@ struct Fp16SatHybrid {
     static constexpr bool kRelaxed = false;
     static constexpr bool kTwoMode = true;
     static constexpr bool kHybrid = true;
+    static constexpr bool kRelu = true;  // exact rows: relu form (relu_word)
     static constexpr int kFpEvery = 0;
     static constexpr uint32_t kByte0 = 0x3B013B01u;
     static constexpr uint32_t NEG = kByte0;
     struct St {
         uint32_t B, base2, d1, ntj2;  // exact mode (patterns 0x3B01 + v)
         uint32_t nd;                  // lazy mode: -dbias as a subnormal f16
+        uint32_t Bd1;                 // exact mode: B (+) dbias (relu form)
     };
     __device__ static __forceinline__ void init(St& s, uint32_t base, const KParams& p) {
         s.base2 = (0x3B01u + base) * 0x00010001u;
@@ -729,6 +752,7 @@ struct Fp16SatHybrid {
         s.ntj2 = (0u - p.tecjb) & 0xffffu;
         s.ntj2 |= s.ntj2 << 16;
         s.nd = (0x8000u | p.dbias) * 0x00010001u;
+        s.Bd1 = relu_bias(s.B, s.d1);
     }
     __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
     // lazy mode: B holds nB (enter_lazy)
@@ -739,6 +763,8 @@ struct Fp16SatHybrid {
         if constexpr (LAZY) {
             const uint32_t pp = as_u32(__hadd2_sat(as_h2(x), as_h2(s.nd)));
             return __viaddmin_s16x2(pp, c, s.B);
+        } else if constexpr (FORM == 1) {
+            return __viaddmax_s16x2(relu_step(x, s.B, s.Bd1), c, kByte0);
         } else {
             const uint32_t m = as_u32(__hmax2(as_h2(x), as_h2(s.B)));
             const uint32_t pp = as_u32(__hadd2_sat(as_h2(m), as_h2(s.d1)));
@@ -761,6 +787,7 @@ struct Fp16SatHybrid {
     }
     __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
         s.B = __viaddmax_s16x2(e, s.ntj2, s.base2);
+        s.Bd1 = relu_bias(s.B, s.d1);
     }
     __device__ static __forceinline__ bool saturated(uint32_t e) {
         return (e & 0xffffu) == 0x3C00u;
@@ -803,9 +830,13 @@ struct Fp16Sat {
     // FPE = 4 (FP16X_ALT): one word in four (h % 4 == 3 of full row groups)
     // uses the FP16 form; FPE = 0 (FP16X): none
     static constexpr int kFpEvery = FPE;
+    // exact rows: relu form (relu_word); not with the FP16 cost words of
+    // FP16X_ALT, whose FP16 pipe they already load (M = 100: -4.8% with both)
+    static constexpr bool kRelu = FPE == 0;
     static constexpr uint32_t NEG = kByte0;
     struct St {
         uint32_t B, base2, d1, ntj2;
+        uint32_t Bd1;  // B (+) dbias, for the relu form of the exact step
     };
     __device__ static __forceinline__ void init(St& s, uint32_t base, const KParams& p) {
         s.base2 = (0x3B01u + base) * 0x00010001u;
@@ -813,18 +844,25 @@ struct Fp16Sat {
         s.d1 = as_u32(__float2half2_rn(float(p.dbias) / 2048.f));
         s.ntj2 = (0u - p.tecjb) & 0xffffu;
         s.ntj2 |= s.ntj2 << 16;
+        s.Bd1 = relu_bias(s.B, s.d1);
     }
     __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
     template <bool LAZY = false>
     __device__ static __forceinline__ uint32_t inject(const St& s) { return LAZY ? s.B : NEG; }
-    template <bool LAZY = false, bool FPW = false>
+    template <bool LAZY = false, bool FPW = false, int FORM = 0>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
         // FPW words (every kFpEvery-th row of a group, see kFpEvery) take
         // their cost as the f16 value -cost/2048 and subtract / clamp on the
-        // FP16 pipe instead of the ALU: that balances the two pipes
-        const uint32_t m =
-            LAZY ? x : as_u32(__hmax2(as_h2(x), as_h2(s.B)));
-        const uint32_t pp = as_u32(__hadd2_sat(as_h2(m), as_h2(s.d1)));
+        // FP16 pipe instead of the ALU: that balances the two pipes.
+        // FORM = 1 (exact mode): max(x, B) (+) dbias as relu(x - B) (+) Bd1,
+        // two FP16 ops instead of HMNMX2 (ALU) + HADD2 (relu_step)
+        uint32_t pp;
+        if constexpr (!LAZY && FORM == 1) {
+            pp = relu_step(x, s.B, s.Bd1);
+        } else {
+            const uint32_t m = LAZY ? x : as_u32(__hmax2(as_h2(x), as_h2(s.B)));
+            pp = as_u32(__hadd2_sat(as_h2(m), as_h2(s.d1)));
+        }
         const uint32_t floor = LAZY ? s.B : kByte0;
         if constexpr (FPW) {
             return as_u32(__hmax2(__hadd2(as_h2(pp), as_h2(c)), as_h2(floor)));
@@ -845,6 +883,7 @@ struct Fp16Sat {
     }
     __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
         s.B = __viaddmax_s16x2(e, s.ntj2, s.base2);  // max(E - (tec+tjb), base)
+        s.Bd1 = relu_bias(s.B, s.d1);
     }
     __device__ static __forceinline__ bool saturated(uint32_t e) {
         return (e & 0xffffu) == 0x3C00u;
@@ -954,6 +993,25 @@ __host__ __device__ constexpr bool fp_word(int k, bool full) {
     }
 }
 
+// Whether word k of a four-word group takes the relu form (two-mode exact
+// mode on the linear-binade cells: Fp16Sat, Fp16SatHybrid).
+template <class V, class = void>
+struct has_relu {
+    static constexpr bool value = false;
+};
+template <class V>
+struct has_relu<V, decltype(void(V::kRelu))> {
+    static constexpr bool value = V::kRelu;
+};
+template <class V, bool LAZY>
+__host__ __device__ constexpr bool relu_word(int k) {
+    if constexpr (has_relu<V>::value && !LAZY) {
+        return ((LHMM_RELU_MASK >> k) & 1) != 0;
+    } else {
+        return false;
+    }
+}
+
 // One chunk of RPI residue rows (fully unrolled).  Returns true when the
 // sub-batch's rows ended inside the chunk.  LAZY (two-mode MSV only): the
 // cells hold max(v, B) and B is constant -- see Fp16Sat.
@@ -963,16 +1021,30 @@ __device__ __forceinline__ void group_barrier(uint32_t id, uint32_t threads) {
 
 // The residue codes of one chunk (RPI rows; bytes 4q..4q+3 of word q are
 // rows r0+4q..r0+4q+3), loaded one chunk ahead so the HBM latency of the
-// residue stream hides behind a chunk of DP work.
+// residue stream hides behind a chunk of DP work.  A lane's rows come in
+// 16-byte blocks (16 rows, database layout in pack_database); with
+// LHMM_RES128 every block is read by one 128-bit load (LDG.E.EF.128) also
+// when the body runs 8- or 4-row chunks: `v` then holds the block of the
+// current chunk, and the next block is loaded during the block's last chunk.
+#ifndef LHMM_RES128
+#define LHMM_RES128 0
+#endif
 template <int RPI>
 struct ResChunk {
+#if LHMM_RES128
+    uint4 v;
+#else
     uint32_t w[RPI / 4];
+#endif
 };
 
 template <int RPI>
 __device__ __forceinline__ ResChunk<RPI> load_res(const uint8_t* src, uint32_t r0) {
     ResChunk<RPI> c;
     const uint8_t* chunk = src + (r0 >> 4) * 512u;
+#if LHMM_RES128
+    c.v = ld_stream(chunk);
+#else
     if constexpr (RPI == 16) {
         const uint4 v = ld_stream(chunk);
         c.w[0] = v.x;
@@ -986,8 +1058,26 @@ __device__ __forceinline__ ResChunk<RPI> load_res(const uint8_t* src, uint32_t r
     } else {
         c.w[0] = __ldcs(reinterpret_cast<const unsigned int*>(chunk + (r0 & 12u)));
     }
+#endif
     return c;
 }
+
+#if LHMM_RES128
+// Word q of the chunk starting at row r0 (RPI < 16: a runtime pick inside
+// the 16-row block; one or two SEL per chunk).
+template <int RPI>
+__device__ __forceinline__ uint32_t res_word(const uint4& v, uint32_t r0, int q) {
+    static_assert(RPI < 16, "a 16-row chunk is its block");
+    if constexpr (RPI == 8) {
+        const bool hi = (r0 & 8u) != 0u;
+        return q == 0 ? (hi ? v.z : v.x) : (hi ? v.w : v.y);
+    } else {
+        const uint32_t k = (r0 >> 2) & 3u;
+        const uint32_t lo = (k & 1u) ? v.y : v.x, up = (k & 1u) ? v.w : v.z;
+        return (k & 2u) ? up : lo;
+    }
+}
+#endif
 
 // Long models (K > 1, see scan_kernel_long): the K warps of a group hold
 // one sequence (TL = 32K table lanes); lane 0 of each warp takes its stripe
@@ -1004,16 +1094,36 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                                           uint32_t* xch = nullptr, uint32_t wig = 0,
                                           uint32_t bar = 0, uint32_t* xin = nullptr) {
     static_assert(K == 1 || (L == 32 && !LAZY), "multi-warp groups use whole warps, exact mode");
+#if LHMM_RES128
+    // `pre` holds this chunk's 16-row block.  RPI = 16: the block is this
+    // chunk, and the next one is loaded at once; RPI < 16: the next block is
+    // loaded once the block's last word is picked (4 rows ahead)
+    uint32_t w16[4] = {pre.v.x, pre.v.y, pre.v.z, pre.v.w};
+    if (RPI == 16 && r0 + RPI < rows) pre = load_res<RPI>(src, r0 + RPI);
+    uint32_t wq = 0;
+#else
     const ResChunk<RPI> cur = pre;  // this chunk's residues, loaded one chunk ago
     if (r0 + RPI < rows) pre = load_res<RPI>(src, r0 + RPI);
     const uint32_t* wds = cur.w;
+#endif
 #pragma unroll
     for (int q = 0; q < RPI / 4; ++q) {
         if (r0 + 4u * q >= rows) return true;  // warp-uniform
+#if LHMM_RES128
+        if constexpr (RPI == 16) {
+            wq = w16[q];
+        } else {
+            wq = res_word<RPI>(pre.v, r0, q);
+            if (q == RPI / 4 - 1 && ((r0 + RPI) & 15u) == 0u && r0 + RPI < rows)
+                pre = load_res<RPI>(src, r0 + RPI);
+        }
+#else
+        const uint32_t wq = wds[q];
+#endif
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const int r = 4 * q + b;
-            const uint32_t x = (wds[q] >> (8 * b)) & 0xffu;
+            const uint32_t x = (wq >> (8 * b)) & 0xffu;
             const uint32_t* tp = tab_lane + x * P;
             // the register holding cell H-1 becomes cell 0 (stripe shift)
             const int stop = ((H - 1 - r) % H + H) % H;
@@ -1203,9 +1313,13 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                     const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
                     // (the condition folds away once the loops are unrolled)
                     if (fp_word<V>(k, full))
-                        g[sl] = V::template cell<LAZY, true>(in, cw[k], st);
+                        g[sl] = relu_word<V, LAZY>(k)
+                                    ? V::template cell<LAZY, true, 1>(in, cw[k], st)
+                                    : V::template cell<LAZY, true, 0>(in, cw[k], st);
                     else
-                        g[sl] = V::template cell<LAZY, false>(in, cw[k], st);
+                        g[sl] = relu_word<V, LAZY>(k)
+                                    ? V::template cell<LAZY, false, 1>(in, cw[k], st)
+                                    : V::template cell<LAZY, false, 0>(in, cw[k], st);
                 }
                 if constexpr (!V::kMsv) {
                     // SSV: fold the new words into E right away so the ALU

@@ -354,10 +354,17 @@ DeviceScan device_scan(const CostMatrix& costs, Flat& flat, const QuantParams& q
     struct Final {
         double bits, p;
     };
-    // (uninitialised: first touched by the parallel loop)
-    std::unique_ptr<Final[]> fin(new Final[n]);
+    // (a per-thread buffer reused across calls: no first-touch page faults in
+    // the timed window)
+    thread_local std::vector<Final> fin_buf;
+    if (fin_buf.size() < n) fin_buf.resize(n);
+    Final* fin = fin_buf.data();
     const bool msv = alg == Algorithm::Msv;
-#pragma omp parallel for schedule(static) num_threads(std::max(1, workers)) if (n > 1024)
+    // one core stays free for the container thread: an OpenMP team as wide as
+    // the machine would wait at its barrier for a preempted member (ms stalls)
+    const int hw = int(std::max(2u, std::thread::hardware_concurrency()));
+    const int team = std::max(1, std::min(workers, container.joinable() ? hw - 1 : hw));
+#pragma omp parallel for schedule(static) num_threads(team) if (n > 1024)
     for (int64_t i = 0; i < int64_t(n); ++i) {
         const uint64_t len = flat.lens[size_t(i)];
         const uint8_t r = raw[size_t(i)];

@@ -35,3 +35,24 @@ def test_build_flags_have_no_fast_math():
     from paper_1707_09683_b200 import build as B
     flags = " ".join(B.COMMON + B.ARCH)
     assert "fast_math" not in flags and "ftz=true" not in flags
+
+
+def test_relu_form_of_the_exact_step_is_exact():
+    """The two-mode exact step's relu form (lhmm_kernel.cuh relu_step):
+    sat(max(x, B) + d) == sat(sat(x - B) + (B + d)) in f16 round-to-nearest,
+    for every pair of linear-binade cells x, B (patterns 0x3B01 + v) and
+    every dbias (d = dbias / 2048) -- exhaustive, 256 x 256 x 256."""
+    import numpy as np
+    f = (0x3B01 + np.arange(256, dtype=np.uint16)).astype(np.uint16).view(np.float16)
+    X, Bv = f[:, None].astype(np.float32), f[None, :].astype(np.float32)
+
+    def sat(a):  # one f16 op: exact f32 sum, one rounding, clamp to [0, 1]
+        return np.clip(a.astype(np.float16), np.float16(0), np.float16(1))
+
+    r = sat(X - Bv).astype(np.float32)
+    for dbias in range(256):
+        d = np.float32(np.float16(dbias / 2048))
+        ref = sat(np.maximum(X, Bv) + d)
+        bd = (Bv + d).astype(np.float16).astype(np.float32)  # HADD2, no clamp
+        new = sat(r + bd)
+        assert np.array_equal(ref.view(np.uint16), new.view(np.uint16)), dbias
