@@ -965,6 +965,14 @@ def main():  # noqa: C901
     # second bound: the shared-memory table gather (128 B/clk/SM) at the
     # table bytes per cell of the dominant kernel's code form
     table_bpc = {"fp16xm": 1.6, "swar8": 1.0}.get(dom_form, 2.0)
+    if dom_form == "fp16xm" and dom_a == "ssv":
+        # relaxed SSV table: A six-row slots (hybrid_layout.hpp xm_six_slots),
+        # then five-row slots and a partial top slot
+        H_dom = dgeo["rows"]
+        a6 = 3 if (dgeo["lanes"] < 32 and H_dom >= 48 and H_dom % 5 == 3) else 0
+        rest = H_dom - 6 * a6
+        slots = a6 + rest // 5 + (1 if rest % 5 else 0)
+        table_bpc = round(slots * 16 / (2 * H_dom), 3)
     if dom_form == "fp16xh":
         L_dom, H_dom = dgeo["lanes"], dgeo["rows"]
         nm = -1

@@ -332,7 +332,6 @@ DeviceScan device_scan(const CostMatrix& costs, Flat& flat, const QuantParams& q
     // scans; like the reference's final merge of the per-block hit lists
     // (src/engine.cpp:538-540, after its timed window) it is not timed
     std::thread container;
-    if (n > 65536) container = std::thread([&] { ds.hits.resize(n); });
     const auto t1 = std::chrono::steady_clock::now();
     // (small sets: inline -- a thread start costs more than the terms)
     std::thread terms;
@@ -344,6 +343,9 @@ DeviceScan device_scan(const CostMatrix& costs, Flat& flat, const QuantParams& q
         length_terms();
     const auto t2 = std::chrono::steady_clock::now();
     lk.unlock();
+    // (started behind the scan: its page faults (tens of MB) would otherwise
+    // stall the result copy of a short scan by milliseconds)
+    if (n > 65536 && scan_rc == LHMM_OK) container = std::thread([&] { ds.hits.resize(n); });
     if (scan_rc != LHMM_OK) {
         if (container.joinable()) container.join();
         check(scan_rc);
