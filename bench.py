@@ -157,6 +157,28 @@ class ReferenceGen:
         return self.ref.quantize(scores, self.oracle.QuantParams(*q))
 
 
+def instruction_bound(form, alg, L, H, m, n_sm, sm_mhz):
+    """Issue-side bound of the relaxed SSV kernel (FP16XM), from its per-row
+    op counts (SASS of the loop body; DESIGN.md §5 instruction budget): per
+    warp and residue row, ALU ops = 2 per byte word (PRMT + VIADDMNMX) +
+    ceil(H/2) E folds (VIMNMX3) + 3, at 2 warp-ops/clk/SM (every op 0.5/clk/SMSP,
+    profiles/r2_pipe_probe.txt); shared-memory wavefronts = 4 per 16-byte slot
+    at 1/clk/SM.  Returned in algorithmic GCUPS (M of the 2LH computed cells)."""
+    if form != "fp16xm" or alg != "ssv":
+        return None
+    a6 = 3 if (L < 32 and H >= 48 and H % 5 == 3) else 0
+    rest = H - 6 * a6
+    slots = a6 + rest // 5 + (1 if rest % 5 else 0)
+    byte_words = 4 * a6 + 2 * (rest // 5)
+    alu = 2 * byte_words + (H + 1) // 2 + 3
+    clk = max(alu / 2.0, 4.0 * slots)
+    cells = 32 * 2 * H * (m / (2.0 * L * H))
+    peak = n_sm * sm_mhz * 1e6 * cells / clk / 1e9
+    return peak, (f"per warp-row: {alu} ALU ops / 2 per clk/SM vs {4 * slots} smem wavefronts "
+                  f"/ 1 per clk/SM ({slots} table slots, {byte_words} byte words, L{L} H{H}); "
+                  f"{32 * 2 * H} computed cells, {m}/{2 * L * H} of them algorithmic")
+
+
 def db_layout(name, scaling, world):
     """The database as chunks [(seed, count)] and each rank's share as
     (chunk, first, last) sequence ranges -- contiguous in the global order
@@ -985,6 +1007,7 @@ def main():  # noqa: C901
         slots = nm + rest // 4 + (1 if rest % 4 else 0)
         table_bpc = round(slots * 16 / (2 * H_dom), 3)
     smem_peak = n_sm * sm_max * 1e6 * (128 / table_bpc) / 1e9
+    instr = instruction_bound(dom_form, dom_a, dgeo["lanes"], dgeo["rows"], dom_m, n_sm, sm_max)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
@@ -1027,6 +1050,9 @@ def main():  # noqa: C901
                                     "basis": f"128 B/clk/SM shared-memory bandwidth / {table_bpc} "
                                              f"emission-table bytes per cell ({dom_form}); every "
                                              "cell gathers its cost from the table"},
+                     "instruction_bound": None if instr is None else {
+                         "peak": round(instr[0], 1), "unit": "GCUPS",
+                         "frac": round(achieved / instr[0], 4), "basis": instr[1]},
                      "hbm": {"achieved": round(hbm_achieved, 1), "peak": hbm_gbs, "unit": "GB/s",
                              "frac": round(hbm_achieved / hbm_gbs, 4),
                              "basis": "1 residue byte per M cells (tables on chip)"}},
