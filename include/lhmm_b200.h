@@ -274,6 +274,20 @@ int lhmm_context_synchronize(lhmm_context* ctx);
 int lhmm_scan_streamed(lhmm_context* ctx, const lhmm_scan_options* opt, int segments,
                        uint8_t* raw_out, uint8_t* pass_out, lhmm_scan_stats* stats);
 
+/* Several scans over ONE streamed upload of the packed host image: job j
+ * scans with profile profile_ids[j] and opts[j] into raw_out[j] / pass_out[j]
+ * (host arrays of local_sequences bytes).  The database is copied in
+ * `segments` pieces (at least 16 MB each) on the copy stream, and every job
+ * scans each piece as it lands, at the geometry the policy picks for the
+ * whole database -- the copy hides behind all the jobs' kernels instead of
+ * the first one's (C4: MSV + SSV over a 10 GB shard).  Results are identical
+ * to one lhmm_scan per job.  The reference analogue is a caller looping
+ * scan_database over models on one BlockSet (src/engine.cpp:496-542). */
+int lhmm_scan_streamed_jobs(lhmm_context* ctx, int n_jobs, const uint32_t* profile_ids,
+                            const lhmm_scan_options* opts, int segments,
+                            uint8_t* const* raw_out, uint8_t* const* pass_out,
+                            lhmm_scan_stats* stats /* n_jobs, may be NULL */);
+
 /* SSV over all sequences, then MSV over the survivors (pass bit set),
  * compacted on the device.  ssv_raw/pass for all; msv_raw valid where
  * pass_out != 0, else 0.  Returns survivors via *rescored. */

@@ -99,6 +99,8 @@ SIGNATURES = {
     "lhmm_context_synchronize": (C.c_int, [vp]),
     "lhmm_scan_streamed": (C.c_int, [vp, C.POINTER(ScanOptionsC), C.c_int, u8p, u8p,
                                      C.POINTER(ScanStatsC)]),
+    "lhmm_scan_streamed_jobs": (C.c_int, [vp, C.c_int, u32p, C.POINTER(ScanOptionsC), C.c_int,
+                                          C.POINTER(u8p), C.POINTER(u8p), C.POINTER(ScanStatsC)]),
     "lhmm_filter_pipeline": (C.c_int, [vp, C.c_double, C.c_int, u8p, u8p, u8p, u64p,
                                        C.POINTER(ScanStatsC), C.POINTER(ScanStatsC)]),
     "lhmm_rng_create": (C.c_int, [C.c_uint64, C.POINTER(vp)]),

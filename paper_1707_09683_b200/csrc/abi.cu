@@ -436,6 +436,26 @@ struct lhmm_context {
     uint64_t n_global = 0;         // sequences of the whole (unsharded) database
     std::vector<void*> peer_own, peer_open;  // exported / mapped peer output buffers
     DevBuf<uint8_t> d_flag;        // FP16X: per-sequence "rescore exactly"
+    DevBuf<uint8_t> d_jobs_out;    // lhmm_scan_streamed_jobs: raw | pass per job
+    DevBuf<uint8_t> d_jobs_aux;    // ... 32-byte counter block + flags per job
+    std::vector<cudaStream_t> job_streams;
+    std::vector<cudaEvent_t> job_events;  // (ev0, ev1) per job
+    // lhmm_scan_streamed_jobs: while set, do_scan launches one job of a
+    // concurrent group -- on the job's stream, with its own counters and
+    // flags, on its share of the SMs, waiting per piece on the shared ready
+    // flags -- and returns right after the launch (the caller finishes it)
+    struct JobLaunch {
+        cudaStream_t stream = nullptr;
+        uint8_t* block = nullptr;     // 32-byte counter block
+        uint8_t* flags = nullptr;     // per-sequence "rescore exactly"
+        double share = 1.0;           // fraction of the persistent grid
+        uint32_t n_pieces = 0;
+        cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+        // set by the launch
+        int variant = 0;
+        uint32_t L = 0, H = 0, grid = 0, threads = 0, smem = 0;
+        bool relaxed = false, track_sat = false, track_modes = false;
+    }* job = nullptr;
 
     std::map<std::tuple<int, int, uint32_t, uint32_t, size_t>, std::pair<int, int>> occupancy;
     // geometry policy results per (m, alg, variant, want_L, tiles)
@@ -640,6 +660,85 @@ int compact(lhmm_context* c, lhmm_context::Pipe& P, const DbView& src, const uin
 int compact_host(lhmm_context* c, lhmm_context::Pipe& P, const uint8_t* sel, DbView* out,
                  uint32_t* nsel_out, bool global_out = false);
 
+// The geometry policy: code form, lanes L and register rows H (and whether
+// the model needs the K-warp kernel) for a scan of `n_tiles` tiles with the
+// current profile; `feedback`: this profile's saturation / rescoring history
+// over the context's database may steer the choice (whole-database scans).
+int resolve_geometry(lhmm_context* c, ProfileSlot& pf, const lhmm_scan_options* opt,
+                     uint64_t n_tiles, bool feedback, int& variant, uint32_t& L, uint32_t& H,
+                     bool& long_model) {
+    L = opt->lanes;
+    H = opt->rows;
+    if (L != 0 && (L > 32 * kMaxLongK || (L & (L - 1))))
+        return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,512]");
+    // models beyond one warp (or an explicit lanes > 32): K warps per sequence
+    long_model = L > 32;
+    if (!long_model && L == 0 && H == 0 && pf.m > max_standard_capacity(opt->alg))
+        long_model = true;
+    if (long_model) {
+        if (!choose_long(pf.m, L, H)) {
+            return set_error(LHMM_ERR_DATA, "no long-model geometry covers model length " +
+                                                std::to_string(pf.m));
+        }
+        variant = LHMM_VARIANT_FP16;
+    } else if (H == 0) {
+        Choice ch;
+        // after one MSV scan of this profile over this database we know
+        // whether its scores saturate; mostly non-saturating inputs keep the
+        // exact-mode code, where the one-body FP16 kernel is faster
+        const bool two_mode_ok =
+            opt->alg == LHMM_MSV
+                ? !(feedback && pf.sat_gen == c->db_gen && pf.sat_frac >= 0.0 &&
+                    pf.sat_frac < 0.5)
+                : !(feedback && pf.flag_gen == c->db_gen && pf.flag_frac > 0.2);
+        // non-saturating MSV: the relaxed FP16XR kernel unless it had to
+        // rescore more than 5% of this database
+        const bool relaxed_msv_ok =
+            opt->alg == LHMM_MSV &&
+            !(feedback && pf.msv_flag_gen == c->db_gen && pf.msv_flag_frac > 0.05);
+        // ... and first the fixed-B form, whose u domain needs dbias <= 127
+        const bool fixb_msv_ok =
+            opt->alg == LHMM_MSV && pf.q.dbias <= 127 &&
+            !(feedback && pf.fixb_flag_gen == c->db_gen && pf.fixb_flag_frac > 0.05);
+        const auto ckey =
+            std::make_tuple(pf.m, opt->alg, variant, L,
+                            n_tiles + (two_mode_ok ? 0 : (1ull << 62)) +
+                                (relaxed_msv_ok ? 0 : (1ull << 61)) +
+                                (fixb_msv_ok ? 0 : (1ull << 60)));
+        const auto cit = c->choices.find(ckey);
+        if (cit != c->choices.end()) {
+            std::tie(ch.variant, ch.L, ch.H) = cit->second;
+        } else {
+            ch = choose_geometry(pf.m, opt->alg, variant, L, n_tiles, c->sm_count, two_mode_ok,
+                                 relaxed_msv_ok, fixb_msv_ok);
+            if (c->choices.size() > 256) c->choices.clear();
+            c->choices.emplace(ckey, std::make_tuple(ch.variant, ch.L, ch.H));
+        }
+        if (!ch.L)
+            return set_error(LHMM_ERR_DATA,
+                             "no instantiated geometry covers model length " + std::to_string(pf.m));
+        variant = ch.variant;
+        L = ch.L;
+        H = ch.H;
+    } else {
+        if (variant == LHMM_VARIANT_AUTO) variant = LHMM_VARIANT_FP16;
+        if (L == 0) {
+            // explicit H: the smallest lane count whose capacity covers the model
+            const uint64_t cpw = lhmm::cells_per_word(variant);
+            L = 1;
+            while (L < 32 && cpw * L * H < pf.m) L *= 2;
+        }
+        // an explicit (variant, L, H) runs exactly that code form -- the
+        // calibration sweep depends on it
+    }
+    if (!long_model && (L < 1 || L > 32 || (L & (L - 1))))
+        return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,32]");
+    if (!long_model && !rows_instantiated(variant, H))
+        return set_error(LHMM_ERR_CONTRACT, "row count " + std::to_string(H) +
+                                                " has no compiled kernel for this variant");
+    return LHMM_OK;
+}
+
 // global_out: outputs (and FP16X flags) are addressed by GLOBAL sequence
 // index -- d_raw / d_pass span the whole database, typically rank 0's
 // buffers mapped through CUDA IPC (the fused gather).
@@ -674,74 +773,11 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (variant == LHMM_VARIANT_FP16XRM && opt->alg == LHMM_SSV)
         variant = LHMM_VARIANT_FP16XM;  // its SSV twin
 
-    uint32_t L = opt->lanes, H = opt->rows;
-    if (L != 0 && (L > 32 * kMaxLongK || (L & (L - 1))))
-        return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,512]");
-    // models beyond one warp (or an explicit lanes > 32): K warps per sequence
-    bool long_model = L > 32;
-    if (!long_model && L == 0 && H == 0 && pf.m > max_standard_capacity(opt->alg))
-        long_model = true;
-    if (long_model) {
-        if (!choose_long(pf.m, L, H)) {
-            return set_error(LHMM_ERR_DATA, "no long-model geometry covers model length " +
-                                                std::to_string(pf.m));
-        }
-        variant = LHMM_VARIANT_FP16;
-    } else if (H == 0) {
-        Choice ch;
-        // after one MSV scan of this profile over this database we know
-        // whether its scores saturate; mostly non-saturating inputs keep the
-        // exact-mode code, where the one-body FP16 kernel is faster
-        const bool two_mode_ok =
-            opt->alg == LHMM_MSV
-                ? !(view == nullptr && pf.sat_gen == c->db_gen && pf.sat_frac >= 0.0 &&
-                    pf.sat_frac < 0.5)
-                : !(view == nullptr && pf.flag_gen == c->db_gen && pf.flag_frac > 0.2);
-        // non-saturating MSV: the relaxed FP16XR kernel unless it had to
-        // rescore more than 5% of this database
-        const bool relaxed_msv_ok =
-            opt->alg == LHMM_MSV &&
-            !(view == nullptr && pf.msv_flag_gen == c->db_gen && pf.msv_flag_frac > 0.05);
-        // ... and first the fixed-B form, whose u domain needs dbias <= 127
-        const bool fixb_msv_ok =
-            opt->alg == LHMM_MSV && pf.q.dbias <= 127 &&
-            !(view == nullptr && pf.fixb_flag_gen == c->db_gen && pf.fixb_flag_frac > 0.05);
-        const auto ckey =
-            std::make_tuple(pf.m, opt->alg, variant, L,
-                            v.n_tiles + (two_mode_ok ? 0 : (1ull << 62)) +
-                                (relaxed_msv_ok ? 0 : (1ull << 61)) +
-                                (fixb_msv_ok ? 0 : (1ull << 60)));
-        const auto cit = c->choices.find(ckey);
-        if (cit != c->choices.end()) {
-            std::tie(ch.variant, ch.L, ch.H) = cit->second;
-        } else {
-            ch = choose_geometry(pf.m, opt->alg, variant, L, v.n_tiles, c->sm_count, two_mode_ok,
-                                 relaxed_msv_ok, fixb_msv_ok);
-            if (c->choices.size() > 256) c->choices.clear();
-            c->choices.emplace(ckey, std::make_tuple(ch.variant, ch.L, ch.H));
-        }
-        if (!ch.L)
-            return set_error(LHMM_ERR_DATA,
-                             "no instantiated geometry covers model length " + std::to_string(pf.m));
-        variant = ch.variant;
-        L = ch.L;
-        H = ch.H;
-    } else {
-        if (variant == LHMM_VARIANT_AUTO) variant = LHMM_VARIANT_FP16;
-        if (L == 0) {
-            // explicit H: the smallest lane count whose capacity covers the model
-            const uint64_t cpw = lhmm::cells_per_word(variant);
-            L = 1;
-            while (L < 32 && cpw * L * H < pf.m) L *= 2;
-        }
-        // an explicit (variant, L, H) runs exactly that code form -- the
-        // calibration sweep depends on it
-    }
-    if (!long_model && (L < 1 || L > 32 || (L & (L - 1))))
-        return set_error(LHMM_ERR_CONTRACT, "lane count must be a power of two in [1,32]");
-    if (!long_model && !rows_instantiated(variant, H))
-        return set_error(LHMM_ERR_CONTRACT, "row count " + std::to_string(H) +
-                                                " has no compiled kernel for this variant");
+    uint32_t L = 0, H = 0;
+    bool long_model = false;
+    if (int rc = resolve_geometry(c, pf, opt, v.n_tiles, view == nullptr, variant, L, H,
+                                  long_model))
+        return rc;
     const uint64_t cap = uint64_t(lhmm::cells_per_word(variant)) * L * H;
     if (cap < pf.m)
         return set_error(LHMM_ERR_DATA, "geometry capacity " + std::to_string(cap) +
@@ -802,7 +838,9 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         lit = pf.lens.emplace(lkey, std::move(lt)).first;
     }
     if (!c->d_block.ptr) return set_error(LHMM_ERR_CONTRACT, "no database set");
-    CUDA_TRY(cudaMemsetAsync(c->d_block.ptr, 0, 32, c->stream));
+    uint32_t* const cnt32 =
+        c->job ? reinterpret_cast<uint32_t*>(c->job->block) : c->counter32();
+    CUDA_TRY(cudaMemsetAsync(cnt32, 0, 32, c->job ? c->job->stream : c->stream));
 
     lhmm::KParams p{};
     p.db = v.db;
@@ -814,7 +852,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     p.table = tab.buf.ptr;
     p.raw_out = d_raw;
     p.pass_out = d_pass;
-    p.counter = c->counter32();
+    p.counter = cnt32;
     p.n_items = uint32_t(v.n_tiles * items_per_tile);
     p.table_bytes = uint32_t(table_bytes);
     p.res_stride = tab.res_stride;
@@ -826,17 +864,20 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     p.tecjb = uint32_t(pf.q.tec) + uint32_t(pf.q.tjb);
     p.fault = opt->fault_injection ? 1u : 0u;
     const bool track_sat = opt->alg == LHMM_MSV && view == nullptr;
-    if (track_sat) p.sat_count = c->counter32() + 1;
+    if (track_sat) p.sat_count = cnt32 + 1;
     const bool track_modes = opt->alg == LHMM_MSV && !long_model &&
                              (variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16X_ALT ||
                               variant == LHMM_VARIANT_FP16XM || variant == LHMM_VARIANT_FP16XH);
-    if (track_modes) p.mode_rows = c->counts_dev() + 2;
+    if (track_modes) p.mode_rows = reinterpret_cast<unsigned long long*>(cnt32) + 2;
     p.wrap = opt->reorder_mode == 1 ? 1u : 0u;
     const bool relaxed = ((variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16XM) &&
                           opt->alg == LHMM_SSV) ||
                          ((variant == LHMM_VARIANT_FP16XR || variant == LHMM_VARIANT_FP16XRM) &&
                           opt->alg == LHMM_MSV);
-    if (relaxed) {
+    if (relaxed && c->job) {
+        p.flag_out = c->job->flags;
+        p.flag_count = cnt32 + 2;
+    } else if (relaxed) {
         if (int rc = c->d_flag.reserve(
                 std::max<uint64_t>(global_out ? c->n_global : c->db.n_local, 1)))
             return rc;
@@ -846,13 +887,13 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         }
         CUDA_TRY(cudaEventRecord(c->evr0, c->stream));
         p.flag_out = c->d_flag.ptr;
-        p.flag_count = c->counter32() + 2;
+        p.flag_count = cnt32 + 2;
     }
 
     lhmm::LaunchCfg cfg{};
     cfg.threads = lhmm::kMaxThreads;
     cfg.smem = long_model ? 0 : table_bytes;  // long models read the table from global
-    cfg.stream = c->stream;
+    cfg.stream = c->job ? c->job->stream : c->stream;
     auto okey = std::make_tuple(variant, opt->alg, L, H, table_bytes);
     auto it = c->occupancy.find(okey);
     if (it == c->occupancy.end()) {
@@ -872,6 +913,32 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     const uint64_t need = (uint64_t(p.n_items) + warps_per_cta - 1) / warps_per_cta;
     cfg.grid = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(c->sm_count) * bps, need)));
 
+    if (c->job) {
+        // one job of lhmm_scan_streamed_jobs: its share of the SMs, waiting
+        // per piece on the ready flags the copy stream writes
+        auto& J = *c->job;
+        lhmm::KParams ps = p;
+        ps.piece_end = c->d_pieces.ptr;
+        ps.piece_ready = c->d_pieces.ptr + kMaxPieces;
+        ps.n_pieces = J.n_pieces;
+        const int cap = int(double(c->sm_count) * bps * J.share + 0.5);
+        cfg.grid = std::max(1, std::min(cfg.grid, cap));
+        CUDA_TRY(cudaEventRecord(J.ev0, J.stream));
+        if (p.n_items > 0 && fn(lhmm::kOpLaunch, int(H), &cfg, &ps) != 0)
+            return set_error(LHMM_ERR_CUDA, std::string("kernel launch failed: ") +
+                                                cudaGetErrorString(cudaGetLastError()));
+        CUDA_TRY(cudaEventRecord(J.ev1, J.stream));
+        J.variant = variant;
+        J.L = L;
+        J.H = H;
+        J.grid = uint32_t(cfg.grid);
+        J.threads = uint32_t(cfg.threads);
+        J.smem = uint32_t(cfg.smem);
+        J.relaxed = relaxed;
+        J.track_sat = track_sat;
+        J.track_modes = track_modes;
+        return LHMM_OK;
+    }
     uint32_t launches = 0;
     if (streamed_db) {
         // out-of-core: pieces of whole tiles up to one ring slot each; the
@@ -1535,6 +1602,12 @@ int lhmm_context_destroy(lhmm_context* c) {
     c->counts_host.release();
     lhmm_peer_buffers_release(c);
     c->d_out_gidx.release();
+    c->d_jobs_out.release();
+    c->d_jobs_aux.release();
+    for (auto st : c->job_streams) cudaStreamDestroy(st);
+    for (auto ev : c->job_events) cudaEventDestroy(ev);
+    c->job_streams.clear();
+    c->job_events.clear();
     c->d_db.release();
     c->d_pieces.release();
     if (c->ev_side) cudaEventDestroy(c->ev_side);
@@ -1837,6 +1910,366 @@ int lhmm_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* raw, uint8
     const int orc = outputs_to_host(c, raw, pass, c->db.n_local);
     c->staged = false;
     return orc;
+}
+
+// The jobs of lhmm_scan_streamed_jobs as concurrent single launches: the
+// whole upload is queued on the copy stream (a ready flag written behind each
+// piece), and every job's persistent kernel runs on its own stream over its
+// share of the SMs (in proportion to its predicted time), claiming tiles in
+// database order and waiting per piece on the flags -- so the copy hides
+// behind all the jobs, with no per-piece launches or grid tails.  Each job is
+// then finished like lhmm_scan: counters read, flagged sequences rescored
+// exactly, policy feedback recorded.
+int scan_jobs_concurrent(lhmm_context* c, int n_jobs, const uint32_t* profile_ids,
+                         const std::vector<lhmm_scan_options>& plan, int segments,
+                         uint8_t* const* raw, uint8_t* const* pass, lhmm_scan_stats* stats) {
+    auto& db = c->db;
+    const uint64_t T = db.n_tiles, n = db.n_local;
+    const size_t J = size_t(n_jobs);
+    if (int rc = c->d_pieces.reserve(2 * kMaxPieces)) return rc;
+    if (int rc = c->d_jobs_aux.reserve(J * (32 + std::max<uint64_t>(n, 1)))) return rc;
+    while (c->job_streams.size() < J) {
+        cudaStream_t st = nullptr;
+        CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        c->job_streams.push_back(st);
+        for (int e = 0; e < 2; ++e) {
+            cudaEvent_t ev = nullptr;
+            CUDA_TRY(cudaEventCreate(&ev));
+            c->job_events.push_back(ev);
+        }
+    }
+    if (!c->ev_side) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
+    // shares of the grid in proportion to each job's predicted time per
+    // residue (its geometry's capacity over its calibrated rate)
+    std::vector<double> w(J, 1.0);
+    double wsum = 0.0;
+    for (size_t j = 0; j < J; ++j) {
+        const lhmm_scan_options& o = plan[j];
+        const uint64_t cap = uint64_t(lhmm::cells_per_word(o.variant)) * o.lanes * o.rows;
+        double rate = o.lanes <= 32 ? calib_rate(o.variant, o.alg, o.lanes, o.rows) : -1.0;
+        if (rate <= 0 && o.lanes <= 32) rate = model_rate(o.variant, o.alg, o.lanes, o.rows);
+        w[j] = rate > 0 ? double(cap) / rate : double(cap);
+        wsum += w[j];
+    }
+    // byte-balanced pieces of at least 4 MB (each costs one copy and one
+    // flag write), as the single-launch streamed scan cuts them
+    segments = int(std::min<uint64_t>(uint64_t(segments),
+                                      std::max<uint64_t>(1, db.data_bytes >> 22)));
+    std::vector<uint32_t> ends;
+    for (int k = 0, t0 = 0; k < segments && uint64_t(t0) < T; ++k) {
+        const uint64_t goal = db.data_bytes * uint64_t(k + 1) / uint64_t(segments);
+        uint64_t t1 = k + 1 == segments
+                          ? T
+                          : uint64_t(std::lower_bound(db.tile_off.begin(), db.tile_off.end(), goal) -
+                                     db.tile_off.begin());
+        t1 = std::max<uint64_t>(t1, uint64_t(t0) + 1);
+        ends.push_back(uint32_t(std::min<uint64_t>(t1, T)));
+        t0 = int(t1);
+    }
+    if (ends.empty()) ends.push_back(uint32_t(T));
+    ends.back() = uint32_t(T);
+    CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev0, 0));
+    CUDA_TRY(cudaMemsetAsync(c->d_pieces.ptr + kMaxPieces, 0, kMaxPieces * 4, c->copy_stream));
+    CUDA_TRY(cudaMemcpyAsync(c->d_pieces.ptr, ends.data(), ends.size() * 4, cudaMemcpyHostToDevice,
+                             c->copy_stream));
+    CUDA_TRY(cudaEventRecord(c->ev_side, c->copy_stream));
+    // the whole upload first (so no kernel can wait on a piece never queued)
+    uint64_t t0 = 0;
+    for (size_t k = 0; k < ends.size(); ++k) {
+        const uint64_t b0 = db.tile_off[t0];
+        const uint64_t b1 = ends[k] < T ? db.tile_off[ends[k]] : db.data_bytes;
+        if (int rc = upload_side(c, t0, ends[k], c->copy_stream)) return rc;
+        CUDA_TRY(cudaMemcpyAsync(c->d_db.ptr + b0, db.data + b0, b1 - b0, cudaMemcpyHostToDevice,
+                                 c->copy_stream));
+        const CUresult cr = c->write_value32(
+            reinterpret_cast<CUstream>(c->copy_stream),
+            reinterpret_cast<CUdeviceptr>(c->d_pieces.ptr + kMaxPieces + k), 1u,
+            CU_STREAM_WRITE_VALUE_DEFAULT);
+        if (cr != CUDA_SUCCESS) return set_error(LHMM_ERR_CUDA, "cuStreamWriteValue32 failed");
+        t0 = ends[k];
+    }
+    std::vector<lhmm_context::JobLaunch> jl(J);
+    for (size_t j = 0; j < J; ++j) {
+        auto& L = jl[j];
+        L.stream = c->job_streams[j];
+        L.block = c->d_jobs_aux.ptr + j * 32;
+        L.flags = c->d_jobs_aux.ptr + J * 32 + j * std::max<uint64_t>(n, 1);
+        L.share = w[j] / wsum;
+        L.n_pieces = uint32_t(ends.size());
+        L.ev0 = c->job_events[2 * j];
+        L.ev1 = c->job_events[2 * j + 1];
+        CUDA_TRY(cudaStreamWaitEvent(L.stream, c->ev_side, 0));
+        c->current = int(profile_ids[j]);
+        c->job = &L;
+        uint8_t* out = c->d_jobs_out.ptr + 2 * n * uint64_t(j);
+        lhmm_scan_stats st{};
+        const int rc = do_scan(c, &plan[j], out, out + n, &st);
+        c->job = nullptr;
+        if (rc) {
+            cudaDeviceSynchronize();  // the queued upload and launched jobs end on their own
+            return rc;
+        }
+    }
+    // finish every job: counters, exact rescoring of its flagged sequences
+    const DbView whole{c->d_db.ptr, c->d_tile_off.ptr, c->d_lens.ptr, c->d_out_idx.ptr,
+                       db.n_tiles, db.residues, n};
+    uint32_t* counts = c->counts_host.reserve(32) ? reinterpret_cast<uint32_t*>(c->counts_host.ptr)
+                                                  : nullptr;
+    if (!counts) return set_error(LHMM_ERR_NOMEM, "cannot allocate pinned counter words");
+    for (size_t j = 0; j < J; ++j) {
+        auto& L = jl[j];
+        CUDA_TRY(cudaMemcpyAsync(counts, L.block, 32, cudaMemcpyDeviceToHost, L.stream));
+        CUDA_TRY(cudaStreamSynchronize(L.stream));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, L.ev0, L.ev1));
+        ProfileSlot& pf = c->profiles[profile_ids[j]];
+        lhmm_scan_stats a{};
+        a.device_ms = ms;
+        a.launches = 1;
+        a.lanes = L.L;
+        a.rows = L.H;
+        a.variant = uint32_t(L.variant);
+        a.grid = L.grid;
+        a.threads = L.threads;
+        a.smem_bytes = L.smem;
+        a.sequences = n;
+        a.residues = db.residues;
+        a.cells = db.residues * uint64_t(pf.m);
+        if (L.track_sat) {
+            a.saturated = counts[1];
+            if (n > 0) {
+                pf.sat_frac = double(counts[1]) / double(n);
+                pf.sat_gen = c->db_gen;
+            }
+        }
+        if (L.track_modes) {
+            uint64_t mr[2];
+            std::memcpy(mr, counts + 4, 16);
+            a.mode_rows = mr[0];
+            a.lazy_rows = mr[1];
+        }
+        if (L.relaxed) {
+            const uint32_t nflag = counts[2];
+            if (nflag) {
+                DbView sub;
+                uint32_t nsel = 0;
+                if (int rc = compact(c, c->resc, whole, L.flags, &sub, &nsel)) return rc;
+                if (nsel) {
+                    lhmm_scan_options ox = plan[j];
+                    ox.variant = LHMM_VARIANT_FP16;
+                    ox.lanes = 0;
+                    ox.rows = 0;
+                    const int twin = L.variant == LHMM_VARIANT_FP16XR    ? LHMM_VARIANT_FP16X
+                                     : L.variant == LHMM_VARIANT_FP16XRM ? LHMM_VARIANT_FP16XM
+                                     : L.variant == LHMM_VARIANT_FP16X   ? LHMM_VARIANT_FP16
+                                                                         : -1;
+                    if (plan[j].reorder_mode == 1 && twin >= 0 && rows_instantiated(twin, L.H)) {
+                        ox.variant = twin;
+                        ox.lanes = L.L;
+                        ox.rows = L.H;
+                    }
+                    c->current = int(profile_ids[j]);
+                    uint8_t* out = c->d_jobs_out.ptr + 2 * n * uint64_t(j);
+                    lhmm_scan_stats sx{};
+                    if (int rc = do_scan(c, &ox, out, out + n, &sx, 0, &sub)) return rc;
+                    a.launches += sx.launches;
+                    a.device_ms += sx.device_ms;
+                }
+                a.recomputed = nsel;
+            }
+            if (n > 0) {
+                const double f = double(nflag) / double(n);
+                if (L.variant == LHMM_VARIANT_FP16XRM) {
+                    pf.fixb_flag_frac = f;
+                    pf.fixb_flag_gen = c->db_gen;
+                } else if (plan[j].alg == LHMM_MSV) {
+                    pf.msv_flag_frac = f;
+                    pf.msv_flag_gen = c->db_gen;
+                } else {
+                    pf.flag_frac = f;
+                    pf.flag_gen = c->db_gen;
+                }
+            }
+        }
+        a.gcups = a.device_ms > 0 ? double(a.cells) / (a.device_ms * 1e-3) / 1e9 : 0.0;
+        if (stats) stats[j] = a;
+    }
+    // every job's results to its host buffers
+    for (size_t j = 0; j < J; ++j) {
+        const uint8_t* out = c->d_jobs_out.ptr + 2 * n * uint64_t(j);
+        if (page_locked(raw[j]) && page_locked(pass[j])) {
+            CUDA_TRY(cudaMemcpyAsync(raw[j], out, n, cudaMemcpyDeviceToHost, c->stream));
+            CUDA_TRY(cudaMemcpyAsync(pass[j], out + n, n, cudaMemcpyDeviceToHost, c->stream));
+        } else {
+            if (!c->out_host.reserve(32 + 2 * n))
+                return set_error(LHMM_ERR_NOMEM, "cannot allocate the pinned output staging");
+            CUDA_TRY(cudaMemcpyAsync(c->out_host.ptr + 32, out, 2 * n, cudaMemcpyDeviceToHost,
+                                     c->stream));
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            std::memcpy(raw[j], c->out_host.ptr + 32, n);
+            std::memcpy(pass[j], c->out_host.ptr + 32 + n, n);
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return LHMM_OK;
+}
+
+// Several scans (profile, options) over ONE streamed upload of the packed
+// host image: the pieces are copied on the copy stream, and as each lands
+// every job scans it (per-piece launches on the piece's tiles, at the
+// geometry the policy picks for the whole database), so the H2D copy hides
+// behind all the jobs' kernels rather than the first one's.  Each job's
+// flagged sequences are rescored exactly inside its piece.
+int lhmm_scan_streamed_jobs(lhmm_context* c, int n_jobs, const uint32_t* profile_ids,
+                            const lhmm_scan_options* opts, int segments, uint8_t* const* raw,
+                            uint8_t* const* pass, lhmm_scan_stats* stats) {
+    if (!c) return set_error(LHMM_ERR_CONTRACT, "null context");
+    if (n_jobs < 1 || !profile_ids || !opts || !raw || !pass)
+        return set_error(LHMM_ERR_CONTRACT, "null argument");
+    for (int j = 0; j < n_jobs; ++j)
+        if (!raw[j] || !pass[j]) return set_error(LHMM_ERR_CONTRACT, "null output");
+    if (segments < 1 || segments > int(kMaxPieces))
+        return set_error(LHMM_ERR_CONTRACT, "segments must lie in [1,64]");
+    DeviceGuard g(c->device);
+    if (!c->have_db) return set_error(LHMM_ERR_CONTRACT, "no database set");
+    if (c->host_resident)
+        return set_error(LHMM_ERR_CONTRACT, "streamed jobs need a device-resident database");
+    auto& db = c->db;
+    const uint64_t T = db.n_tiles, n = db.n_local;
+    const int prev = c->current;
+    // every job's code form and geometry, fixed once for the whole database
+    std::vector<lhmm_scan_options> plan(static_cast<size_t>(n_jobs));
+    for (int j = 0; j < n_jobs; ++j) {
+        if (int rc = lhmm_select_profile(c, profile_ids[j])) return rc;
+        if (opts[j].alg != LHMM_MSV && opts[j].alg != LHMM_SSV)
+            return set_error(LHMM_ERR_CONTRACT, "unknown algorithm");
+        if (opts[j].variant < LHMM_VARIANT_AUTO || opts[j].variant > LHMM_VARIANT_FP16XRM)
+            return set_error(LHMM_ERR_CONTRACT, "unknown kernel variant");
+        plan[size_t(j)] = opts[j];
+        int variant = opts[j].variant;
+        if (opts[j].alg == LHMM_SSV) {
+            if (variant == LHMM_VARIANT_FP16X_ALT || variant == LHMM_VARIANT_FP16XR)
+                variant = LHMM_VARIANT_FP16X;
+            if (variant == LHMM_VARIANT_FP16XH || variant == LHMM_VARIANT_FP16XRM)
+                variant = LHMM_VARIANT_FP16XM;
+        }
+        uint32_t L = 0, H = 0;
+        bool long_model = false;
+        if (int rc = resolve_geometry(c, c->profiles[c->current], &opts[j], T, true, variant, L,
+                                      H, long_model))
+            return rc;
+        plan[size_t(j)].variant = variant;
+        plan[size_t(j)].lanes = L;
+        plan[size_t(j)].rows = H;
+    }
+    if (int rc = c->d_jobs_out.reserve(std::max<uint64_t>(1, 2 * n * uint64_t(n_jobs)))) return rc;
+    if (int rc = c->d_db.reserve(db.data_bytes)) return rc;
+    if (c->stream_mem_ops) {
+        const int rc = scan_jobs_concurrent(c, n_jobs, profile_ids, plan, segments, raw, pass, stats);
+        c->job = nullptr;
+        c->current = prev;
+        return rc;
+    }
+    // pieces of at least 16 MB (each costs one launch, and its tail, per job)
+    segments = int(std::min<uint64_t>(uint64_t(segments), std::max<uint64_t>(1, db.data_bytes >> 24)));
+    if (c->seg_events.size() < size_t(segments)) {
+        for (auto e : c->seg_events) cudaEventDestroy(e);
+        c->seg_events.assign(size_t(segments), nullptr);
+        for (auto& e : c->seg_events) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    std::vector<uint64_t> ends;
+    for (int k = 0, t0 = 0; k < segments && uint64_t(t0) < T; ++k) {
+        const uint64_t goal = db.data_bytes * uint64_t(k + 1) / uint64_t(segments);
+        uint64_t t1 = k + 1 == segments
+                          ? T
+                          : uint64_t(std::lower_bound(db.tile_off.begin(), db.tile_off.end(), goal) -
+                                     db.tile_off.begin());
+        t1 = std::min<uint64_t>(T, std::max<uint64_t>(t1, uint64_t(t0) + 1));
+        ends.push_back(t1);
+        t0 = int(t1);
+    }
+    if (!ends.empty()) ends.back() = T;
+    CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev0, 0));
+    // the whole upload is queued at once on the copy stream
+    uint64_t t0 = 0;
+    for (size_t k = 0; k < ends.size(); ++k) {
+        const uint64_t t1 = ends[k];
+        const uint64_t b0 = db.tile_off[t0], b1 = t1 < T ? db.tile_off[t1] : db.data_bytes;
+        if (int rc = upload_side(c, t0, t1, c->copy_stream)) return rc;
+        CUDA_TRY(cudaMemcpyAsync(c->d_db.ptr + b0, db.data + b0, b1 - b0, cudaMemcpyHostToDevice,
+                                 c->copy_stream));
+        CUDA_TRY(cudaEventRecord(c->seg_events[k], c->copy_stream));
+        t0 = t1;
+    }
+    std::vector<lhmm_scan_stats> acc(static_cast<size_t>(n_jobs));
+    for (auto& a : acc) a = lhmm_scan_stats{};
+    t0 = 0;
+    int rc = LHMM_OK;
+    for (size_t k = 0; k < ends.size() && rc == LHMM_OK; ++k) {
+        const uint64_t t1 = ends[k];
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->seg_events[k], 0));
+        uint64_t res = 0, seqs = 0;
+        for (uint64_t t = t0; t < t1; ++t)
+            for (int q = 0; q < 32; ++q)
+                if (db.out_idx[t * 32 + q] != 0xffffffffu) {
+                    ++seqs;
+                    res += db.lens[t * 32 + q];
+                }
+        const DbView piece{c->d_db.ptr, c->d_tile_off.ptr + t0, c->d_lens.ptr + t0 * 32,
+                           c->d_out_idx.ptr + t0 * 32, t1 - t0, res, seqs};
+        for (int j = 0; j < n_jobs && rc == LHMM_OK; ++j) {
+            c->current = int(profile_ids[j]);
+            uint8_t* out = c->d_jobs_out.ptr + 2 * n * uint64_t(j);
+            lhmm_scan_stats st{};
+            rc = do_scan(c, &plan[size_t(j)], out, out + n, &st, 0, &piece);
+            if (rc) break;
+            lhmm_scan_stats& a = acc[size_t(j)];
+            a.device_ms += st.device_ms;
+            a.launches += st.launches;
+            a.recomputed += st.recomputed;
+            a.saturated += st.saturated;
+            a.mode_rows += st.mode_rows;
+            a.lazy_rows += st.lazy_rows;
+            a.residues += st.residues;
+            a.cells += st.cells;
+            a.lanes = st.lanes;
+            a.rows = st.rows;
+            a.variant = st.variant;
+            a.grid = st.grid;
+            a.threads = st.threads;
+            a.smem_bytes = st.smem_bytes;
+        }
+        t0 = t1;
+    }
+    c->current = prev;
+    if (rc) return rc;
+    // every job's results to its host buffers (pinned: straight DMA)
+    for (int j = 0; j < n_jobs; ++j) {
+        const uint8_t* out = c->d_jobs_out.ptr + 2 * n * uint64_t(j);
+        if (page_locked(raw[j]) && page_locked(pass[j])) {
+            CUDA_TRY(cudaMemcpyAsync(raw[j], out, n, cudaMemcpyDeviceToHost, c->stream));
+            CUDA_TRY(cudaMemcpyAsync(pass[j], out + n, n, cudaMemcpyDeviceToHost, c->stream));
+        } else {
+            if (!c->out_host.reserve(32 + 2 * n))
+                return set_error(LHMM_ERR_NOMEM, "cannot allocate the pinned output staging");
+            CUDA_TRY(cudaMemcpyAsync(c->out_host.ptr + 32, out, 2 * n, cudaMemcpyDeviceToHost,
+                                     c->stream));
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            std::memcpy(raw[j], c->out_host.ptr + 32, n);
+            std::memcpy(pass[j], c->out_host.ptr + 32 + n, n);
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (stats)
+        for (int j = 0; j < n_jobs; ++j) {
+            lhmm_scan_stats& a = acc[size_t(j)];
+            a.sequences = n;
+            a.gcups = a.device_ms > 0 ? double(a.cells) / (a.device_ms * 1e-3) / 1e9 : 0.0;
+            stats[j] = a;
+        }
+    return LHMM_OK;
 }
 
 int lhmm_scan_streamed(lhmm_context* c, const lhmm_scan_options* opt, int segments,

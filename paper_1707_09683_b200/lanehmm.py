@@ -395,6 +395,32 @@ class Scanner:
                           st.device_ms * 1e-3, st.gcups, raw[:n], passed[:n].view(bool),
                           st.as_dict())
 
+    def scan_streamed_jobs(self, jobs, segments=64, outs=None):
+        """Several scans over ONE streamed upload of the packed host image
+        (lhmm_scan_streamed_jobs): `jobs` = [(profile_id, ScanOptions)], each
+        piece scanned by every job as it lands.  `outs`: optional [(raw,
+        passed)] per job.  Returns one ScanReport per job."""
+        k = len(jobs)
+        if k < 1:
+            raise ContractError("no jobs")
+        outs = [self._outputs(None if outs is None else outs[j]) for j in range(k)]
+        ids = (C.c_uint32 * k)(*[int(p) for p, _ in jobs])
+        opts = (_native.ScanOptionsC * k)(*[o.c() for _, o in jobs])
+        raws = (_native.u8p * k)(*[r.ctypes.data_as(_native.u8p) for r, _ in outs])
+        passes = (_native.u8p * k)(*[p.ctypes.data_as(_native.u8p) for _, p in outs])
+        sts = (_native.ScanStatsC * k)()
+        _check(_native.lib().lhmm_scan_streamed_jobs(self._ctx, k, ids, opts, int(segments), raws,
+                                                     passes, sts))
+        n = self.n_local
+        reps = []
+        for j, (_, o) in enumerate(jobs):
+            st = sts[j]
+            raw, passed = outs[j]
+            reps.append(ScanReport(o.alg, st.lanes, st.rows, st.variant, st.sequences,
+                                   st.residues, st.device_ms * 1e-3, st.gcups, raw[:n],
+                                   passed[:n].view(bool), st.as_dict()))
+        return reps
+
     def filter_pipeline(self, threshold, variant=Variant.Auto):
         """SSV over the resident database, survivors (pValue <= t or overflow)
         compacted on the device, MSV over the survivors (lhmm_filter_pipeline).

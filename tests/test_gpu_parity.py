@@ -239,6 +239,54 @@ def test_streamed_scan_matches_resident_scan(ora, mem_ops, monkeypatch):
         np.testing.assert_array_equal(s.scan(P.ScanOptions(alg=P.Algorithm.Msv)).raw, want)
 
 
+@pytest.mark.parametrize("mem_ops", ["1", "0"], ids=["concurrent", "per_piece"])
+def test_streamed_jobs_match_oracle_and_resident_scans(ora, mem_ops, monkeypatch):
+    """lhmm_scan_streamed_jobs: several (profile, options) jobs over ONE
+    streamed upload -- concurrent single launches on shares of the SMs
+    waiting on piece flags, or per-piece launches -- each job's raw bytes and
+    pass bits equal its resident lhmm_scan and the scalar oracle (MSV and SSV,
+    default and non-saturating QuantParams, relaxed forms with rescoring, a
+    long model, pageable and page-locked outputs)."""
+    import torch
+    monkeypatch.setenv("LHMM_STREAM_MEM_OPS", mem_ops)
+    rng = P.Rng(0x10B5)
+    db = rng.lognormal_records(150000, 290, 0.65, 2)  # ~55 MB packed: 3 pieces
+    qd, qn = P.QuantParams(), P.QuantParams(3.0, 120, 3, 20, 20)
+    spec = [(200, qd, P.Algorithm.Msv), (200, qd, P.Algorithm.Ssv), (400, qn, P.Algorithm.Msv),
+            (1000, qd, P.Algorithm.Ssv), (5000, qn, P.Algorithm.Msv)]
+    with P.Scanner(0) as s:
+        s.set_database(db)
+        jobs, want, lam = [], [], []
+        for m, q, alg in spec:
+            hmm = rng.random_profile(m)
+            costs = P.quantize_emissions(hmm, q)
+            pid = s.add_profile(costs, q, hmm.lambda_, hmm.tau)
+            jobs.append((pid, P.ScanOptions(alg=alg, threshold=0.022)))
+            want.append((costs, q, alg))
+            lam.append((hmm.lambda_, hmm.tau))
+        n = s.n_local
+        pinned = [(torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy(),
+                   torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy()) for _ in jobs]
+        for outs in (None, pinned):
+            reps = s.scan_streamed_jobs(jobs, 64, outs=outs)
+            for (pid, o), rep in zip(jobs, reps):
+                s.select_profile(pid)
+                base = s.scan(o)
+                np.testing.assert_array_equal(rep.raw, base.raw)
+                np.testing.assert_array_equal(rep.passed, base.passed)
+                assert rep.stats["launches"] >= (1 if mem_ops == "1" else 3)
+                assert rep.lanes == base.lanes and rep.rows == base.rows
+        # oracle on a fixed-stride sample of every job
+        idx = np.arange(0, db.count, 37)
+        off = db.offsets
+        res = np.concatenate([db.residues[off[i]:off[i + 1]] for i in idx])
+        soff = np.concatenate([[0], np.cumsum(off[idx + 1] - off[idx])]).astype(np.uint64)
+        for (costs, q, alg), rep in zip(want, reps):
+            a = 0 if alg == P.Algorithm.Msv else 1
+            np.testing.assert_array_equal(rep.raw[idx],
+                                          ora.scan_flat(a, costs.bytes, res, soff, oq(q)))
+
+
 @pytest.mark.parametrize("threshold", [0.0, 0.022, 0.3, 1.0])
 def test_device_filter_pipeline_matches_oracle(ora, threshold):
     """filter_pipeline semantics (test_engine.cpp:406-450, acceptance
