@@ -289,6 +289,7 @@ static uint32_t slot_rows(int variant, uint32_t H, int alg = -1, uint32_t L = 0)
     if (variant == LHMM_VARIANT_FP16XRM) alg = LHMM_SSV;
     if (variant != LHMM_VARIANT_FP16XM) return H;
     if (alg == LHMM_SSV && L > 0) return uint32_t(4 * xm_slots(int(H), int(L)));
+    if (alg == LHMM_MSV && L > 0) return uint32_t(4 * xm_slots_msv(int(H), int(L)));
     return (H + 4u) / 5u * 4u;
 }
 
@@ -426,8 +427,11 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
         // negated): the cost itself, in both forms
         // SSV (relaxed) tables start with A six-row slots: rows 6s, 6s+1 as
         // f16 pairs, rows 6s+2..6s+5 as four signed-byte pairs
-        const uint32_t A = alg == LHMM_MSV ? 0u : uint32_t(xm_six_slots(int(H), int(L)));
-        const uint32_t nslots = alg == LHMM_MSV ? (H + 4) / 5 : uint32_t(xm_slots(int(H), int(L)));
+        // (MSV, cells negated: the same slot shapes, xm_six_slots_msv)
+        const uint32_t A = uint32_t(alg == LHMM_MSV ? xm_six_slots_msv(int(H), int(L))
+                                                    : xm_six_slots(int(H), int(L)));
+        const uint32_t nslots = uint32_t(alg == LHMM_MSV ? xm_slots_msv(int(H), int(L))
+                                                         : xm_slots(int(H), int(L)));
         for (uint32_t x = 0; x < 23; ++x)
             for (uint32_t hg = 0; hg < nslots; ++hg)
                 for (uint32_t oig = 0; oig < L; ++oig) {
@@ -443,10 +447,12 @@ void build_table(const uint8_t* costs, uint32_t m, int variant, int alg, uint32_
                                                  ? 0xff
                                                  : costs[(node - 1) * 21 + x];
                             if (alg == LHMM_MSV) {
-                                if (k < 3)
+                                if (k < nf) {
                                     slot[k] |= uint32_t(cost) << (16 * c);
-                                else
-                                    slot[3] |= uint32_t(cost) << (8 * (2 * (k - 3) + c));
+                                } else {
+                                    const uint32_t kb = k - nf;
+                                    slot[nf + kb / 2] |= uint32_t(cost) << (8 * (2 * (kb % 2) + c));
+                                }
                                 continue;
                             }
                             const int t = int(dbias) - cost;

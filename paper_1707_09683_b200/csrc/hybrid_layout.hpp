@@ -60,4 +60,21 @@ LHMM_HD constexpr int xm_slots(int H, int L) {
     return a + h5 / 5 + (h5 % 5 ? 1 : 0);
 }
 
+// Six-row slots for the negated two-mode MSV form on the mixed table (FP16XM
+// MSV), LHMM_XM_MSV_SIX=1: by the op count its lazy rows are bound by the
+// table gather (2.8 ALU vs 3.2 shared-memory cycles per word), but measured
+// on B200 the extra byte unpacks cost more than the slot saves: -2.3% / -1.6%
+// / -1.6% at L8 H53 / L8 H63 / L16 H63 (profiles/r2_ab_xm_msv_six.txt).  Off.
+#ifndef LHMM_XM_MSV_SIX
+#define LHMM_XM_MSV_SIX 0
+#endif
+LHMM_HD constexpr int xm_six_slots_msv(int H, int L) {
+    return LHMM_XM_MSV_SIX ? xm_six_slots(H, L) : 0;
+}
+LHMM_HD constexpr int xm_slots_msv(int H, int L) {
+    const int a = xm_six_slots_msv(H, L);
+    const int h5 = H - 6 * a;
+    return a + h5 / 5 + (h5 % 5 ? 1 : 0);
+}
+
 }  // namespace lhmm

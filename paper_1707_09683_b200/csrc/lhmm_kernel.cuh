@@ -650,6 +650,7 @@ struct Fp16SatMixed {
     static_assert(ALG == 0, "the negated two-mode form is MSV");
     static constexpr int CPW = 2;
     static constexpr int kGroup = 5;
+    static constexpr bool kSix = LHMM_XM_MSV_SIX != 0;  // xm_six_slots_msv
     static constexpr bool kMsv = true;
     static constexpr bool kRelaxed = false;
     static constexpr bool kTwoMode = true;
@@ -1191,7 +1192,8 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                 // slot of r 16-bit-pair words.  The relaxed SSV table (kSix)
                 // starts with A six-row slots (two 16-bit-pair words, two
                 // words of four bytes; hybrid_layout.hpp xm_six_slots)
-                constexpr int A = six_rows<V>::value ? xm_six_slots(H, L) : 0;
+                constexpr int A = !six_rows<V>::value ? 0
+                                  : V::kMsv ? xm_six_slots_msv(H, L) : xm_six_slots(H, L);
                 constexpr int B6 = 6 * A;          // first row of the five-row part
                 constexpr int NG = (H - B6) / 5;   // five-row slots
                 constexpr int RT = (H - B6) % 5;
@@ -1271,8 +1273,9 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                             else
                                 g[sl] = V::template cell<LAZY, false, 0>(in, cw[k], st);
                         }
-                        // E: three folds per six-row slot (SSV-shaped rows)
-                        static_assert(!V::kMsv, "six-row slots belong to the relaxed SSV table");
+                        // E: three folds per six-row slot (SSV-shaped rows;
+                        // MSV folds its row after the row)
+                        if constexpr (!V::kMsv) {
                         const int s0 = ((hb - 1 - r) % H + H) % H;
                         const int s1 = ((hb - r) % H + H) % H;
                         const int s2 = ((hb + 1 - r) % H + H) % H;
@@ -1283,6 +1286,7 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                         *acc[(3 * hs + 1) % 4] = V::acc2(*acc[(3 * hs + 1) % 4], g[s0], g[s1]);
                         *acc[(3 * hs + 2) % 4] = V::acc2(*acc[(3 * hs + 2) % 4], g[s2], g[s3]);
                         *acc[(3 * hs + 3) % 4] = V::acc2(*acc[(3 * hs + 3) % 4], g[s4], g[s5]);
+                        }
                     }
                 }
             } else {
