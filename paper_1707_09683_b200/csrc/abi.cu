@@ -2163,6 +2163,17 @@ int lhmm_scan_streamed_jobs(lhmm_context* c, int n_jobs, const uint32_t* profile
         plan[size_t(j)].lanes = L;
         plan[size_t(j)].rows = H;
     }
+    if (T == 0 || n == 0) {  // nothing to upload or scan
+        c->current = prev;
+        if (stats)
+            for (int j = 0; j < n_jobs; ++j) {
+                stats[j] = lhmm_scan_stats{};
+                stats[j].lanes = plan[size_t(j)].lanes;
+                stats[j].rows = plan[size_t(j)].rows;
+                stats[j].variant = uint32_t(plan[size_t(j)].variant);
+            }
+        return LHMM_OK;
+    }
     if (int rc = c->d_jobs_out.reserve(std::max<uint64_t>(1, 2 * n * uint64_t(n_jobs)))) return rc;
     if (int rc = c->d_db.reserve(db.data_bytes)) return rc;
     if (c->stream_mem_ops) {

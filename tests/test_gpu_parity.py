@@ -287,6 +287,31 @@ def test_streamed_jobs_match_oracle_and_resident_scans(ora, mem_ops, monkeypatch
                                           ora.scan_flat(a, costs.bytes, res, soff, oq(q)))
 
 
+def test_streamed_jobs_contract():
+    """lhmm_scan_streamed_jobs: errors like the other scan entry points (no
+    jobs, bad piece count, unknown profile id); the same profile may appear
+    in several jobs."""
+    rng = P.Rng(0x10B6)
+    hmm = rng.random_profile(60)
+    q = P.QuantParams()
+    costs = P.quantize_emissions(hmm, q)
+    with P.Scanner(0) as s:
+        pid = s.add_profile(costs, q, hmm.lambda_, hmm.tau)
+        s.set_database(rng.random_records(100, 20, 80))
+        o = P.ScanOptions(alg=P.Algorithm.Msv)
+        with pytest.raises(P.ContractError):
+            s.scan_streamed_jobs([])
+        with pytest.raises(P.ContractError):
+            s.scan_streamed_jobs([(pid, o)], 0)
+        with pytest.raises(P.ContractError):
+            s.scan_streamed_jobs([(pid + 7, o)], 4)
+        rep = s.scan_streamed_jobs([(pid, o), (pid, P.ScanOptions(alg=P.Algorithm.Ssv))], 4)
+        assert [r.raw.size for r in rep] == [100, 100]
+        s.select_profile(pid)
+        np.testing.assert_array_equal(rep[0].raw, s.scan(o).raw)
+        np.testing.assert_array_equal(rep[1].raw, s.scan(P.ScanOptions(alg=P.Algorithm.Ssv)).raw)
+
+
 @pytest.mark.parametrize("threshold", [0.0, 0.022, 0.3, 1.0])
 def test_device_filter_pipeline_matches_oracle(ora, threshold):
     """filter_pipeline semantics (test_engine.cpp:406-450, acceptance
