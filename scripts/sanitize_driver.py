@@ -97,6 +97,18 @@ def main():
                 rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv, variant=v, lanes=L, threshold=0.2))
                 check(rep, cn, qn, hits, P.Algorithm.Msv)
                 assert rep.stats["recomputed"] > 0
+        # several scans over one streamed upload (concurrent kernels on SM
+        # shares waiting on piece flags, per-job counters and flags, rescoring)
+        pd = s.add_profile(costs, q, hmm.lambda_, hmm.tau)
+        pn = s.add_profile(cn, qn, hmm.lambda_, hmm.tau)
+        jobs = [(pd, P.ScanOptions(alg=P.Algorithm.Msv, threshold=0.2)),
+                (pd, P.ScanOptions(alg=P.Algorithm.Ssv, threshold=0.2)),
+                (pn, P.ScanOptions(alg=P.Algorithm.Msv, variant=P.Variant.Fp16xRelaxedFixedB,
+                                   lanes=8, threshold=0.2))]
+        reps = s.scan_streamed_jobs(jobs, 4)
+        check(reps[0], costs, q, hits, P.Algorithm.Msv)
+        check(reps[1], costs, q, hits, P.Algorithm.Ssv)
+        check(reps[2], cn, qn, hits, P.Algorithm.Msv)
         import torch
         n = hits.count
         perm = torch.randperm(n, device="cuda")
@@ -105,7 +117,9 @@ def main():
         s.scatter_results(dst[0].data_ptr(), dst[1].data_ptr(), src[0].data_ptr(),
                           src[1].data_ptr(), perm.data_ptr(), n)
         s.synchronize()
-        assert torch.equal(dst[:, perm], src)
+        # (compared on the host: .item() would draw on torch's pinned host
+        # cache, which memcheck's leak check reports at exit)
+        assert (dst[:, perm].cpu().numpy() == src.cpu().numpy()).all()
         del perm, src, dst
         torch.cuda.synchronize()
         torch.cuda.empty_cache()  # the caching allocator's blocks (memcheck leak check)
