@@ -437,6 +437,10 @@ struct lhmm_context {
     std::vector<void*> peer_own, peer_open;  // exported / mapped peer output buffers
     DevBuf<uint8_t> d_flag;        // FP16X: per-sequence "rescore exactly"
     DevBuf<uint8_t> d_jobs_out;    // lhmm_scan_streamed_jobs: raw | pass per job
+    bool in_probe = false;         // do_scan runs the saturation probe's sample scan
+    bool probe_enabled = true;     // LHMM_SAT_PROBE=0 turns the probe off
+    uint64_t probe_min_cells = 50000000000ull;  // LHMM_SAT_PROBE_MIN_GCELLS
+    cudaEvent_t ev_probe[2] = {nullptr, nullptr};
     DevBuf<uint8_t> d_jobs_aux;    // ... 32-byte counter block + flags per job
     std::vector<cudaStream_t> job_streams;
     std::vector<cudaEvent_t> job_events;  // (ev0, ev1) per job
@@ -739,6 +743,19 @@ int resolve_geometry(lhmm_context* c, ProfileSlot& pf, const lhmm_scan_options* 
     return LHMM_OK;
 }
 
+// The saturation probe's sample: every `stride`-th slot of the length-sorted
+// tiles (so every length class is represented) whose sequence has at most
+// `max_len` residues (the sample scan's time is its longest row chain);
+// sel (per local sequence) must be zeroed first.
+__global__ void stride_select(const uint32_t* __restrict__ out_idx,
+                              const uint32_t* __restrict__ lens, uint64_t nslots,
+                              uint32_t stride, uint32_t max_len, uint8_t* __restrict__ sel) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nslots || i % stride != 0) return;
+    const uint32_t o = out_idx[i];
+    if (o != lhmm::kNoOutput && lens[i] <= max_len) sel[o] = 1u;
+}
+
 // global_out: outputs (and FP16X flags) are addressed by GLOBAL sequence
 // index -- d_raw / d_pass span the whole database, typically rank 0's
 // buffers mapped through CUDA IPC (the fused gather).
@@ -773,6 +790,50 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     if (variant == LHMM_VARIANT_FP16XRM && opt->alg == LHMM_SSV)
         variant = LHMM_VARIANT_FP16XM;  // its SSV twin
 
+    // First MSV scan of a profile over this database (auto policy, no
+    // saturation feedback yet): a 1-in-64 sample of the sequences of at most
+    // 512 residues, compacted on the device and scanned first, measures
+    // whether its scores saturate, so a non-saturating profile runs the
+    // relaxed FP16XRM/FP16XR forms from its first full scan on instead of the
+    // two-mode kernel (which would be picked blind).  Only for scans of at
+    // least 50 G cells, where the sample (~0.3-0.9 ms on B200) is small next
+    // to the scan; its time counts in the scan's device time.
+    double probe_ms = 0.0;
+    uint32_t probe_launches = 0;
+    if (view == nullptr && !c->in_probe && segments == 0 && !global_out && !c->host_resident &&
+        opt->alg == LHMM_MSV && opt->variant == LHMM_VARIANT_AUTO && opt->lanes == 0 &&
+        opt->rows == 0 && pf.sat_gen != c->db_gen && c->db.n_tiles >= 4096 &&
+        c->db.residues * uint64_t(pf.m) >= c->probe_min_cells &&
+        pf.m <= max_standard_capacity(LHMM_MSV) && c->probe_enabled) {
+        const uint64_t n = c->db.n_local;
+        if (!c->ev_probe[0]) {
+            CUDA_TRY(cudaEventCreate(&c->ev_probe[0]));
+            CUDA_TRY(cudaEventCreate(&c->ev_probe[1]));
+        }
+        if (int rc = c->d_flag.reserve(std::max<uint64_t>(n, 1))) return rc;
+        CUDA_TRY(cudaEventRecord(c->ev_probe[0], c->stream));
+        CUDA_TRY(cudaMemsetAsync(c->d_flag.ptr, 0, std::max<uint64_t>(n, 1), c->stream));
+        const uint64_t nslots = v.n_tiles * 32;
+        stride_select<<<unsigned((nslots + 255) / 256), 256, 0, c->stream>>>(
+            v.out_idx, v.lens, nslots, 64u, 512u, c->d_flag.ptr);
+        CUDA_TRY(cudaPeekAtLastError());
+        DbView sample;
+        uint32_t nsel = 0;
+        if (int rc = compact(c, c->resc, v, c->d_flag.ptr, &sample, &nsel)) return rc;
+        if (nsel > 0) {
+            lhmm_scan_stats ps{};
+            c->in_probe = true;
+            const int rc = do_scan(c, opt, d_raw, d_pass, &ps, 0, &sample);
+            c->in_probe = false;
+            if (rc) return rc;
+            probe_launches = ps.launches;
+        }
+        CUDA_TRY(cudaEventRecord(c->ev_probe[1], c->stream));
+        CUDA_TRY(cudaEventSynchronize(c->ev_probe[1]));
+        float pms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&pms, c->ev_probe[0], c->ev_probe[1]));
+        probe_ms = pms;
+    }
     uint32_t L = 0, H = 0;
     bool long_model = false;
     if (int rc = resolve_geometry(c, pf, opt, v.n_tiles, view == nullptr, variant, L, H,
@@ -863,7 +924,8 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     p.dbias = pf.q.dbias;
     p.tecjb = uint32_t(pf.q.tec) + uint32_t(pf.q.tjb);
     p.fault = opt->fault_injection ? 1u : 0u;
-    const bool track_sat = opt->alg == LHMM_MSV && view == nullptr;
+    // (the probe's sample scan records the saturation feedback too)
+    const bool track_sat = opt->alg == LHMM_MSV && (view == nullptr || c->in_probe);
     if (track_sat) p.sat_count = cnt32 + 1;
     const bool track_modes = opt->alg == LHMM_MSV && !long_model &&
                              (variant == LHMM_VARIANT_FP16X || variant == LHMM_VARIANT_FP16X_ALT ||
@@ -1198,15 +1260,15 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
     }
     if (st) {
         std::memset(st, 0, sizeof(*st));
-        st->device_ms = ms;
+        st->device_ms = ms + probe_ms;
         st->sequences = v.sequences;
         st->residues = v.residues;
         st->cells = v.residues * uint64_t(pf.m);
-        st->gcups = ms > 0 ? double(st->cells) / (ms * 1e-3) / 1e9 : 0.0;
+        st->gcups = st->device_ms > 0 ? double(st->cells) / (st->device_ms * 1e-3) / 1e9 : 0.0;
         st->lanes = L;
         st->rows = H;
         st->variant = uint32_t(variant);
-        st->launches = launches;
+        st->launches = launches + probe_launches;
         st->grid = uint32_t(cfg.grid);
         st->threads = uint32_t(cfg.threads);
         st->smem_bytes = uint32_t(cfg.smem);
@@ -1566,6 +1628,12 @@ int lhmm_context_create(int device, lhmm_context** out) {
         return set_error(LHMM_ERR_CUDA, "stream/event creation failed");
     }
     c->stream = c->own_stream;
+    {
+        const char* env = std::getenv("LHMM_SAT_PROBE");
+        c->probe_enabled = !env || std::atoi(env) != 0;
+        const char* mc = std::getenv("LHMM_SAT_PROBE_MIN_GCELLS");
+        if (mc) c->probe_min_cells = uint64_t(std::max(0.0, std::atof(mc)) * 1e9);
+    }
     // single-launch streamed scans need stream memory operations; probe once
     // (LHMM_STREAM_MEM_OPS=0 forces the per-piece launch path)
     {
@@ -1604,6 +1672,8 @@ int lhmm_context_destroy(lhmm_context* c) {
     c->d_out_gidx.release();
     c->d_jobs_out.release();
     c->d_jobs_aux.release();
+    for (auto& ev : c->ev_probe)
+        if (ev) cudaEventDestroy(ev);
     for (auto st : c->job_streams) cudaStreamDestroy(st);
     for (auto ev : c->job_events) cudaEventDestroy(ev);
     c->job_streams.clear();

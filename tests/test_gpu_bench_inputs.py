@@ -266,12 +266,17 @@ def test_relaxed_msv_matches_oracle(chk, L, variant):
                 assert rep.stats["recomputed"] >= int((want >= 256 - q.dbias).sum())
 
 
-def test_policy_picks_relaxed_msv_for_non_saturating_profiles(chk):
-    """The first MSV scan of a profile runs a two-mode kernel and counts
-    saturated scores; a non-saturating profile then runs the relaxed FP16XR
-    kernel, a saturating one stays on the two-mode kernels, and a profile
-    whose relaxed scan had to rescore many sequences (30% planted hits) falls
-    back to the exact FP16 kernel -- every scan exact."""
+@pytest.mark.parametrize("probe", ["1", "0"], ids=["probe", "no_probe"])
+def test_policy_picks_relaxed_msv_for_non_saturating_profiles(chk, probe, monkeypatch):
+    """The first MSV scan of a profile measures saturation -- on a 1-in-64
+    sample scanned ahead of it (the probe), or, with LHMM_SAT_PROBE=0, by
+    running a two-mode kernel and counting saturated scores; a non-saturating
+    profile then runs the relaxed FP16XRM / FP16XR kernels (from its first
+    scan on, with the probe), a saturating one stays on the two-mode kernels,
+    and a profile whose relaxed scan had to rescore many sequences (30%
+    planted hits) falls back to the exact FP16 kernel -- every scan exact."""
+    monkeypatch.setenv("LHMM_SAT_PROBE", probe)
+    monkeypatch.setenv("LHMM_SAT_PROBE_MIN_GCELLS", "0")  # (the probe's size gate: 50 G cells)
     rng = P.Rng(0x9E1)
     hmm = rng.random_profile(400)
     plain = rng.lognormal_records(140000, 60.0, 0.65, 2)
@@ -291,7 +296,10 @@ def test_policy_picks_relaxed_msv_for_non_saturating_profiles(chk):
                 rep = s.scan(P.ScanOptions(alg=P.Algorithm.Msv, threshold=0.022))
                 np.testing.assert_array_equal(rep.raw, want)
                 seen.append(rep.variant)
-            assert seen[0] in two_mode, seen
+            if kind == "two_mode" or probe == "0":
+                assert seen[0] in two_mode, seen
+            else:
+                assert seen[0] in relaxed, seen
             if kind == "two_mode":
                 assert all(v in two_mode for v in seen), seen
             elif kind == "relaxed":
