@@ -651,6 +651,7 @@ struct Fp16SatMixed {
     static constexpr int CPW = 2;
     static constexpr int kGroup = 5;
     static constexpr bool kSix = LHMM_XM_MSV_SIX != 0;  // xm_six_slots_msv
+    static constexpr bool kRelu5 = true;  // exact rows: relu form (relu_word5)
     static constexpr bool kMsv = true;
     static constexpr bool kRelaxed = false;
     static constexpr bool kTwoMode = true;
@@ -658,20 +659,31 @@ struct Fp16SatMixed {
     static constexpr uint32_t NEG = 0x00FF00FFu;  // byte 0 in both halves
     struct St {
         uint32_t B, nbase2, nd, tj2;  // B holds nB = 255 - B
+        uint32_t nBd;                 // nB (+) -dbias (relu form, unclamped)
     };
     __device__ static __forceinline__ void init(St& s, uint32_t base, const KParams& p) {
         s.nbase2 = (255u - base) * 0x00010001u;
         s.B = s.nbase2;
         s.nd = (0x8000u | p.dbias) * 0x00010001u;  // -dbias as a subnormal f16
         s.tj2 = p.tecjb * 0x00010001u;
+        s.nBd = as_u32(__hadd2(as_h2(s.B), as_h2(s.nd)));
     }
     __device__ static __forceinline__ uint32_t init_word(const St&) { return NEG; }
     template <bool LAZY = false>
     __device__ static __forceinline__ uint32_t inject(const St& s) { return LAZY ? s.B : NEG; }
+    // FORM & 8 (exact mode, relu_word5): min(n, nB) (+) -dbias as
+    // sat(nBd - sat(nB - n)) -- two FP16 ops instead of VIMNMX (ALU) + HADD2;
+    // exact in the subnormal domain (integer units below 2^10)
     template <bool LAZY = false, bool FPW = false, int FORM = 0>
     __device__ static __forceinline__ uint32_t cell(uint32_t x, uint32_t c, const St& s) {
-        const uint32_t m = LAZY ? x : __vminu2(x, s.B);
-        const uint32_t pp = as_u32(__hadd2_sat(as_h2(m), as_h2(s.nd)));
+        uint32_t pp;
+        if constexpr (!LAZY && (FORM & 8)) {
+            const uint32_t r = as_u32(__hsub2_sat(as_h2(s.B), as_h2(x)));
+            pp = as_u32(__hsub2_sat(as_h2(s.nBd), as_h2(r)));
+        } else {
+            const uint32_t m = LAZY ? x : __vminu2(x, s.B);
+            pp = as_u32(__hadd2_sat(as_h2(m), as_h2(s.nd)));
+        }
         return __viaddmin_s16x2(pp, c, LAZY ? s.B : NEG);
     }
     // the byte words of a slot: cost bytes (0,1) and (2,3), zero-extended
@@ -691,6 +703,7 @@ struct Fp16SatMixed {
     }
     __device__ static __forceinline__ void update_B(St& s, uint32_t e) {
         s.B = __viaddmin_s16x2(e, s.tj2, s.nbase2);  // nB = min(nbase, nE + tec + tjb)
+        s.nBd = as_u32(__hadd2(as_h2(s.B), as_h2(s.nd)));
     }
     __device__ static __forceinline__ bool saturated(uint32_t e) { return (e & 0xffffu) == 0u; }
     template <int H>
@@ -1013,6 +1026,30 @@ __host__ __device__ constexpr bool relu_word(int k) {
     }
 }
 
+// Whether word k of a five-row slot takes the relu form in the negated
+// two-mode exact mode (Fp16SatMixed; bit k of LHMM_RELU5_MASK).  Off: words
+// 1 and 3 measured +1.3% at L16 H63 but -8.3% at L8 H53 and flat on C1
+// (profiles/r2_ab_relu5.txt).
+#ifndef LHMM_RELU5_MASK
+#define LHMM_RELU5_MASK 0
+#endif
+template <class V, class = void>
+struct has_relu5 {
+    static constexpr bool value = false;
+};
+template <class V>
+struct has_relu5<V, decltype(void(V::kRelu5))> {
+    static constexpr bool value = V::kRelu5;
+};
+template <class V, bool LAZY>
+__host__ __device__ constexpr bool relu_word5(int k) {
+    if constexpr (has_relu5<V>::value && !LAZY) {
+        return ((LHMM_RELU5_MASK >> k) & 1) != 0;
+    } else {
+        return false;
+    }
+}
+
 // One chunk of RPI residue rows (fully unrolled).  Returns true when the
 // sub-batch's rows ended inside the chunk.  LAZY (two-mode MSV only): the
 // cells hold max(v, B) and B is constant -- see Fp16Sat.
@@ -1230,9 +1267,13 @@ __device__ __forceinline__ bool run_chunk(uint32_t (&g)[H], uint32_t& e0, uint32
                         const int sl = ((h - 1 - r) % H + H) % H;
                         const uint32_t in = h == 0 ? V::shift(g[sl], up) : g[sl];
                         if (k >= 3)
-                            g[sl] = V::template cell<LAZY, false, 3>(in, cw[k], st);
+                            g[sl] = relu_word5<V, LAZY>(k)
+                                        ? V::template cell<LAZY, false, 3 | 8>(in, cw[k], st)
+                                        : V::template cell<LAZY, false, 3>(in, cw[k], st);
                         else
-                            g[sl] = V::template cell<LAZY, false, 0>(in, cw[k], st);
+                            g[sl] = relu_word5<V, LAZY>(k)
+                                        ? V::template cell<LAZY, false, 8>(in, cw[k], st)
+                                        : V::template cell<LAZY, false, 0>(in, cw[k], st);
                     }
                     if constexpr (!V::kMsv) {
                     // E: two folds per group, spread over the four maxima;

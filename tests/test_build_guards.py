@@ -56,3 +56,28 @@ def test_relu_form_of_the_exact_step_is_exact():
         bd = (Bv + d).astype(np.float16).astype(np.float32)  # HADD2, no clamp
         new = sat(r + bd)
         assert np.array_equal(ref.view(np.uint16), new.view(np.uint16)), dbias
+
+
+def test_relu_form_of_the_negated_exact_step_is_exact():
+    """The negated two-mode exact step's relu form (Fp16SatMixed, FORM & 8):
+    sat(min(n, nB) - d) == sat((nB - d) - sat(nB - n)) in the f16 subnormal
+    domain (byte units of 2^-24), for every cell n, every nB and every dbias d
+    -- exhaustive, 256 x 256 x 256."""
+    import numpy as np
+    unit = np.float32(2.0 ** -24)
+    n = (np.arange(256, dtype=np.float32) * unit).astype(np.float16)
+    N, NB = n[:, None].astype(np.float32), n[None, :].astype(np.float32)
+
+    def f16(a):  # one f16 op: exact f32 result, one rounding
+        return a.astype(np.float16)
+
+    def sat(a):
+        return np.clip(f16(a), np.float16(0), np.float16(1))
+
+    r = sat(NB - N).astype(np.float32)
+    for d in range(256):
+        dd = np.float32(np.float16(d * 2.0 ** -24))
+        ref = sat(np.minimum(N, NB) - dd)
+        nbd = f16(NB - dd).astype(np.float32)  # HADD2 (no clamp): may be negative
+        new = sat(nbd - r)
+        assert np.array_equal(ref.view(np.uint16), new.view(np.uint16)), d
