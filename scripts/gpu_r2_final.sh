@@ -12,7 +12,7 @@ LHMM_DROPIN_TIMING=1 ./oracle/_ref/dropin_bench 1000000 3 > gpurun_out/fin_dropi
 ./oracle/_ref/acceptance_b200 > gpurun_out/fin_acc_b200.txt 2>&1
 LHMM_STREAM_MEM_OPS=0 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/fin_launches.csv python bench.py --steps 2 --warmup 1 --legs none > gpurun_out/fin_ncu_bench.log 2>&1
-for a in "c2dom --m 1000 --alg ssv" "c3 --m 2405 --alg msv" "m400msv --m 400 --alg msv"; do
+for a in "c2dom --m 1000 --alg ssv" "c3 --m 2405 --alg msv"; do
   set -- $a; name=$1; shift
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s 2 -c 1 \
       -o gpurun_out/fin_prof_$name python scripts/one_scan.py "$@" > gpurun_out/fin_ncu_$name.log 2>&1
