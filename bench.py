@@ -635,7 +635,11 @@ def main():  # noqa: C901
                              variant=variant, lanes=args.lanes, rows=args.rows,
                              threshold=THRESHOLD)
 
-    verifier = Verifier(res, off, args.verify_sample, host_threads) if "verify" in legs else None
+    # (N > 1: each rank checks its share of the sample, so the union stays
+    # --verify-sample sequences per scan while every rank's host threads --
+    # cpu_count / N -- finish in about the N = 1 time)
+    per_rank_sample = max(2500, args.verify_sample // world) if world > 1 else args.verify_sample
+    verifier = Verifier(res, off, per_rank_sample, host_threads) if "verify" in legs else None
 
     scans = [(m, a) for m in models_m for a in algs]
     for m, _ in scans:
