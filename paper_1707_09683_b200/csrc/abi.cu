@@ -756,6 +756,20 @@ __global__ void stride_select(const uint32_t* __restrict__ out_idx,
     if (o != lhmm::kNoOutput && lens[i] <= max_len) sel[o] = 1u;
 }
 
+// Cumulative byte goal of piece k of a streamed upload in `segments`
+// pieces.  With LHMM_PIECE_RAMP the first three pieces are 1/8, 1/4 and 1/2
+// of the others, so the kernel (which claims the longest tiles -- the most
+// work per byte -- first) starts after a small first copy.
+#ifndef LHMM_PIECE_RAMP
+#define LHMM_PIECE_RAMP 1
+#endif
+uint64_t piece_goal(uint64_t bytes, int k, int segments) {
+    if (!LHMM_PIECE_RAMP || segments <= 4) return bytes * uint64_t(k + 1) / uint64_t(segments);
+    const double total = double(segments) - 3.0 + 0.875;
+    const double w = k >= 2 ? double(k + 1) - 3.0 + 0.875 : (k == 0 ? 0.125 : 0.375);
+    return uint64_t(double(bytes) * (w / total));
+}
+
 // global_out: outputs (and FP16X flags) are addressed by GLOBAL sequence
 // index -- d_raw / d_pass span the whole database, typically rank 0's
 // buffers mapped through CUDA IPC (the fused gather).
@@ -1067,7 +1081,7 @@ int do_scan(lhmm_context* c, const lhmm_scan_options* opt, uint8_t* d_raw, uint8
         if (!c->ev_side) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
         std::vector<uint32_t> ends;
         for (int k = 0, t0 = 0; k < segments && uint64_t(t0) < T; ++k) {
-            const uint64_t goal = db.data_bytes * uint64_t(k + 1) / uint64_t(segments);
+            const uint64_t goal = piece_goal(db.data_bytes, k, segments);
             uint64_t t1 = k + 1 == segments ? T
                                             : uint64_t(std::lower_bound(db.tile_off.begin(),
                                                                         db.tile_off.end(), goal) -
