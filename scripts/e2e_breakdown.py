@@ -1,9 +1,12 @@
 #!/usr/bin/env python
-"""Where the end-to-end time of a bench step goes (C2 by default): per model,
-the resident device scan (device outputs), the resident scan with host
-outputs, and the streamed scan (H2D under the kernel), each timed with a
-host clock around a synchronised call and with the library's device time."""
+"""Where the end-to-end time of a C2 step goes: per model (SSV, M = 1000 /
+400 / 48 over the 1M Swiss-Prot-like set), the resident scan into device
+buffers, the resident scan with page-locked host outputs, and the streamed
+scan (H2D of the packed image under the kernel), each as the library's
+device time and a host clock around the synchronous call (median of 10)."""
+import json
 import os
+import statistics
 import sys
 import time
 
@@ -11,50 +14,42 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import bench  # noqa: E402
 import paper_1707_09683_b200 as P  # noqa: E402
 
 
-def main():
-    wl = bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
-    alg, models_m, gen = wl[1], wl[2], wl[4]
-    q = P.QuantParams()
-    db = bench.make_db(P, gen, 1_000_000)
-    models = bench.make_models(P, models_m, q)
-    s = P.Scanner(0)
-    s.set_stream(torch.cuda.current_stream().cuda_stream)
-    s.set_database(db)
-    pids = [s.add_profile(c, q, h.lambda_, h.tau) for h, c in models]
-    n = db.count
-    raw = torch.empty(n, dtype=torch.uint8, device="cuda")
-    pas = torch.empty(n, dtype=torch.uint8, device="cuda")
-    pinned = (torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy(),
-              torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy())
-    a = P.Algorithm.Msv if alg == "msv" else P.Algorithm.Ssv
-    opt = P.ScanOptions(alg=a, threshold=0.022)
-
-    def timed(fn, reps=5):
-        for _ in range(2):
-            fn()
+def timed(fn, reps=10):
+    dev, wall = [], []
+    for _ in range(reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        dev = 0.0
-        for _ in range(reps):
-            st = fn()
-            dev += st if isinstance(st, float) else 0.0
-        torch.cuda.synchronize()
-        return (time.perf_counter() - t0) / reps * 1e3, dev / reps
+        r = fn()
+        wall.append((time.perf_counter() - t0) * 1e3)
+        st = r if isinstance(r, dict) else r.stats  # (scan_device returns the stats dict)
+        dev.append(st["device_ms"])
+    return round(statistics.median(dev), 3), round(statistics.median(wall), 3)
 
-    for pid, (h, _) in zip(pids, models):
-        s.select_profile(pid)
-        w1, d1 = timed(lambda: s.scan_device(opt, raw.data_ptr(), pas.data_ptr())["device_ms"])
-        w2, d2 = timed(lambda: s.scan(opt).elapsed_seconds * 1e3)
-        w3, d3 = timed(lambda: s.scan_streamed(opt, 64).elapsed_seconds * 1e3)
-        w4, d4 = timed(lambda: s.scan(opt, out=pinned).elapsed_seconds * 1e3)
-        w5, d5 = timed(lambda: s.scan_streamed(opt, 64, out=pinned).elapsed_seconds * 1e3)
-        print(f"M={h.length}: device-out wall {w1:.3f} ms (dev {d1:.3f}); host-out wall {w2:.3f} "
-              f"(dev {d2:.3f}); streamed wall {w3:.3f} (dev {d3:.3f}); pinned host-out wall "
-              f"{w4:.3f}; pinned streamed wall {w5:.3f}", flush=True)
+
+def main():
+    db = P.Rng(0x5EED).lognormal_records(1_000_000, 290, 0.65, 2)
+    q = P.QuantParams()
+    with P.Scanner(0) as s:
+        s.set_database(db)
+        n = s.n_local
+        raw = torch.empty(n, dtype=torch.uint8, device="cuda")
+        pas = torch.empty(n, dtype=torch.uint8, device="cuda")
+        host = (torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy(),
+                torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy())
+        o = P.ScanOptions(alg=P.Algorithm.Ssv, threshold=0.022)
+        for m in (1000, 400, 48):
+            hmm = P.Rng(7000 + m).random_profile(m)
+            s.set_profile(P.quantize_emissions(hmm, q), q, hmm.lambda_, hmm.tau)
+            for _ in range(2):
+                s.scan(o)
+            row = {"M": m,
+                   "device_outputs": timed(lambda: s.scan_device(o, raw.data_ptr(), pas.data_ptr())),
+                   "host_outputs": timed(lambda: s.scan(o, out=host)),
+                   "streamed": timed(lambda: s.scan_streamed(o, 64, out=host))}
+            print(json.dumps(row), flush=True)
 
 
 if __name__ == "__main__":
